@@ -1,0 +1,203 @@
+"""CPU oracle training steps for the small CNN (C1) and CIFAR ResNet-18 (C2). TEST INFRASTRUCTURE ONLY.
+
+Parameters are declared in the same order, with the same names and seed
+draws, as paper_2409_11600_b200.models (one ``default_rng(seed).integers(0,
+2**31-1)`` per random tensor, builtins.py:89-91), so both sides start from
+identical weights. Arithmetic is float64 (ref_ops / restated). With
+``bf16=True`` values are rounded to bfloat16 at the points where the device
+stores bf16 (activations, their gradients, tensor-core operands), which is
+what "the oracle consumes operands rounded to the kernel's input precision"
+means for a whole step (SURVEY.md §7 hard part 5).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import ref_ops as R
+from . import restated as X
+
+
+class _Decl:
+    def __init__(self, seed):
+        self.rng = np.random.default_rng(seed)
+        self.params: dict[str, np.ndarray] = {}
+        self.order: list[str] = []
+        self.n = 0
+
+    def _name(self, key):
+        self.order.append(key)
+        self.n += 1
+        return key
+
+    def conv(self, key, cout, r, s, cin):
+        seed = int(self.rng.integers(0, 2**31 - 1))
+        self.params[self._name(key)] = X.xavier_conv(cout, r, s, cin, seed)
+
+    def bn(self, key, c):
+        gb = np.zeros((2, c), np.float32)
+        gb[0] = 1.0
+        self.params[self._name(key)] = gb
+
+    def linear(self, key, rows, cols):
+        seed = int(self.rng.integers(0, 2**31 - 1))
+        self.params[self._name(key)] = R.xavier_uniform(rows, cols, seed)
+
+    def zeros(self, key, *dims):
+        self.params[self._name(key)] = np.zeros(dims, np.float32)
+
+
+class _Opt:
+    """SGD-momentum state per parameter (nn.py:91-99)."""
+
+    def __init__(self, params):
+        self.vel = {k: np.zeros_like(v) for k, v in params.items()}
+
+    def sgd(self, params, grads, lr, momentum):
+        for k in params:
+            params[k], self.vel[k] = R.sgd_update(params[k], grads[k].astype(np.float32), self.vel[k], lr, momentum)
+
+
+class SmallCNNOracle:
+    def __init__(self, seed=0, hw=32, classes=10):
+        d = _Decl(seed)
+        d.conv("w1", 16, 3, 3, 3)
+        d.zeros("b1", 16)
+        d.conv("w2", 32, 3, 3, 16)
+        d.zeros("b2", 32)
+        d.linear("fc_w", classes, 32 * (hw // 2) ** 2)
+        d.zeros("fc_b", classes)
+        self.params = d.params
+        self.opt = _Opt(self.params)
+
+    def loss_and_grads(self, x_nchw, y, bf16=False):
+        q = X.round_bf16 if bf16 else (lambda a: np.asarray(a, np.float64))
+        p = self.params
+        x = q(np.transpose(x_nchw, (0, 2, 3, 1)))
+        w1, w2 = q(p["w1"]), q(p["w2"])
+        c1 = q(X.conv2d_fwd(x, w1, 1, 1))
+        a1 = q(c1 + p["b1"])
+        h1 = np.maximum(a1, 0)
+        c2 = q(X.conv2d_fwd(h1, w2, 2, 1))
+        a2 = q(c2 + p["b2"])
+        h2 = np.maximum(a2, 0)
+        f = h2.reshape(h2.shape[0], -1)
+        fcw = q(p["fc_w"]) if bf16 else p["fc_w"].astype(np.float64)
+        logits = (f @ fcw.T).astype(np.float32) + p["fc_b"]
+        loss, probs = R.cross_entropy(logits, y)
+        g = R.cross_entropy_grad(probs, y).astype(np.float64)
+        grads = {"fc_b": g.sum(axis=0)}
+        grads["fc_w"] = (q(g) if bf16 else g).T @ f
+        df = q(g @ p["fc_w"].astype(np.float64))
+        dh2 = df.reshape(h2.shape)
+        da2 = dh2 * (a2 > 0)
+        grads["b2"] = da2.reshape(-1, da2.shape[-1]).sum(axis=0)
+        grads["w2"] = X.conv2d_wgrad(h1, da2, p["w2"].shape, 2, 1)
+        dh1 = q(X.conv2d_dgrad(da2, w2, h1.shape, 2, 1))
+        da1 = dh1 * (a1 > 0)
+        grads["b1"] = da1.reshape(-1, da1.shape[-1]).sum(axis=0)
+        grads["w1"] = X.conv2d_wgrad(x, da1, p["w1"].shape, 1, 1)
+        return loss, grads, logits
+
+    def train_step(self, x_nchw, y, lr=0.01, momentum=0.9, bf16=False):
+        loss, grads, _ = self.loss_and_grads(x_nchw, y, bf16=bf16)
+        self.opt.sgd(self.params, grads, lr, momentum)
+        return loss
+
+
+class ResNet18Oracle:
+    """CIFAR ResNet-18 training step (same declaration as paper_2409_11600_b200.models.ResNet18)."""
+
+    STAGES = ((64, 1), (128, 2), (256, 2), (512, 2))
+
+    def __init__(self, seed=0, classes=10):
+        d = _Decl(seed)
+        d.conv("stem_w", 64, 3, 3, 3)
+        d.bn("stem_bn", 64)
+        self.blocks = []
+        cin = 64
+        i = 0
+        for cout, stride in self.STAGES:
+            for b in range(2):
+                st = stride if b == 0 else 1
+                pre = f"b{i}_"
+                d.conv(pre + "w1", cout, 3, 3, cin)
+                d.bn(pre + "bn1", cout)
+                d.conv(pre + "w2", cout, 3, 3, cout)
+                d.bn(pre + "bn2", cout)
+                proj = st != 1 or cin != cout
+                if proj:
+                    d.conv(pre + "wsc", cout, 1, 1, cin)
+                    d.bn(pre + "bnsc", cout)
+                self.blocks.append((pre, st, proj))
+                cin = cout
+                i += 1
+        d.linear("fc_w", classes, 512)
+        d.zeros("fc_b", classes)
+        self.params = d.params
+        self.order = d.order
+        self.opt = _Opt(self.params)
+
+    def loss_and_grads(self, x_nchw, y, bf16=False):
+        q = X.round_bf16 if bf16 else (lambda a: np.asarray(a, np.float64))
+        p = self.params
+        W = {k: q(v) for k, v in p.items() if v.ndim == 4}
+        caches = []
+
+        def conv_bn(h, wk, bnk, st, pad, relu, res=None):
+            c = q(X.conv2d_fwd(h, W[wk], st, pad))
+            y_, cache = X.batchnorm_fwd(c, p[bnk][0], p[bnk][1], relu=relu, residual=res)
+            y_ = q(y_)
+            return c, y_, cache
+
+        x = q(np.transpose(x_nchw, (0, 2, 3, 1)))
+        c0, h, cache0 = conv_bn(x, "stem_w", "stem_bn", 1, 1, True)
+        stem = (x, c0, h, cache0)
+        for pre, st, proj in self.blocks:
+            hin = h
+            c1, o, k1 = conv_bn(hin, pre + "w1", pre + "bn1", st, 1, True)
+            if proj:
+                cs, sc, ks = conv_bn(hin, pre + "wsc", pre + "bnsc", st, 0, False)
+            else:
+                cs, sc, ks = None, hin, None
+            c2, h, k2 = conv_bn(o, pre + "w2", pre + "bn2", 1, 1, True, res=sc)
+            caches.append((pre, st, proj, hin, c1, o, k1, cs, sc, ks, c2, h, k2))
+        feat = X.avgpool_fwd(h).astype(np.float32)
+        fcw = p["fc_w"]
+        logits = R.matmul_t(feat, fcw) + p["fc_b"]
+        loss, probs = R.cross_entropy(logits, y)
+        g = R.cross_entropy_grad(probs, y)
+        grads = {"fc_b": g.astype(np.float64).sum(axis=0), "fc_w": R.plain_matmul(g.T, feat).astype(np.float64)}
+        dfeat = R.plain_matmul(g, fcw)
+        dh = q(X.avgpool_bwd(dfeat, h.shape))
+        for (pre, st, proj, hin, c1, o, k1, cs, sc, ks, c2, hout, k2) in reversed(caches):
+            dc2, dg, db, dres = X.batchnorm_bwd(dh, k2, y_out=hout, relu=True)
+            dc2, dres = q(dc2), q(dres)
+            grads[pre + "bn2"] = np.stack([dg, db])
+            grads[pre + "w2"] = X.conv2d_wgrad(o, dc2, W[pre + "w2"].shape, 1, 1)
+            do = q(X.conv2d_dgrad(dc2, W[pre + "w2"], o.shape, 1, 1))
+            dc1, dg, db, _ = X.batchnorm_bwd(do, k1, y_out=o, relu=True)
+            dc1 = q(dc1)
+            grads[pre + "bn1"] = np.stack([dg, db])
+            grads[pre + "w1"] = X.conv2d_wgrad(hin, dc1, W[pre + "w1"].shape, st, 1)
+            dhin = q(X.conv2d_dgrad(dc1, W[pre + "w1"], hin.shape, st, 1))
+            if proj:
+                dcs, dg, db, _ = X.batchnorm_bwd(dres, ks, relu=False)
+                dcs = q(dcs)
+                grads[pre + "bnsc"] = np.stack([dg, db])
+                grads[pre + "wsc"] = X.conv2d_wgrad(hin, dcs, W[pre + "wsc"].shape, st, 0)
+                dhin = q(dhin + q(X.conv2d_dgrad(dcs, W[pre + "wsc"], hin.shape, st, 0)))
+            else:
+                dhin = q(dhin + dres)
+            dh = dhin
+        x, c0, h0, cache0 = stem
+        dc0, dg, db, _ = X.batchnorm_bwd(dh, cache0, y_out=h0, relu=True)
+        dc0 = q(dc0)
+        grads["stem_bn"] = np.stack([dg, db])
+        grads["stem_w"] = X.conv2d_wgrad(x, dc0, W["stem_w"].shape, 1, 1)
+        return loss, grads, logits
+
+    def train_step(self, x_nchw, y, lr=0.1, momentum=0.9, bf16=False):
+        loss, grads, _ = self.loss_and_grads(x_nchw, y, bf16=bf16)
+        self.opt.sgd(self.params, grads, lr, momentum)
+        return loss

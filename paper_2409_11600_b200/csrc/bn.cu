@@ -1,0 +1,305 @@
+// BatchNorm (training mode) fused with residual add and ReLU (K7).
+//
+// Absent from the reference; restated in oracle/restated.py
+// (batchnorm_fwd / batchnorm_bwd) with the reference's conventions: float32
+// storage, float64 accumulation of the statistics, biased batch variance.
+//   fwd: y = relu( (x - mean) * invstd * gamma + beta  [+ residual] )
+//   bwd: dz = dy * [y > 0];  dbeta = sum dz;  dgamma = sum dz * xhat
+//        dx = gamma*invstd*(dz - dbeta/M - xhat*dgamma/M);  dres = dz
+// x / y / dy / dx / residual are NHWC bf16 viewed as [rows, C]; gamma_beta is
+// the fp32 parameter [2, C]. Each pass is a vectorised (8 x bf16) sweep;
+// per-block channel partials go to a workspace and are folded in float64 in a
+// fixed order (deterministic, no atomics).
+#include "common.cuh"
+#include "../../include/nskb.h"
+
+namespace {
+
+constexpr int BT = 256;      // threads per block
+constexpr int MAXBLK = 592;  // 4 * 148
+
+struct Pack8 {
+  float v[8];
+};
+
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* f) {
+  uint4 u = __ldg((const uint4*)p);
+  const __nv_bfloat162* h = (const __nv_bfloat162*)&u;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float* f) {
+  uint4 u;
+  u.x = pack_bf16x2(f[0], f[1]);
+  u.y = pack_bf16x2(f[2], f[3]);
+  u.z = pack_bf16x2(f[4], f[5]);
+  u.w = pack_bf16x2(f[6], f[7]);
+  *(uint4*)p = u;
+}
+
+// Block-level channel reduction of two per-thread 8-vectors, written as partials[blk][2][C].
+__device__ void block_reduce_store(float* s1, float* s2, int C, float* part) {
+  extern __shared__ float red[];  // [BT/CV][C] x 2
+  const int CV = C / 8;
+  const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
+  float* r1 = red;
+  float* r2 = red + RPB * C;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    r1[ro * C + cv * 8 + j] = s1[j];
+    r2[ro * C + cv * 8 + j] = s2[j];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += BT) {
+    float a = 0.f, b = 0.f;
+    for (int r = 0; r < RPB; ++r) {
+      a += r1[r * C + c];
+      b += r2[r * C + c];
+    }
+    part[(size_t)blockIdx.x * 2 * C + c] = a;
+    part[(size_t)blockIdx.x * 2 * C + C + c] = b;
+  }
+}
+
+// pass 1 of fwd: sum x and sum x^2 per channel
+__global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __restrict__ x, uint64_t rows, int C,
+                                                      float* part) {
+  const int CV = C / 8;
+  const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
+  float s1[8] = {0}, s2[8] = {0};
+  for (uint64_t r = (uint64_t)blockIdx.x * RPB + ro; r < rows; r += (uint64_t)gridDim.x * RPB) {
+    float f[8];
+    ld8(x + r * C + cv * 8, f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s1[j] += f[j];
+      s2[j] += f[j] * f[j];
+    }
+  }
+  block_reduce_store(s1, s2, C, part);
+}
+
+constexpr int FT = 128;  // finalize threads: one block per channel folds the block partials
+
+// float64 fold of the two partial rows of channel c over nblk blocks (fixed order -> deterministic)
+__device__ void fold_partials(const float* part, int nblk, int C, int c, double* a_out, double* b_out) {
+  __shared__ double ra[FT / 32], rb[FT / 32];
+  double a = 0.0, b = 0.0;
+  for (int k = threadIdx.x; k < nblk; k += FT) {
+    a += (double)part[(size_t)k * 2 * C + c];
+    b += (double)part[(size_t)k * 2 * C + C + c];
+  }
+  a = warp_sum_d(a);
+  b = warp_sum_d(b);
+  if ((threadIdx.x & 31) == 0) {
+    ra[threadIdx.x >> 5] = a;
+    rb[threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = b = 0.0;
+    for (int i = 0; i < FT / 32; ++i) {
+      a += ra[i];
+      b += rb[i];
+    }
+    *a_out = a;
+    *b_out = b;
+  }
+}
+
+// fold partials (float64) -> mean, invstd and the fused affine (scale, shift); grid = C blocks
+__global__ void __launch_bounds__(FT) bn_fwd_finalize(const float* part, int nblk, uint64_t rows, int C, float eps,
+                                                      const float* gb, float* mean, float* invstd, float* scale,
+                                                      float* shift) {
+  const int c = blockIdx.x;
+  double a, b;
+  fold_partials(part, nblk, C, c, &a, &b);
+  if (threadIdx.x == 0) {
+    double mu = a / (double)rows;
+    double var = b / (double)rows - mu * mu;
+    if (var < 0.0) var = 0.0;
+    double is = 1.0 / sqrt(var + (double)eps);
+    mean[c] = (float)mu;
+    invstd[c] = (float)is;
+    double g = gb[c], be = gb[C + c];
+    scale[c] = (float)(g * is);
+    shift[c] = (float)(be - mu * g * is);
+  }
+}
+
+__global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __restrict__ x,
+                                                      const __nv_bfloat16* __restrict__ res,
+                                                      const float* __restrict__ scale, const float* __restrict__ shift,
+                                                      __nv_bfloat16* __restrict__ y, uint64_t rows, int C, int relu) {
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  const int CV = C / 8;
+  for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
+    const int c0 = (int)(i % CV) * 8;
+    float f[8], r[8];
+    ld8(x + i * 8, f);
+    if (res) ld8(res + i * 8, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = f[j] * scale[c0 + j] + shift[c0 + j];
+      if (res) v += r[j];
+      if (relu) v = v > 0.f ? v : 0.f;
+      f[j] = v;
+    }
+    st8(y + i * 8, f);
+  }
+}
+
+// bwd pass 1: sum dz and sum dz*x per channel, dz = dy * [y > 0] (relu) or dy
+__global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                           const __nv_bfloat16* __restrict__ x,
+                                                           const __nv_bfloat16* __restrict__ y, uint64_t rows, int C,
+                                                           float* part) {
+  const int CV = C / 8;
+  const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
+  float s1[8] = {0}, s2[8] = {0};
+  for (uint64_t r = (uint64_t)blockIdx.x * RPB + ro; r < rows; r += (uint64_t)gridDim.x * RPB) {
+    const uint64_t off = r * C + cv * 8;
+    float g[8], xv[8];
+    ld8(dy + off, g);
+    ld8(x + off, xv);
+    if (y) {
+      float yv[8];
+      ld8(y + off, yv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = yv[j] > 0.f ? g[j] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s1[j] += g[j];
+      s2[j] += g[j] * xv[j];
+    }
+  }
+  block_reduce_store(s1, s2, C, part);
+}
+
+// dgamma/dbeta and dx = A*dz + B*x + Cc per channel
+__global__ void __launch_bounds__(FT) bn_bwd_finalize(const float* part, int nblk, uint64_t rows, int C,
+                                                      const float* gb, const float* mean, const float* invstd,
+                                                      float* dgb, float beta_acc, float* coef) {
+  const int c = blockIdx.x;
+  double sdz, sdzx;
+  fold_partials(part, nblk, C, c, &sdz, &sdzx);
+  if (threadIdx.x == 0) {
+    const double mu = mean[c], is = invstd[c], g = gb[c], M = (double)rows;
+    const double dbeta = sdz;
+    const double dgamma = is * (sdzx - mu * sdz);
+    if (beta_acc != 0.f) {
+      dgb[c] = (float)(dgamma + beta_acc * dgb[c]);
+      dgb[C + c] = (float)(dbeta + beta_acc * dgb[C + c]);
+    } else {
+      dgb[c] = (float)dgamma;
+      dgb[C + c] = (float)dbeta;
+    }
+    const double A = g * is;
+    const double B = -g * is * is * dgamma / M;
+    const double Cc = -g * is * dbeta / M + g * is * is * mu * dgamma / M;
+    coef[c] = (float)A;
+    coef[C + c] = (float)B;
+    coef[2 * C + c] = (float)Cc;
+  }
+}
+
+__global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy,
+                                                          const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ y,
+                                                          const float* __restrict__ coef,
+                                                          __nv_bfloat16* __restrict__ dx,
+                                                          __nv_bfloat16* __restrict__ dres, uint64_t rows, int C) {
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  const int CV = C / 8;
+  for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
+    const int c0 = (int)(i % CV) * 8;
+    float g[8], xv[8];
+    ld8(dy + i * 8, g);
+    ld8(x + i * 8, xv);
+    if (y) {
+      float yv[8];
+      ld8(y + i * 8, yv);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = yv[j] > 0.f ? g[j] : 0.f;
+    }
+    if (dres) st8(dres + i * 8, g);
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = coef[c0 + j] * g[j] + coef[C + c0 + j] * xv[j] + coef[2 * C + c0 + j];
+    st8(dx + i * 8, o);
+  }
+}
+
+int nblocks(uint64_t rows, int C) {
+  const int RPB = BT / (C / 8);
+  uint64_t want = (rows + RPB * 8 - 1) / (RPB * 8);  // >= 8 rows per thread
+  if (want > MAXBLK) want = MAXBLK;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+int check(uint64_t rows, int C, const void* a, const void* b) {
+  if (C % 8 || C < 8 || C > 2048 || (BT % (C / 8)))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "batchnorm: C must be a multiple of 8 dividing 2048");
+  if (((uintptr_t)a & 15) || (b && ((uintptr_t)b & 15)))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "batchnorm: buffers must be 16-byte aligned");
+  return NSK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint64_t nsk_bn_workspace(uint64_t rows, int C) {
+  return (uint64_t)MAXBLK * 2 * C * sizeof(float) + 4 * (uint64_t)C * sizeof(float);
+}
+
+int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
+               float eps, int relu, const void* residual, float* ws, void* stream) {
+  int rc = check(rows, C, x, residual);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = nblocks(rows, C);
+  const int RPB = BT / (C / 8);
+  const size_t smem = 2 * (size_t)RPB * C * sizeof(float);
+  float* part = ws;
+  float* scale = ws + (size_t)MAXBLK * 2 * C;
+  float* shift = scale + C;
+  bn_stats_kernel<<<nb, BT, smem, st>>>((const __nv_bfloat16*)x, rows, C, part);
+  bn_fwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
+                                                        shift, (__nv_bfloat16*)y, rows, C, relu);
+  NSK_LAUNCH_CHECK("bn_fwd");
+  return NSK_OK;
+}
+
+int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* gamma_beta, const float* mean,
+               const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
+               float* ws, void* stream) {
+  int rc = check(rows, C, dy, x);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = nblocks(rows, C);
+  const int RPB = BT / (C / 8);
+  const size_t smem = 2 * (size_t)RPB * C * sizeof(float);
+  float* part = ws;
+  float* coef = ws + (size_t)MAXBLK * 2 * C;  // 3*C floats (workspace reserves 4*C)
+  bn_bwd_reduce_kernel<<<nb, BT, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                                             (const __nv_bfloat16*)y_relu, rows, C, part);
+  bn_bwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc,
+                                                   coef);
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  bn_bwd_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)y_relu, coef, (__nv_bfloat16*)dx,
+      (__nv_bfloat16*)dres, rows, C);
+  NSK_LAUNCH_CHECK("bn_bwd");
+  return NSK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// Embedding gather / scatter-add (K15).
+//
+// Reference: the GRU input path is onehot(tokens) @ E (tensor.py:299-317 then
+// matmul_t tensor.py:213-229, the substitution PAPER.md:173). The forward of
+// onehot@E in float64 is an exact copy of row E[tok] (a one-term sum), so the
+// gather is bit-identical to it; the backward dE = onehot^T @ dx becomes a
+// scatter-add of dx rows into dE (fp32 atomics).
+#include "common.cuh"
+#include "../../include/nskb.h"
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void stv(T* p, float v);
+template <>
+__device__ __forceinline__ void stv<float>(float* p, float v) { *p = v; }
+template <>
+__device__ __forceinline__ void stv<__nv_bfloat16>(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+template <typename T>
+__device__ __forceinline__ float ldv(const T* p);
+template <>
+__device__ __forceinline__ float ldv<float>(const float* p) { return *p; }
+template <>
+__device__ __forceinline__ float ldv<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+
+template <typename T>
+__global__ void embed_fwd_kernel(const float* __restrict__ table, const int32_t* __restrict__ tok, uint64_t n, int E,
+                                 int V, T* __restrict__ out, int* err) {
+  const uint64_t total = n * (uint64_t)E;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = i / E;
+    int e = (int)(i - r * E);
+    int t = tok[r];
+    if (t < 0 || t >= V) {
+      if (e == 0 && err) atomicMin(err, (int)r);
+      stv<T>(out + i, 0.f);
+    } else {
+      stv<T>(out + i, table[(uint64_t)t * E + e]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void embed_bwd_kernel(const T* __restrict__ dout, const int32_t* __restrict__ tok, uint64_t n, int E,
+                                 float* dtable) {
+  const uint64_t total = n * (uint64_t)E;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t r = i / E;
+    int e = (int)(i - r * E);
+    atomicAdd(dtable + (uint64_t)tok[r] * E + e, ldv<T>(dout + i));
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsk_embedding_fwd(const float* table, const int32_t* tokens, uint64_t n, int E, int dtype_out, void* out, int V,
+                      int* err_flag, void* stream) {
+  uint64_t total = n * (uint64_t)E;
+  if (!total) return NSK_OK;
+  if (dtype_out == NSK_DTYPE_F32)
+    embed_fwd_kernel<float><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(table, tokens, n, E, V,
+                                                                                          (float*)out, err_flag);
+  else
+    embed_fwd_kernel<__nv_bfloat16><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+        table, tokens, n, E, V, (__nv_bfloat16*)out, err_flag);
+  NSK_LAUNCH_CHECK("embedding_fwd");
+  return NSK_OK;
+}
+
+int nsk_embedding_bwd(const void* dout, int dtype_in, const int32_t* tokens, uint64_t n, int E, float* dtable,
+                      void* stream) {
+  uint64_t total = n * (uint64_t)E;
+  if (!total) return NSK_OK;
+  if (dtype_in == NSK_DTYPE_F32)
+    embed_bwd_kernel<float><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>((const float*)dout, tokens, n,
+                                                                                          E, dtable);
+  else
+    embed_bwd_kernel<__nv_bfloat16><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16*)dout, tokens, n, E, dtable);
+  NSK_LAUNCH_CHECK("embedding_bwd");
+  return NSK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// Multi-tensor optimizers (K11 SGD-momentum, K12 AdamW + global-norm clip).
+//
+// Reference (pkg/src/nsk/nn.py):
+//   sgd_step      nn.py:91-99   v <- mu*v + g ; w <- w - lr*v          (float64 math, float32 store)
+//   adamw_step    nn.py:102-119 w *= 1 - lr*wd ; bias-corrected Adam  (float64 math, float32 store)
+//   clip_grad_norm nn.py:122-139 global float64 L2, grads scaled by float32(max/norm)
+// One launch covers every parameter: blockIdx.y selects the tensor, blocks
+// stride over its elements. Tensor tables (pointers, sizes) are device arrays
+// built once by the Python ParamGroup. The optimizer also refreshes the bf16
+// shadow copy of each weight that conv/GEMM kernels read (w_bf16 may be NULL).
+#include "common.cuh"
+#include "../../include/nskb.h"
+
+namespace {
+
+__global__ void sgd_kernel(float* const* w, const float* const* g, float* const* v, void* const* wb,
+                           const uint64_t* numel, double lr, double mu, float gscale) {
+  const int t = blockIdx.y;
+  const uint64_t n = numel[t];
+  float* W = w[t];
+  const float* G = g[t];
+  float* V = v[t];
+  __nv_bfloat16* B = (__nv_bfloat16*)wb[t];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    // explicit _rn ops: no FMA contraction, so results match numpy's float64 arithmetic bit for bit
+    double gi = (double)__fmul_rn(G[i], gscale);
+    double vi = __dadd_rn(__dmul_rn(mu, (double)V[i]), gi);
+    V[i] = (float)vi;
+    float wn = (float)__dsub_rn((double)W[i], __dmul_rn(lr, vi));
+    W[i] = wn;
+    if (B) B[i] = __float2bfloat16_rn(wn);
+  }
+}
+
+__global__ void adamw_kernel(float* const* w, const float* const* g, float* const* m, float* const* v, void* const* wb,
+                             const uint64_t* numel, double lr, double wd, double b1, double b2, double eps, double bc1,
+                             double bc2, const float* gscale_dev) {
+  const int t = blockIdx.y;
+  const uint64_t n = numel[t];
+  float* W = w[t];
+  const float* G = g[t];
+  float* Mm = m[t];
+  float* Vv = v[t];
+  __nv_bfloat16* B = (__nv_bfloat16*)wb[t];
+  const float gs = gscale_dev ? gscale_dev[0] : 1.f;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    double gi = (double)(gscale_dev ? __fmul_rn(G[i], gs) : G[i]);
+    double wi = __dmul_rn((double)W[i], __dsub_rn(1.0, __dmul_rn(lr, wd)));
+    double mi = __dadd_rn(__dmul_rn(b1, (double)Mm[i]), __dmul_rn(__dsub_rn(1.0, b1), gi));
+    double vi = __dadd_rn(__dmul_rn(b2, (double)Vv[i]), __dmul_rn(__dmul_rn(__dsub_rn(1.0, b2), gi), gi));
+    Mm[i] = (float)mi;
+    Vv[i] = (float)vi;
+    double mh = __ddiv_rn(mi, bc1), vh = __ddiv_rn(vi, bc2);
+    float wn = (float)__dsub_rn(wi, __ddiv_rn(__dmul_rn(lr, mh), __dadd_rn(__dsqrt_rn(vh), eps)));
+    W[i] = wn;
+    if (B) B[i] = __float2bfloat16_rn(wn);
+  }
+}
+
+constexpr int NB = 1024;  // partial slots for the norm reduction
+
+__global__ void sqnorm_partial_kernel(const float* const* g, const uint64_t* numel, int nt, double* part) {
+  __shared__ double red[256 / 32];
+  double s = 0.0;
+  for (int t = 0; t < nt; ++t) {
+    const float* G = g[t];
+    const uint64_t n = numel[t];
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+      double x = (double)G[i];
+      s += x * x;
+    }
+  }
+  s = warp_sum_d(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 256 / 32; ++i) t += red[i];
+    part[1 + blockIdx.x] = t;
+  }
+}
+
+__global__ void sqnorm_final_kernel(double* part, int nb) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < nb; ++i) t += part[1 + i];
+    part[0] = t;
+  }
+}
+
+__global__ void clip_scale_kernel(const double* sq, float max_norm, float* scale) {
+  double norm = sqrt(sq[0]);
+  scale[0] = norm <= (double)max_norm ? 1.f : (float)((double)max_norm / norm);
+}
+
+__global__ void scale_kernel(float* const* g, const uint64_t* numel, const float* scale) {
+  const float s = scale[0];
+  if (s == 1.f) return;
+  const int t = blockIdx.y;
+  float* G = g[t];
+  const uint64_t n = numel[t];
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    G[i] *= s;
+}
+
+// blocks per tensor: ~16 resident blocks per SM across the whole launch
+unsigned blocks_x(int nt) {
+  int b = (16 * nsk::sm_count() + nt - 1) / (nt > 0 ? nt : 1);
+  if (b < 16) b = 16;
+  if (b > 4096) b = 4096;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsk_sgd_multi(int nt, float* const* w, const float* const* g, float* const* v, void* const* wb,
+                  const uint64_t* numel, double lr, double momentum, float grad_scale, void* stream) {
+  if (nt < 1) return NSK_OK;
+  dim3 grid(blocks_x(nt), nt);
+  sgd_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, v, wb, numel, lr, momentum, grad_scale);
+  NSK_LAUNCH_CHECK("sgd_multi");
+  return NSK_OK;
+}
+
+int nsk_adamw_multi(int nt, float* const* w, const float* const* g, float* const* m, float* const* v,
+                    void* const* wb, const uint64_t* numel, int step, double lr, double wd, double beta1,
+                    double beta2, double eps, const float* grad_scale_dev, void* stream) {
+  if (nt < 1) return NSK_OK;
+  double b1 = beta1, b2 = beta2;
+  double bc1 = 1.0 - pow(b1, (double)step), bc2 = 1.0 - pow(b2, (double)step);
+  dim3 grid(blocks_x(nt), nt);
+  adamw_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, m, v, wb, numel, lr, wd, b1, b2, eps, bc1, bc2,
+                                                       grad_scale_dev);
+  NSK_LAUNCH_CHECK("adamw_multi");
+  return NSK_OK;
+}
+
+// out must hold 1 + 1024 doubles; out[0] receives the sum of squares.
+int nsk_sqnorm_multi(int nt, const float* const* g, const uint64_t* numel, double* out, void* stream) {
+  int nb = 2 * nsk::sm_count();
+  if (nb > NB) nb = NB;
+  sqnorm_partial_kernel<<<nb, 256, 0, (cudaStream_t)stream>>>(g, numel, nt, out);
+  sqnorm_final_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(out, nb);
+  NSK_LAUNCH_CHECK("sqnorm_multi");
+  return NSK_OK;
+}
+
+int nsk_clip_scale(const double* sqnorm, float max_norm, float* scale_dev, void* stream) {
+  clip_scale_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sqnorm, max_norm, scale_dev);
+  NSK_LAUNCH_CHECK("clip_scale");
+  return NSK_OK;
+}
+
+int nsk_scale_multi(int nt, float* const* g, const uint64_t* numel, const float* scale_dev, void* stream) {
+  if (nt < 1) return NSK_OK;
+  dim3 grid(blocks_x(nt), nt);
+  scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(g, numel, scale_dev);
+  NSK_LAUNCH_CHECK("scale_multi");
+  return NSK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,637 @@
+// tcgen05/TMEM implicit-GEMM engine: dense GEMM (linear layers) and conv2d
+// fprop / dgrad / wgrad on NHWC bf16 activations, fed by TMA.
+//
+// Replaces (reference): matmul_t   pkg/src/nsk/tensor.py:213-229
+//                       plain_matmul pkg/src/nsk/tensor.py:232-234 (via gradient_rule autodiff.py:265-267)
+//                       conv2d (absent in the reference; restated in oracle/restated.py)
+//
+// One CTA computes one 128 x BN output tile (or one K-split of it):
+//   warp 0 lane 0 : TMA producer   (STAGES-deep smem ring, mbarrier full/empty)
+//   warp 1 lane 0 : MMA issuer     (tcgen05.mma kind::f16 | kind::tf32, fp32 accum in TMEM)
+//   warp 2        : TMEM allocator
+//   warps 4..7    : epilogue       (tcgen05.ld -> bias/beta/convert -> global)
+// Every smem stage holds 128 bytes of K per operand row: 4 UMMA k-substeps.
+// Operands can be K-major (TMA box {128B of K, rows}) or MN-major
+// (boxes of 64 bf16 / 32 fp32 MN-elements x KS K-rows), all 128B-swizzled.
+#include "common.cuh"
+#include "../../include/nskb.h"
+
+namespace {
+
+enum { MODE_GEMM = 0, MODE_CONV = 1, MODE_WGRAD = 2 };
+enum { BMODE_2D = 0, BMODE_DGRAD3D = 1 };
+
+constexpr int kMaxTaps = 9;
+
+struct UmmaProb {
+  int mode, bmode;
+  int a_mn, b_mn;
+  int M, N;
+  int k_steps;      // K-steps for this launch (per class for conv; total for wgrad)
+  int k_per_split;  // wgrad: K-steps per split
+  // conv / wgrad pixel tiling (A operand is a 4D NHWC tensor map)
+  int Wt, Ht, Nt;   // pixel tile extents (output-grid units)
+  int Wo, Ho;       // output grid (fprop/dgrad) or dy grid (wgrad)
+  int cs;           // coordinate stride (conv stride)
+  int cchunks;      // reduction channel chunks of 64 per tap
+  int ntaps[4];
+  signed char tdh[4][kMaxTaps], tdw[4][kMaxTaps], tw[4][kMaxTaps];
+  int os, Hd, Wd;   // output pixel mapping: (n, i*os+ph, j*os+pw) in an [Hd x Wd] grid
+  int atoms_total;  // wgrad: M / 64
+  int cin_atoms;    // wgrad: Cin / 64
+  // epilogue
+  void* out;
+  long long ldc;
+  int out_f32;
+  const float* bias;
+  float beta;
+  int Mpad;         // wgrad workspace rows per split
+};
+
+template <int ESZ>
+struct KT {
+  static constexpr int KE = 128 / ESZ;  // elements per 128B row
+  static constexpr int KS = 128 / ESZ;  // K rows per stage for MN-major operands (64 bf16 / 32 fp32)
+  static constexpr int UK = 32 / ESZ;   // UMMA K per instruction (16 bf16 / 8 tf32)
+};
+
+template <int BN, int ESZ, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 1) + 16 + 1024;
+};
+
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+template <int BN, int ESZ, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UmmaProb p) {
+  using S = Smem<BN, ESZ, STAGES>;
+  using T = KT<ESZ>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + S::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int cls = (p.mode == MODE_CONV) ? blockIdx.z : 0;
+  const int m0 = blockIdx.x * 128;
+  const int n0 = blockIdx.y * BN;
+
+  int kb = 0, ke = p.k_steps;
+  if (p.mode == MODE_WGRAD) {
+    kb = blockIdx.z * p.k_per_split;
+    ke = min(p.k_steps, kb + p.k_per_split);
+  } else if (p.mode == MODE_CONV) {
+    ke = p.ntaps[cls] * p.cchunks;
+  }
+  const int nk = ke > kb ? ke - kb : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    int n_img = 0, h_img = 0, w_img = 0;
+    if (p.mode == MODE_CONV) {
+      int hw = p.Ho * p.Wo;
+      n_img = m0 / hw;
+      int rem = m0 - n_img * hw;
+      h_img = rem / p.Wo;
+      w_img = rem - h_img * p.Wo;
+    }
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % STAGES;
+      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+      uint8_t* sa = smem + s * S::STAGE_BYTES;
+      uint8_t* sb = sa + S::A_BYTES;
+      const int kk = kb + i;
+      uint32_t bytes = S::A_BYTES + S::B_BYTES;
+      if (p.mode == MODE_WGRAD && m0 / 64 + 1 >= p.atoms_total) bytes -= 8192;  // second M atom out of range
+      mbar_expect_tx(&full[s], bytes);
+      // ---- A ----
+      if (p.mode == MODE_GEMM) {
+        if (!p.a_mn) {
+          tma_load_2d(&tmA, &full[s], sa, kk * T::KE, m0);
+        } else {
+#pragma unroll
+          for (int a = 0; a < 128 / T::KE; ++a)
+            tma_load_2d(&tmA, &full[s], sa + a * (T::KS * 128), m0 + a * T::KE, kk * T::KS);
+        }
+      } else if (p.mode == MODE_CONV) {
+        const int tap = kk / p.cchunks;
+        const int c0 = (kk - tap * p.cchunks) * 64;
+        tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[cls][tap], h_img * p.cs + p.tdh[cls][tap], n_img);
+      } else {  // WGRAD: A = x, MN-major atoms of 64 channels at tap offsets; K = 64 dy pixels
+        const int pix0 = kk * 64;
+        int hw = p.Ho * p.Wo;
+        int nn = pix0 / hw;
+        int rem = pix0 - nn * hw;
+        int hh = rem / p.Wo;
+        int ww = rem - hh * p.Wo;
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int ga = m0 / 64 + a;
+          if (ga < p.atoms_total) {
+            const int tap = ga / p.cin_atoms;
+            const int c0 = (ga - tap * p.cin_atoms) * 64;
+            tma_load_4d(&tmA, &full[s], sa + a * 8192, c0, ww * p.cs + p.tdw[0][tap], hh * p.cs + p.tdh[0][tap], nn);
+          }
+        }
+      }
+      // ---- B ----
+      if (p.mode == MODE_GEMM || p.mode == MODE_WGRAD) {
+        if (!p.b_mn) {
+          tma_load_2d(&tmB, &full[s], sb, kk * T::KE, n0);
+        } else {
+#pragma unroll
+          for (int b = 0; b < BN / T::KE; ++b)
+            tma_load_2d(&tmB, &full[s], sb + b * (T::KS * 128), n0 + b * T::KE, kk * T::KS);
+        }
+      } else {  // CONV
+        const int tap = kk / p.cchunks;
+        const int c0 = (kk - tap * p.cchunks) * 64;
+        if (p.bmode == BMODE_2D) {
+          // fprop: W[Kout][taps*Cin] K-major
+          tma_load_2d(&tmB, &full[s], sb, p.tw[cls][tap] * (p.cchunks * 64) + c0, n0);
+        } else {
+          // dgrad: W viewed as 3D (Cin, taps, Kout); N = Cin (MN-major), K = Kout rows
+#pragma unroll
+          for (int b = 0; b < BN / 64; ++b)
+            tma_load_3d(&tmB, &full[s], sb + b * 8192, n0 + b * 64, p.tw[cls][tap], c0);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    const int a_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? 0 : p.a_mn);
+    const int b_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? (p.bmode == BMODE_DGRAD3D) : p.b_mn);
+    const uint32_t idesc = make_idesc(ESZ == 2 ? 1u : 2u, (uint32_t)a_mn, (uint32_t)b_mn, 128u, (uint32_t)BN);
+    const uint32_t a_lbo = a_mn ? (T::KS * 128) : 16;
+    const uint32_t b_lbo = b_mn ? (T::KS * 128) : 16;
+    const uint32_t a_step = a_mn ? (T::UK * 128) : 32;
+    const uint32_t b_step = b_mn ? (T::UK * 128) : 32;
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % STAGES;
+      mbar_wait(&full[s], (i / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
+      const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint64_t ad = sdesc_sw128(sa + j * a_step, a_lbo, 1024);
+        uint64_t bd = sdesc_sw128(sb + j * b_step, b_lbo, 1024);
+        if (ESZ == 2)
+          umma_bf16(tmem_base, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+        else
+          umma_tf32(tmem_base, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+      }
+      umma_commit(&empty[s]);
+    }
+    umma_commit(accum);
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // tile row == TMEM lane
+    const int m = m0 + r;
+    if (nk > 0) {
+      mbar_wait(accum, 0);
+      tc_fence_after();
+    }
+    bool row_ok;
+    long long row_off;
+    if (p.mode == MODE_WGRAD) {
+      row_ok = m < p.M;
+      row_off = ((long long)blockIdx.z * p.Mpad + m) * (long long)p.ldc;
+    } else if (p.mode == MODE_CONV) {
+      row_ok = m < p.M;
+      int hw = p.Ho * p.Wo;
+      int nn = m / hw;
+      int rem = m - nn * hw;
+      int ii = rem / p.Wo;
+      int jj = rem - ii * p.Wo;
+      int ph = cls >> 1, pw = cls & 1;
+      long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
+      row_off = pix * p.ldc;
+    } else {
+      row_ok = m < p.M;
+      row_off = (long long)m * p.ldc;
+    }
+    const bool vec_ok = ((p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0);
+    int nchunks = (p.N - n0 + 31) / 32;
+    if (nchunks > BN / 32) nchunks = BN / 32;
+#pragma unroll 1
+    for (int c = 0; c < nchunks; ++c) {
+      uint32_t v[32];
+      if (nk > 0) {
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + c * 32, v);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = 0;
+      }
+      if (!row_ok) continue;
+      const int col0 = n0 + c * 32;
+      float f[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(v[t]);
+      if (p.bias) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t)
+          if (col0 + t < p.N) f[t] += p.bias[col0 + t];
+      }
+      const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
+      if (p.out_f32) {
+        float* o = (float*)p.out + row_off + col0;
+        if (p.beta != 0.f) {
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) f[t] += p.beta * o[t];
+        }
+        if (full_chunk) {
+#pragma unroll
+          for (int t = 0; t < 32; t += 4) *(float4*)(o + t) = make_float4(f[t], f[t + 1], f[t + 2], f[t + 3]);
+        } else {
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) o[t] = f[t];
+        }
+      } else {
+        __nv_bfloat16* o = (__nv_bfloat16*)p.out + row_off + col0;
+        if (full_chunk) {
+#pragma unroll
+          for (int t = 0; t < 32; t += 8) {
+            uint4 u;
+            u.x = pack_bf16x2(f[t], f[t + 1]);
+            u.y = pack_bf16x2(f[t + 2], f[t + 3]);
+            u.z = pack_bf16x2(f[t + 4], f[t + 5]);
+            u.w = pack_bf16x2(f[t + 6], f[t + 7]);
+            *(uint4*)(o + t) = u;
+          }
+        } else {
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) o[t] = __float2bfloat16_rn(f[t]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, BN < 32 ? 32 : BN);
+  }
+}
+
+// wgrad split-K reduction: ws[split][Mpad][N] (rows = (tap, cin), cols = cout)
+//   -> dw[cout][tap][cin] (+= if beta).  The transpose keeps the cin index fastest.
+__global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M, int N, float* dw,
+                                    float beta) {
+  long long total = (long long)M * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int n = (int)(idx / M);  // cout
+    int m = (int)(idx - (long long)n * M);
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) acc += ws[((long long)s * Mpad + m) * N + n];
+    float* d = dw + (long long)n * M + m;
+    *d = beta != 0.f ? acc + beta * *d : acc;
+  }
+}
+
+template <int BN, int ESZ, int STAGES>
+int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const UmmaProb& p, dim3 grid, cudaStream_t st) {
+  using S = Smem<BN, ESZ, STAGES>;
+  auto kern = umma_kernel<BN, ESZ, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+    if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(umma)");
+    configured = true;
+  }
+  kern<<<grid, 256, S::TOTAL, st>>>(a, b, p);
+  NSK_LAUNCH_CHECK("umma_kernel");
+  return NSK_OK;
+}
+
+template <int ESZ>
+int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, const UmmaProb& p, dim3 grid, cudaStream_t st) {
+  switch (BN) {
+    case 64:
+      return launch_umma<64, ESZ, 4>(a, b, p, grid, st);
+    case 128:
+      return launch_umma<128, ESZ, 3>(a, b, p, grid, st);
+    case 256:
+      return launch_umma<256, ESZ, 3>(a, b, p, grid, st);
+  }
+  return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
+}
+
+int pick_bn(int N) {
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  return 256;
+}
+
+// pixel tile (Wt, Ht, Nt) covering `rows` consecutive output pixels in (n,h,w) raster order
+bool pixel_tile(int Wo, int Ho, int rows, int* Wt, int* Ht, int* Nt) {
+  if (Wo > rows || rows % Wo != 0) return false;
+  int per = rows / Wo;
+  if (per <= Ho) {
+    if (Ho % per != 0) return false;
+    *Wt = Wo;
+    *Ht = per;
+    *Nt = 1;
+  } else {
+    if (per % Ho != 0) return false;
+    *Wt = Wo;
+    *Ht = Ho;
+    *Nt = per / Ho;
+  }
+  return true;
+}
+
+int nhwc_map(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int c_box, int Wt, int Ht, int Nt, int cs) {
+  uint64_t dims[4] = {(uint64_t)C, (uint64_t)W, (uint64_t)H, (uint64_t)N};
+  uint64_t strides[3] = {(uint64_t)C * 2, (uint64_t)W * C * 2, (uint64_t)H * W * C * 2};
+  uint32_t box[4] = {(uint32_t)c_box, (uint32_t)(Wt * cs), (uint32_t)(Ht * cs), (uint32_t)Nt};
+  uint32_t es[4] = {1, (uint32_t)cs, (uint32_t)cs, 1};
+  return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ptr, dims, strides, box, es,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+int check_desc(const NskConvDesc* d) {
+  if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride < 1)
+    return nsk::set_error(NSK_ERR_SHAPE, "conv2d: invalid descriptor");
+  if (d->R * d->S > kMaxTaps) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d: filter larger than 3x3");
+  if (d->C % 64 != 0 || d->K % 64 != 0)
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d: channel counts must be multiples of 64 (pad the stem)");
+  return NSK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, long long lda, const void* B,
+             long long ldb, void* C, long long ldc, int c_f32, const float* bias, float beta, void* stream) {
+  if (M < 1 || N < 1 || K < 1) return nsk::set_error(NSK_ERR_SHAPE, "gemm: empty problem");
+  const int esz = dtype == NSK_DTYPE_BF16 ? 2 : 4;
+  if ((lda * esz) % 16 || (ldb * esz) % 16 || ((uintptr_t)A % 16) || ((uintptr_t)B % 16))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "gemm: operands must be 16-byte aligned with 16-byte row pitch");
+  if (beta != 0.f && !c_f32) return nsk::set_error(NSK_ERR_UNSUPPORTED, "gemm: beta needs an fp32 output");
+  const int KE = 128 / esz;
+  const int BN = pick_bn(N);
+  CUtensorMapDataType dt = esz == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap ma, mb;
+  int rc;
+  {
+    uint64_t dims[2], str[1];
+    uint32_t box[2];
+    if (!a_mn) {
+      dims[0] = K; dims[1] = M; box[0] = KE; box[1] = 128;
+    } else {
+      dims[0] = M; dims[1] = K; box[0] = KE; box[1] = KE;
+    }
+    str[0] = (uint64_t)lda * esz;
+    if ((rc = nsk::encode_tmap(&ma, dt, 2, A, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+    if (!b_mn) {
+      dims[0] = K; dims[1] = N; box[0] = KE; box[1] = BN;
+    } else {
+      dims[0] = N; dims[1] = K; box[0] = KE; box[1] = KE;
+    }
+    str[0] = (uint64_t)ldb * esz;
+    if ((rc = nsk::encode_tmap(&mb, dt, 2, B, dims, str, box, nullptr, CU_TENSOR_MAP_SWIZZLE_128B))) return rc;
+  }
+  UmmaProb p{};
+  p.mode = MODE_GEMM;
+  p.a_mn = a_mn;
+  p.b_mn = b_mn;
+  p.M = M;
+  p.N = N;
+  p.k_steps = (K + KE - 1) / KE;
+  p.out = C;
+  p.ldc = ldc;
+  p.out_f32 = c_f32;
+  p.bias = bias;
+  p.beta = beta;
+  dim3 grid((M + 127) / 128, (N + BN - 1) / BN, 1);
+  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+  return dispatch_bn<4>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+}
+
+// y[n,p,q,k] = sum_{c,r,s} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]   (NHWC / KRSC, bf16)
+int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int y_f32, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  const int P = d->P, Q = d->Q;
+  int Wt, Ht, Nt;
+  if (!pixel_tile(Q, P, 128, &Wt, &Ht, &Nt))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d fprop: output width must tile 128 pixels");
+  const int BN = pick_bn(d->K);
+  CUtensorMap ma, mb;
+  if ((rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
+  {
+    const int RS = d->R * d->S;
+    uint64_t dims[2] = {(uint64_t)RS * d->C, (uint64_t)d->K};
+    uint64_t str[1] = {(uint64_t)RS * d->C * 2};
+    uint32_t box[2] = {64, (uint32_t)BN};
+    if ((rc = nsk::encode_tmap(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, nullptr,
+                               CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  UmmaProb p{};
+  p.mode = MODE_CONV;
+  p.bmode = BMODE_2D;
+  p.M = d->N * P * Q;
+  p.N = d->K;
+  p.Wt = Wt; p.Ht = Ht; p.Nt = Nt;
+  p.Wo = Q; p.Ho = P;
+  p.cs = d->stride;
+  p.cchunks = d->C / 64;
+  int t = 0;
+  for (int r = 0; r < d->R; ++r)
+    for (int s = 0; s < d->S; ++s, ++t) {
+      p.tdh[0][t] = (signed char)(r - d->pad);
+      p.tdw[0][t] = (signed char)(s - d->pad);
+      p.tw[0][t] = (signed char)t;
+    }
+  p.ntaps[0] = t;
+  p.os = 1; p.Hd = P; p.Wd = Q;
+  p.out = y;
+  p.ldc = d->K;
+  p.out_f32 = y_f32;
+  dim3 grid((p.M + 127) / 128, (d->K + BN - 1) / BN, 1);
+  return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+}
+
+// dx[n,h,w,c] = sum_{k,r,s : h = p*st-pad+r} dy[n,p,q,k] * w[k,r,s,c]
+// stride 1: one launch over all taps; stride 2: four output-parity classes
+// (blockIdx.z), each a stride-1 gather over dy with its subset of taps.
+int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  const int P = d->P, Q = d->Q, st = d->stride;
+  if (st > 2) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: stride > 2");
+  if (d->H % st || d->W % st) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: H, W must divide stride");
+  // output grid of each class
+  const int Hg = d->H / st, Wg = d->W / st;
+  int Wt, Ht, Nt;
+  if (!pixel_tile(Wg, Hg, 128, &Wt, &Ht, &Nt))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: input width must tile 128 pixels");
+  const int BN = pick_bn(d->C);
+  CUtensorMap ma, mb;
+  if ((rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
+  {
+    const int RS = d->R * d->S;
+    uint64_t dims[3] = {(uint64_t)d->C, (uint64_t)RS, (uint64_t)d->K};
+    uint64_t str[2] = {(uint64_t)d->C * 2, (uint64_t)RS * d->C * 2};
+    uint32_t box[3] = {64, 1, 64};
+    if ((rc = nsk::encode_tmap(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, w, dims, str, box, nullptr,
+                               CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  UmmaProb p{};
+  p.mode = MODE_CONV;
+  p.bmode = BMODE_DGRAD3D;
+  p.M = d->N * Hg * Wg;
+  p.N = d->C;
+  p.Wt = Wt; p.Ht = Ht; p.Nt = Nt;
+  p.Wo = Wg; p.Ho = Hg;
+  p.cs = 1;
+  p.cchunks = d->K / 64;
+  const int ncls = st * st;
+  for (int c = 0; c < ncls; ++c) {
+    const int ph = st == 2 ? (c >> 1) : 0, pw = st == 2 ? (c & 1) : 0;
+    int t = 0;
+    for (int r = 0; r < d->R; ++r)
+      for (int s = 0; s < d->S; ++s) {
+        // h = i*st + ph = p*st - pad + r  =>  p = i + (ph + pad - r)/st when divisible
+        int nh = ph + d->pad - r, nw = pw + d->pad - s;
+        if (((nh % st) + st) % st || ((nw % st) + st) % st) continue;
+        int dh = nh >= 0 ? nh / st : -((-nh + st - 1) / st);
+        int dw = nw >= 0 ? nw / st : -((-nw + st - 1) / st);
+        p.tdh[c][t] = (signed char)dh;
+        p.tdw[c][t] = (signed char)dw;
+        p.tw[c][t] = (signed char)(r * d->S + s);
+        ++t;
+      }
+    p.ntaps[c] = t;
+  }
+  // map classes to (ph, pw) = (c>>1, c&1) even when stride == 1 (single class 0)
+  p.os = st; p.Hd = d->H; p.Wd = d->W;
+  p.out = dx;
+  p.ldc = d->C;
+  p.out_f32 = 0;
+  dim3 grid((p.M + 127) / 128, (d->C + BN - 1) / BN, ncls);
+  return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+}
+
+uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
+  const int M = d->R * d->S * d->C;
+  const int Mpad = ((M + 127) / 128) * 128;
+  const long long pix = (long long)d->N * d->P * d->Q;
+  const int k_steps = (int)((pix + 63) / 64);
+  const int mt = Mpad / 128;
+  const int BN = pick_bn(d->K);
+  const int nt = (d->K + BN - 1) / BN;
+  int target = 2 * nsk::sm_count();
+  int splits = target / (mt * nt);
+  if (splits < 1) splits = 1;
+  int max_splits = k_steps / 4 > 0 ? k_steps / 4 : 1;
+  if (splits > max_splits) splits = max_splits;
+  return (uint64_t)splits * Mpad * d->K * sizeof(float);
+}
+
+// dw[k,r,s,c] (+)= sum_{n,p,q} dy[n,p,q,k] * x[n, p*st-pad+r, q*st-pad+s, c]   (fp32 out)
+int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float* dw, float beta, void* ws,
+                     uint64_t ws_bytes, void* stream) {
+  int rc = check_desc(d);
+  if (rc) return rc;
+  const int P = d->P, Q = d->Q;
+  int Wt, Ht, Nt;
+  if (!pixel_tile(Q, P, 64, &Wt, &Ht, &Nt))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: output width must tile 64 pixels");
+  const long long pix = (long long)d->N * P * Q;
+  if (pix % 64) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: N*P*Q must be a multiple of 64");
+  const int RS = d->R * d->S;
+  const int M = RS * d->C;
+  const int Mpad = ((M + 127) / 128) * 128;
+  const int k_steps = (int)(pix / 64);
+  const int BN = pick_bn(d->K);
+  const int mt = Mpad / 128, nt = (d->K + BN - 1) / BN;
+  int splits = (int)(ws_bytes / ((uint64_t)Mpad * d->K * sizeof(float)));
+  if (splits < 1) return nsk::set_error(NSK_ERR_SHAPE, "conv2d wgrad: workspace too small");
+  uint64_t want = nsk_conv2d_wgrad_workspace(d) / ((uint64_t)Mpad * d->K * sizeof(float));
+  if ((uint64_t)splits > want) splits = (int)want;
+  const int per = (k_steps + splits - 1) / splits;
+  splits = (k_steps + per - 1) / per;
+  CUtensorMap ma, mb;
+  if ((rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
+  {
+    uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)pix};
+    uint64_t str[1] = {(uint64_t)d->K * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = nsk::encode_tmap(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dy, dims, str, box, nullptr,
+                               CU_TENSOR_MAP_SWIZZLE_128B)))
+      return rc;
+  }
+  UmmaProb p{};
+  p.mode = MODE_WGRAD;
+  p.a_mn = 1;
+  p.b_mn = 1;
+  p.M = M;
+  p.N = d->K;
+  p.k_steps = k_steps;
+  p.k_per_split = per;
+  p.Wt = Wt; p.Ht = Ht; p.Nt = Nt;
+  p.Wo = Q; p.Ho = P;
+  p.cs = d->stride;
+  int t = 0;
+  for (int r = 0; r < d->R; ++r)
+    for (int s = 0; s < d->S; ++s, ++t) {
+      p.tdh[0][t] = (signed char)(r - d->pad);
+      p.tdw[0][t] = (signed char)(s - d->pad);
+    }
+  p.atoms_total = M / 64;
+  p.cin_atoms = d->C / 64;
+  p.out = ws;
+  p.ldc = d->K;
+  p.out_f32 = 1;
+  p.Mpad = Mpad;
+  dim3 grid(mt, nt, splits);
+  if ((rc = dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream))) return rc;
+  long long total = (long long)M * d->K;
+  wgrad_reduce_kernel<<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>((const float*)ws, splits, Mpad, M,
+                                                                                   d->K, dw, beta);
+  NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
+  return NSK_OK;
+}
+
+}  // extern "C"

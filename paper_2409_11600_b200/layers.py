@@ -1,0 +1,302 @@
+"""New tape-recorded ops for CNN / GRU training (absent from the reference).
+
+Each op follows the reference's recording pattern (autodiff.rec_* in
+pkg/src/nsk/autodiff.py:165-248): compute the output with a libnskb kernel,
+``record`` a node with its saved operands, and register a gradient rule.
+Their CPU restatements (float64) live in oracle/restated.py.
+
+Activations are NHWC bfloat16; parameters and their gradients float32 (the
+tensor-core kernels read a bf16 shadow of each weight, refreshed by the
+optimizer). Gradients always take the dtype of the tensor they belong to.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import BF16, F32, ConvDesc, check
+from .autodiff import SUNK, _internal_tensor, record, rule
+from .errors import NskRuntimeError, NskTypeError
+from .tensor import Buffer, Pool, Tensor, empty_tensor, release_tensor
+
+
+class Workspace:
+    """Grow-only scratch shared by kernels that need temporary device memory (stream-ordered reuse)."""
+
+    def __init__(self):
+        self.buf: Buffer | None = None
+
+    def get(self, nbytes: int) -> Buffer:
+        if self.buf is None or self.buf.nbytes < nbytes:
+            self.buf = Buffer((max(nbytes, 1 << 20) + 3) // 4, F32)
+        return self.buf
+
+
+WGRAD_WS = Workspace()
+BN_WS = Workspace()
+
+
+def _temp_bf16(t: Tensor, pool: Pool) -> tuple[int, Tensor | None]:
+    """bf16 pointer for ``t``: itself, a parameter's shadow, or a pooled cast copy (returned for release)."""
+    if t.dtype == BF16:
+        return t.ptr, None
+    if t.param_name is not None:
+        return t.bf16_ptr(), None
+    tmp = empty_tensor(pool, t.shape, BF16)
+    check(_lib.lib().nsk_cast(F32, t.ptr, BF16, tmp.ptr, t.numel, _lib.stream()))
+    return tmp.ptr, tmp
+
+
+# --- conv2d ---------------------------------------------------------------------------------
+
+def conv_out(h: int, k: int, stride: int, pad: int) -> int:
+    return (h + 2 * pad - k) // stride + 1
+
+
+def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool) -> Tensor:
+    """y[n,p,q,k] = sum_{r,s,c} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]  (NHWC x KRSC -> NHWC, bf16)."""
+    if x.rank != 4 or w.rank != 4:
+        raise NskTypeError(f"conv2d needs NHWC input and KRSC filters, got {list(x.shape)} and {list(w.shape)}")
+    n, h, wd, c = x.shape
+    k, r, s, c2 = w.shape
+    if c != c2:
+        raise NskTypeError(f"conv2d channel mismatch: input has {c}, filters expect {c2}")
+    p, q = conv_out(h, r, stride, pad), conv_out(wd, s, stride, pad)
+    if p < 1 or q < 1:
+        raise NskTypeError(f"conv2d output would be empty for input {list(x.shape)}")
+    desc = ConvDesc(n, h, wd, c, k, r, s, stride, pad, p, q)
+    y = empty_tensor(pool, (n, p, q, k), BF16)
+    lib = _lib.lib()
+    st = _lib.stream()
+    xp, xtmp = _temp_bf16(x, pool)
+    wp = w.bf16_ptr() if w.dtype == F32 else w.ptr
+    if c % 64 == 0:
+        check(lib.nsk_conv2d_fprop(C.byref(desc), xp, wp, y.ptr, 0, st))
+        saved = (x, w)
+        attrs = {"desc": desc, "stem": False}
+        if xtmp is not None:
+            release_tensor(pool, xtmp)
+    else:
+        # small-channel stem: explicit im2col (K = R*S*C padded to 64) + tcgen05 GEMM
+        rsc = r * s * c
+        kp = (rsc + 63) // 64 * 64
+        cols = empty_tensor(pool, (n * p * q, kp), BF16)
+        check(lib.nsk_im2col(xp, cols.ptr, n, h, wd, c, r, s, stride, pad, p, q, kp, st))
+        if xtmp is not None:
+            release_tensor(pool, xtmp)
+        wpk = empty_tensor(pool, (k, kp), BF16)
+        check(lib.nsk_fill_bf16(wpk.ptr, wpk.numel, 0.0, st))
+        check(lib.nsk_memcpy2d_d2d(wpk.ptr, kp * 2, wp, rsc * 2, rsc * 2, k, st))
+        check(lib.nsk_gemm(BF16, 0, 0, n * p * q, k, kp, cols.ptr, kp, wpk.ptr, kp, y.ptr, k, 0, None, 0.0, st))
+        release_tensor(pool, wpk)
+        _internal_tensor(cols)
+        saved = (cols, w)
+        attrs = {"desc": desc, "stem": True, "kp": kp}
+    record("conv2d", y, x, w, saved=saved, attrs=attrs)
+    return y
+
+
+@rule("conv2d")
+def _r_conv2d(node, g, pool, sinks):
+    desc = node.attrs["desc"]
+    xin, w = node.saved
+    lib = _lib.lib()
+    st = _lib.stream()
+    dx = dw = None
+    gp, gtmp = _temp_bf16(g, pool)
+    if node.inputs[0].requires_grad:
+        dx = empty_tensor(pool, tuple(node.inputs[0].tensor.shape), BF16)
+        wb = w.bf16_ptr() if w.dtype == F32 else w.ptr
+        if node.attrs["stem"]:
+            # dcols[M, Kp] = dy[M, K] . Wp[K, Kp] (Wp MN-major), then the col2im gather
+            kp = node.attrs["kp"]
+            rsc = desc.R * desc.S * desc.C
+            m = desc.N * desc.P * desc.Q
+            wpk = empty_tensor(pool, (desc.K, kp), BF16)
+            check(lib.nsk_fill_bf16(wpk.ptr, wpk.numel, 0.0, st))
+            check(lib.nsk_memcpy2d_d2d(wpk.ptr, kp * 2, wb, rsc * 2, rsc * 2, desc.K, st))
+            dcols = empty_tensor(pool, (m, kp), F32)
+            check(lib.nsk_gemm(BF16, 0, 1, m, kp, desc.K, gp, desc.K, wpk.ptr, kp, dcols.ptr, kp, 1, None, 0.0, st))
+            check(lib.nsk_col2im(dcols.ptr, dx.ptr, desc.N, desc.H, desc.W, desc.C, desc.R, desc.S, desc.stride,
+                                 desc.pad, desc.P, desc.Q, kp, st))
+            release_tensor(pool, dcols)
+            release_tensor(pool, wpk)
+        else:
+            check(lib.nsk_conv2d_dgrad(C.byref(desc), gp, wb, dx.ptr, st))
+    if node.inputs[1].requires_grad:
+        if sinks[1] is not None:
+            out_ptr, beta, dw = sinks[1].ptr, 1.0, SUNK
+        else:
+            dwt = empty_tensor(pool, w.shape, F32)
+            out_ptr, beta, dw = dwt.ptr, 0.0, dwt
+        if node.attrs["stem"]:
+            # dW[k, rsc] = dy^T . cols : A = dy [M][K] (MN-major), B = cols [M][Kp] (MN-major), N = R*S*C
+            m = desc.N * desc.P * desc.Q
+            rsc = desc.R * desc.S * desc.C
+            check(lib.nsk_gemm(BF16, 1, 1, desc.K, rsc, m, gp, desc.K, xin.ptr, node.attrs["kp"], out_ptr, rsc, 1,
+                               None, beta, st))
+        else:
+            xp, xtmp = _temp_bf16(xin, pool)
+            need = lib.nsk_conv2d_wgrad_workspace(C.byref(desc))
+            ws = WGRAD_WS.get(need)
+            check(lib.nsk_conv2d_wgrad(C.byref(desc), xp, gp, out_ptr, beta, ws.ptr, ws.nbytes, st))
+            if xtmp is not None:
+                release_tensor(pool, xtmp)
+    if gtmp is not None:
+        release_tensor(pool, gtmp)
+    return [dx, dw]
+
+
+# --- batchnorm (+ residual, + relu) ---------------------------------------------------------------
+
+def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: Tensor | None = None,
+              eps: float = 1e-5) -> Tensor:
+    """Training-mode batch norm over N*H*W per channel, gamma_beta = [2, C]; optional residual add and ReLU."""
+    if x.dtype != BF16:
+        raise NskTypeError("batchnorm expects a bf16 NHWC activation")
+    c = x.shape[-1]
+    if gb.shape != (2, c):
+        raise NskTypeError(f"batchnorm parameters must be [2, {c}], got {list(gb.shape)}")
+    if residual is not None and (residual.shape != x.shape or residual.dtype != BF16):
+        raise NskTypeError("batchnorm residual must match the input shape (bf16)")
+    rows = x.numel // c
+    lib = _lib.lib()
+    st = _lib.stream()
+    y = empty_tensor(pool, x.shape, BF16)
+    mean = _internal_tensor(empty_tensor(pool, (c,)))
+    invstd = _internal_tensor(empty_tensor(pool, (c,)))
+    ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
+    check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu),
+                         None if residual is None else residual.ptr, ws.ptr, st))
+    saved = (x, gb, mean, invstd) + ((y,) if relu else ())
+    record("batchnorm", y, x, gb, residual, saved=saved, attrs={"relu": relu, "rows": rows, "c": c})
+    return y
+
+
+@rule("batchnorm")
+def _r_batchnorm(node, g, pool, sinks):
+    x, gb, mean, invstd = node.saved[:4]
+    y = node.saved[4] if node.attrs["relu"] else None
+    rows, c = node.attrs["rows"], node.attrs["c"]
+    lib = _lib.lib()
+    st = _lib.stream()
+    if g.dtype != BF16:
+        raise NskRuntimeError("batchnorm gradient must be bf16")
+    dx = empty_tensor(pool, x.shape, BF16) if node.inputs[0].requires_grad else None
+    res_node = node.inputs[2]
+    dres = empty_tensor(pool, x.shape, BF16) if (res_node is not None and res_node.requires_grad) else None
+    if sinks[1] is not None:
+        dgb_ptr, beta, dgb = sinks[1].ptr, 1.0, SUNK
+    else:
+        t = empty_tensor(pool, (2, c))
+        dgb_ptr, beta, dgb = t.ptr, 0.0, t
+    scratch_dx = None
+    if dx is None:
+        scratch_dx = empty_tensor(pool, x.shape, BF16)
+    ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
+    check(lib.nsk_bn_bwd(g.ptr, x.ptr, None if y is None else y.ptr, gb.ptr, mean.ptr, invstd.ptr,
+                         (dx or scratch_dx).ptr, None if dres is None else dres.ptr, dgb_ptr, beta, rows, c,
+                         ws.ptr, st))
+    if scratch_dx is not None:
+        release_tensor(pool, scratch_dx)
+    if not node.inputs[1].requires_grad:
+        if dgb is not SUNK and dgb is not None:
+            release_tensor(pool, dgb)
+        dgb = None
+    return [dx, dgb, dres]
+
+
+# --- pooling / reshape / layout -------------------------------------------------------------------
+
+def avgpool_global(x: Tensor, pool: Pool) -> Tensor:
+    """[N, H, W, C] -> [N, C] float32 mean over H*W."""
+    n, h, w, c = x.shape
+    y = empty_tensor(pool, (n, c))
+    check(_lib.lib().nsk_avgpool_fwd(x.dtype, x.ptr, y.ptr, n, h * w, c, _lib.stream()))
+    record("avgpool", y, x, attrs={"shape": x.shape, "dtype": x.dtype})
+    return y
+
+
+@rule("avgpool")
+def _r_avgpool(node, g, pool, sinks):
+    shape, dtype = node.attrs["shape"], node.attrs["dtype"]
+    n, h, w, c = shape
+    dx = empty_tensor(pool, shape, dtype)
+    check(_lib.lib().nsk_avgpool_bwd(g.ptr, dtype, dx.ptr, n, h * w, c, _lib.stream()))
+    return [dx]
+
+
+def maxpool(x: Tensor, k: int, stride: int, pad: int, pool: Pool) -> Tensor:
+    if x.dtype != BF16:
+        raise NskTypeError("maxpool expects a bf16 NHWC activation")
+    n, h, w, c = x.shape
+    p, q = conv_out(h, k, stride, pad), conv_out(w, k, stride, pad)
+    y = empty_tensor(pool, (n, p, q, c), BF16)
+    check(_lib.lib().nsk_maxpool_fwd(x.ptr, y.ptr, n, h, w, c, k, stride, pad, p, q, _lib.stream()))
+    record("maxpool", y, x, saved=(x,), attrs={"k": k, "stride": stride, "pad": pad})
+    return y
+
+
+@rule("maxpool")
+def _r_maxpool(node, g, pool, sinks):
+    (x,) = node.saved
+    a = node.attrs
+    n, h, w, c = x.shape
+    _, p, q, _ = g.shape
+    dx = empty_tensor(pool, x.shape, BF16)
+    check(_lib.lib().nsk_maxpool_bwd(x.ptr, g.ptr, dx.ptr, n, h, w, c, a["k"], a["stride"], a["pad"], p, q,
+                                     _lib.stream()))
+    return [dx]
+
+
+def reshape(x: Tensor, shape, pool: Pool) -> Tensor:
+    """A recorded copy with a new shape (row-major order kept; NHWC flatten)."""
+    shape = tuple(int(d) for d in shape)
+    if int(np.prod(shape)) != x.numel:
+        raise NskTypeError(f"cannot reshape {list(x.shape)} to {list(shape)}")
+    y = empty_tensor(pool, shape, x.dtype)
+    check(_lib.lib().nsk_memcpy_d2d(y.ptr, x.ptr, x.buffer.nbytes, _lib.stream()))
+    record("reshape", y, x, attrs={"shape": x.shape})
+    return y
+
+
+@rule("reshape")
+def _r_reshape(node, g, pool, sinks):
+    dx = empty_tensor(pool, node.attrs["shape"], g.dtype)
+    check(_lib.lib().nsk_memcpy_d2d(dx.ptr, g.ptr, g.buffer.nbytes, _lib.stream()))
+    return [dx]
+
+
+def cast(x: Tensor, dtype: int, pool: Pool) -> Tensor:
+    if x.dtype == dtype:
+        return x
+    y = empty_tensor(pool, x.shape, dtype)
+    check(_lib.lib().nsk_cast(x.dtype, x.ptr, dtype, y.ptr, x.numel, _lib.stream()))
+    record("cast", y, x, attrs={"dtype": x.dtype})
+    return y
+
+
+@rule("cast")
+def _r_cast(node, g, pool, sinks):
+    dt = node.attrs["dtype"]
+    dx = empty_tensor(pool, g.shape, dt)
+    check(_lib.lib().nsk_cast(g.dtype, g.ptr, dt, dx.ptr, g.numel, _lib.stream()))
+    return [dx]
+
+
+def nchw_to_nhwc(x: Tensor, pool: Pool, channels_pad: int | None = None) -> Tensor:
+    """Host-layout images [N, C, H, W] float32 -> NHWC bf16 (no gradient: data preparation)."""
+    n, c, h, w = x.shape
+    cp = channels_pad or c
+    y = empty_tensor(pool, (n, h, w, cp), BF16)
+    check(_lib.lib().nsk_nchw_to_nhwc(x.ptr, y.ptr, n, c, h, w, cp, _lib.stream()))
+    record("layout", y, x)
+    return y
+
+
+@rule("layout")
+def _r_layout(node, g, pool, sinks):
+    raise NskRuntimeError("nchw_to_nhwc is a data-preparation op and has no gradient")

@@ -1,0 +1,140 @@
+"""Model declarations on the drop-in surface: small CNN (C1) and CIFAR ResNet-18 (C2).
+
+Parameters are created through the session exactly like the reference's
+``xavier_uniform`` / ``param_zeros`` builtins (builtins.py:85-104): names
+``p0, p1, ...`` in declaration order, one ``session.rng`` seed draw per
+randomly initialised tensor. oracle/models.py declares the same parameters in
+the same order, so both sides start from bit-identical weights.
+
+Forward passes record on the session tape; each block output is pushed as an
+assignment, the way the interpreter pushes every statement (runtime.py:192-202).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import autodiff, layers, nn
+from .runtime import Session
+from .tensor import Tensor
+
+
+class Params:
+    """Declaration-order parameter factory bound to a session."""
+
+    def __init__(self, session: Session):
+        self.s = session
+
+    def _add(self, t):
+        self.s.param_group.add(t.param_name, t)
+        return t
+
+    def conv(self, cout, r, s, cin) -> Tensor:
+        name = self.s.new_param_name()
+        return self._add(nn.xavier_uniform_conv(cout, r, s, cin, self.s.new_seed(), self.s.pool, name))
+
+    def bn(self, c) -> Tensor:
+        gb = np.zeros((2, c), np.float32)
+        gb[0] = 1.0
+        return self._add(autodiff.make_param(self.s.pool, gb, self.s.new_param_name()))
+
+    def linear(self, rows, cols) -> Tensor:
+        name = self.s.new_param_name()
+        return self._add(nn.xavier_uniform_init(rows, cols, self.s.new_seed(), self.s.pool, name=name))
+
+    def zeros(self, *dims) -> Tensor:
+        return self._add(autodiff.make_param(self.s.pool, np.zeros(dims, np.float32), self.s.new_param_name()))
+
+
+class SmallCNN:
+    """C1: conv 3->16 3x3 p1 + b -> ReLU -> conv 16->32 3x3 s2 p1 + b -> ReLU -> flatten (NHWC) -> linear -> CE."""
+
+    def __init__(self, session: Session, hw: int = 32, classes: int = 10):
+        P = Params(session)
+        self.s = session
+        self.w1, self.b1 = P.conv(16, 3, 3, 3), P.zeros(16)
+        self.w2, self.b2 = P.conv(32, 3, 3, 16), P.zeros(32)
+        feat = 32 * (hw // 2) * (hw // 2)
+        self.fc_w, self.fc_b = P.linear(classes, feat), P.zeros(classes)
+
+    def forward(self, x_nchw: Tensor) -> Tensor:
+        pool, push = self.s.pool, self.s.push_named
+        x = layers.nchw_to_nhwc(x_nchw, pool)
+        push("cnn.x", x)
+        h = autodiff.rec_elementwise("relu", autodiff.rec_bias_add(layers.conv2d(x, self.w1, 1, 1, pool), self.b1,
+                                                                   pool), None, pool)
+        push("cnn.h1", h)
+        h = autodiff.rec_elementwise("relu", autodiff.rec_bias_add(layers.conv2d(h, self.w2, 2, 1, pool), self.b2,
+                                                                   pool), None, pool)
+        push("cnn.h2", h)
+        f = layers.reshape(h, (h.shape[0], h.numel // h.shape[0]), pool)
+        logits = nn.linear(f, self.fc_w, self.fc_b, pool)
+        push("cnn.logits", logits)
+        return logits
+
+
+class ResNet18:
+    """CIFAR ResNet-18: 3x3 stem, no max-pool, [2,2,2,2] BasicBlocks, 1x1 projection shortcuts,
+    BN after every conv, global average pool, fc -> 11,173,962 parameters."""
+
+    STAGES = ((64, 1), (128, 2), (256, 2), (512, 2))
+
+    def __init__(self, session: Session, classes: int = 10):
+        P = Params(session)
+        self.s = session
+        self.stem_w, self.stem_bn = P.conv(64, 3, 3, 3), P.bn(64)
+        self.blocks = []
+        cin = 64
+        for cout, stride in self.STAGES:
+            for b in range(2):
+                st = stride if b == 0 else 1
+                blk = {"stride": st, "w1": P.conv(cout, 3, 3, cin), "bn1": P.bn(cout),
+                       "w2": P.conv(cout, 3, 3, cout), "bn2": P.bn(cout)}
+                if st != 1 or cin != cout:
+                    blk["wsc"], blk["bnsc"] = P.conv(cout, 1, 1, cin), P.bn(cout)
+                self.blocks.append(blk)
+                cin = cout
+        self.fc_w, self.fc_b = P.linear(classes, 512), P.zeros(classes)
+
+    def num_params(self) -> int:
+        return sum(t.numel for _n, t in self.s.param_group.params)
+
+    def forward(self, x_nchw: Tensor | None = None, x_nhwc: Tensor | None = None) -> Tensor:
+        pool, push = self.s.pool, self.s.push_named
+        x = x_nhwc if x_nhwc is not None else layers.nchw_to_nhwc(x_nchw, pool)
+        push("rn.x", x)
+        h = layers.batchnorm(layers.conv2d(x, self.stem_w, 1, 1, pool), self.stem_bn, pool, relu=True)
+        push("rn.stem", h)
+        for i, blk in enumerate(self.blocks):
+            st = blk["stride"]
+            o = layers.batchnorm(layers.conv2d(h, blk["w1"], st, 1, pool), blk["bn1"], pool, relu=True)
+            if "wsc" in blk:
+                sc = layers.batchnorm(layers.conv2d(h, blk["wsc"], st, 0, pool), blk["bnsc"], pool, relu=False)
+            else:
+                sc = h
+            h = layers.batchnorm(layers.conv2d(o, blk["w2"], 1, 1, pool), blk["bn2"], pool, relu=True, residual=sc)
+            push(f"rn.block{i}", h)
+        feat = layers.avgpool_global(h, pool)
+        logits = nn.linear(feat, self.fc_w, self.fc_b, pool)
+        push("rn.logits", logits)
+        return logits
+
+
+def resnet18_train_flops_per_image() -> float:
+    """Algorithmic training FLOPs per 32x32 image (3.329 GFLOP): forward, wgrad and dgrad
+    MACs x 2, without the stem's dgrad (its input needs no gradient)."""
+    macs = 0
+    h = 32
+    stem = h * h * 64 * 27
+    macs += stem
+    cin = 64
+    for cout, stride in ResNet18.STAGES:
+        for b in range(2):
+            st = stride if b == 0 else 1
+            ho = h // st
+            macs += ho * ho * cout * cin * 9 + ho * ho * cout * cout * 9
+            if st != 1 or cin != cout:
+                macs += ho * ho * cout * cin
+            h, cin = ho, cout
+    macs += 512 * 10
+    return 2.0 * (3 * macs - stem)

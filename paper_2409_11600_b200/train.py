@@ -1,0 +1,189 @@
+"""The public training-step API: host batch in, loss out, one CUDA graph per step.
+
+A step is exactly the reference training loop body (pkg/README.md example;
+builtins.py:146-169): forward through the tape, ``cross_entropy``,
+``backward()``, the optimizer step, ``zero_grad()``. The first ``warmup``
+steps run eagerly; they warm the Pool so every later step acquires the same
+buffers in the same order (the reference's warm-pool invariant, SPEC.md:344,
+test_autodiff.py:247-269). The next step is captured once as a CUDA graph and
+replayed thereafter -- the per-op host bookkeeping (~8 + 15 us per op in the
+reference) disappears from the steady state.
+
+Inputs travel host -> pinned staging -> device on the compute stream before
+the graph launch; the loss is read back from a device scalar slot.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib, autodiff, nn
+from ._lib import F32, check
+from .autodiff import backward, data_from_device
+from .errors import NskRuntimeError
+from .tensor import SCALARS, Buffer, DeviceScalar, Tensor, check_index_values
+
+
+class PinnedArray:
+    """A page-locked host array (cudaHostAlloc) for async H2D staging."""
+
+    def __init__(self, shape, dtype=np.float32):
+        self.shape = tuple(shape)
+        self.dtype = np.dtype(dtype)
+        nbytes = int(np.prod(self.shape)) * self.dtype.itemsize
+        p = C.c_void_p()
+        check(_lib.lib().nsk_pinned_alloc(max(nbytes, 1), C.byref(p)))
+        self.ptr = p.value
+        self.nbytes = nbytes
+        raw = (C.c_char * max(nbytes, 1)).from_address(self.ptr)
+        self.array = np.frombuffer(raw, dtype=self.dtype, count=int(np.prod(self.shape))).reshape(self.shape)
+
+    def __del__(self):
+        try:
+            if self.ptr and _lib._lib is not None:
+                _lib._lib.nsk_pinned_free(self.ptr)
+        except Exception:
+            pass
+
+
+class StepGraph:
+    """A captured step: replay with ``launch``."""
+
+    def __init__(self, exec_handle: int, nodes: int):
+        self.exec = exec_handle
+        self.nodes = nodes
+
+    def launch(self):
+        check(_lib.lib().nsk_graph_launch(self.exec, _lib.stream()))
+
+    def __del__(self):
+        try:
+            if self.exec and _lib._lib is not None:
+                _lib._lib.nsk_graph_destroy(self.exec)
+        except Exception:
+            pass
+
+
+def capture(fn):
+    """Run ``fn`` under stream capture and return (StepGraph, fn's result). Nothing executes yet."""
+    lib = _lib.lib()
+    st = _lib.stream()
+    check(lib.nsk_graph_begin(st))
+    try:
+        result = fn()
+    except BaseException:
+        ex, n = C.c_void_p(), C.c_uint64()
+        lib.nsk_graph_end(st, C.byref(ex), C.byref(n))
+        if ex.value:
+            lib.nsk_graph_destroy(ex.value)
+        raise
+    ex, n = C.c_void_p(), C.c_uint64()
+    check(lib.nsk_graph_end(st, C.byref(ex), C.byref(n)))
+    return StepGraph(ex.value, int(n.value)), result
+
+
+class Trainer:
+    """Classification training loop over a tape-recorded model.
+
+    ``optimizer`` is ``("sgd", lr, momentum)`` or ``("adamw", Hyperparams, clip_norm|None)``.
+    """
+
+    def __init__(self, session, model, x_shape, classes: int, optimizer=("sgd", 0.1, 0.9), graph: bool = True,
+                 warmup: int = 2, dp=None):
+        self.s = session
+        self.model = model
+        self.classes = classes
+        self.opt = optimizer
+        self.use_graph = graph
+        self.warmup = warmup
+        self.dp = dp
+        self.x_shape = tuple(x_shape)
+        b = self.x_shape[0]
+        self.x_pin = PinnedArray(self.x_shape)
+        self.y_pin = PinnedArray((b,))
+        pool = session.pool
+        self.x_dev = Tensor(self.x_shape, Buffer(int(np.prod(self.x_shape)), F32))
+        self.y_dev = Tensor((b,), Buffer(b, F32))
+        for t in (self.x_dev, self.y_dev):
+            t.refs = 1  # external hold: the traversal never returns these to the pool
+        self.y_dev.host_src = self.y_pin.array
+        self.steps_done = 0
+        self.graph: StepGraph | None = None
+        self.loss_slot: int | None = None
+        self.fresh_at_capture = None
+        self._copied = None
+
+    # -- the step body (recorded on the tape) --
+    def _body(self) -> DeviceScalar:
+        s = self.s
+        x = data_from_device(self.x_dev)
+        y = data_from_device(self.y_dev)
+        logits = self.model.forward(x)
+        loss = nn.cross_entropy(logits, y, s.pool)
+        s.push_named("train.loss", loss)
+        backward(s.tape(), s.grad_cache, s.pool)
+        if self.dp is not None:
+            self.dp.finish_backward()
+        kind = self.opt[0]
+        if kind == "sgd":
+            nn.sgd_step(s.param_group, s.grad_cache, self.opt[1], self.opt[2])
+        elif kind == "adamw":
+            hp, clip = self.opt[1], self.opt[2]
+            scale = None
+            if clip is not None:
+                scale = nn.clip_grad_norm(s.grad_cache, clip)
+            nn.adamw_step(s.param_group, s.grad_cache, hp)
+        else:
+            raise NskRuntimeError(f"unknown optimizer {kind!r}")
+        s.grad_cache.zero_after_step()
+        if loss._scalar is None:
+            raise NskRuntimeError("loss was not reclaimed by backward()")
+        return loss._scalar
+
+    def stage(self, x_host, y_host) -> None:
+        """Host batch -> pinned -> device (async on the compute stream)."""
+        y = np.asarray(y_host, dtype=np.float32).reshape(-1)
+        check_index_values(y, self.classes, "target")
+        lib, st = _lib.lib(), _lib.stream()
+        if self._copied is None:
+            ev = C.c_void_p()
+            check(lib.nsk_event_create(0, C.byref(ev)))
+            self._copied = ev.value
+        else:
+            check(lib.nsk_event_sync(self._copied))  # previous H2D finished reading the pinned buffers
+        np.copyto(self.x_pin.array, np.asarray(x_host, dtype=np.float32).reshape(self.x_shape))
+        np.copyto(self.y_pin.array, y)
+        check(lib.nsk_memcpy_h2d(self.x_dev.ptr, self.x_pin.ptr, self.x_pin.nbytes, st))
+        check(lib.nsk_memcpy_h2d(self.y_dev.ptr, self.y_pin.ptr, self.y_pin.nbytes, st))
+        check(lib.nsk_event_record(self._copied, st))
+
+    def run_staged(self) -> DeviceScalar:
+        """One step on the already-staged device batch (no host copies)."""
+        if self.graph is not None:
+            self.graph.launch()
+            self.steps_done += 1
+            return DeviceScalar(self.loss_slot)
+        if self.use_graph and self.steps_done >= self.warmup:
+            fresh = self.s.pool.stats()["fresh"]
+            self.graph, sc = capture(self._body)
+            if self.s.pool.stats()["fresh"] != fresh:
+                raise NskRuntimeError("pool was not warm at capture time")
+            self.loss_slot = sc.slot
+            self.graph.launch()
+            self.steps_done += 1
+            return DeviceScalar(self.loss_slot)
+        sc = self._body()
+        self.steps_done += 1
+        return sc
+
+    def step(self, x_host, y_host) -> DeviceScalar:
+        """The public call: copy the host batch in, run one training step, return the loss (on device)."""
+        self.stage(x_host, y_host)
+        # the pinned staging buffers may be overwritten by the next stage() only after this step's copies ran
+        return self.run_staged()
+
+    @property
+    def launches_per_step(self) -> int:
+        return self.graph.nodes if self.graph is not None else -1
