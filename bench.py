@@ -1,0 +1,319 @@
+"""Benchmark: CIFAR-10-shape ResNet-18 training step on B200 (BASELINE.json metric / config C2, C5).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N > 1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N)
+
+One step = forward + cross-entropy + backward + SGD(lr 0.1, momentum 0.9) + zero_grad on a
+synthetic batch of 256 images per GPU (weak scaling), replayed as one CUDA graph. ``value`` is
+device-timed (CUDA events per step, L2 flushed between timed steps, max over ranks); ``e2e``
+goes through the public Trainer.step(host x, host y) call with the H2D copy of the batch and
+the D2H read of the loss inside the timed region. ``--impl reference`` times the reference's
+CPU path (the oracle port of the reference arithmetic + restated conv/BN ops, float64, all host
+cores) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train images/sec, CIFAR-10-shape ResNet at 1/2/4/8 B200; conv/GEMM % of peak"
+BATCH = 256
+FLOPS_PER_IMG = None  # filled from the model definition
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), d["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=5)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def synthetic_batch(seed: int, b: int = BATCH):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((b, 3, 32, 32)).astype(np.float32)
+    y = rng.integers(0, 10, b).astype(np.float32)
+    return x, y
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_oracle(sample_imgs: int, steps: int, warmup: int = 1):
+    """The reference CPU path (oracle port, float64) on a bounded sample: returns (img/s, per-step seconds)."""
+    from oracle import models as om
+
+    ref = om.ResNet18Oracle(seed=0)
+    x, y = synthetic_batch(1234, sample_imgs)
+    for _ in range(warmup):
+        ref.train_step(x, y, lr=0.1, momentum=0.9)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        ref.train_step(x, y, lr=0.1, momentum=0.9)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return sample_imgs / med, times
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    cores = cpu_cores()
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
+    sample = 16
+    ips, times = run_oracle(sample, max(1, min(args.steps, 3)), warmup=1)
+    line = {
+        "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": 1, "ms_per_step": 1000.0 * statistics.median(times) * BATCH / sample,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD), reference CPU path "
+                               "(oracle port: reference arithmetic + restated conv/BN, float64)",
+                   "global_batch": BATCH, "sample_images_per_step": sample, "parallelism": "cpu"},
+        "cpu_baseline": {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} images/step x {len(times)} steps of the B=256 workload"},
+        "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def time_conv_kernel(lib, _lib, iters=20):
+    """Dominant tensor-core kernel timed alone: stage-1 3x3 conv fprop 64->64, B=256 at 32x32."""
+    from paper_2409_11600_b200._lib import BF16, ConvDesc
+    from paper_2409_11600_b200.tensor import Buffer
+
+    d = ConvDesc(BATCH, 32, 32, 64, 64, 3, 3, 1, 1, 32, 32)
+    x = Buffer(BATCH * 32 * 32 * 64, BF16)
+    x.fill(0.5)
+    w = Buffer(64 * 9 * 64, BF16)
+    w.fill(0.01)
+    y = Buffer(BATCH * 32 * 32 * 64, BF16)
+    st = _lib.stream()
+    for _ in range(3):
+        _lib.check(lib.nsk_conv2d_fprop(C.byref(d), x.ptr, w.ptr, y.ptr, 0, st))
+    e0, e1 = C.c_void_p(), C.c_void_p()
+    lib.nsk_event_create(1, C.byref(e0))
+    lib.nsk_event_create(1, C.byref(e1))
+    lib.nsk_event_record(e0, st)
+    for _ in range(iters):
+        lib.nsk_conv2d_fprop(C.byref(d), x.ptr, w.ptr, y.ptr, 0, st)
+    lib.nsk_event_record(e1, st)
+    lib.nsk_event_sync(e1)
+    ms = C.c_float()
+    lib.nsk_event_elapsed_ms(e0, e1, C.byref(ms))
+    per_ms = ms.value / iters
+    flops = 2.0 * BATCH * 32 * 32 * 64 * 64 * 9
+    return flops, per_ms
+
+
+def profiled_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture (or None)."""
+    p = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def ours_arm(args, rank, world, local_rank):
+    from paper_2409_11600_b200 import _lib
+    from paper_2409_11600_b200.models import ResNet18, resnet18_train_flops_per_image
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.tensor import Buffer
+    from paper_2409_11600_b200.train import Trainer
+
+    _lib.ctx.init(local_rank)
+    lib = _lib.lib()
+    st = _lib.stream()
+    dp = None
+    s = Session(seed=0)
+    model = ResNet18(s)
+    if world > 1:
+        from paper_2409_11600_b200.dp import DataParallel
+
+        dp = DataParallel(s, rank, world)
+        dp.broadcast_params()
+    x, y = synthetic_batch(1000 + rank)
+    tr = Trainer(s, model, x.shape, 10, optimizer=("sgd", 0.1, 0.9), graph=True, warmup=2, dp=dp)
+
+    def barrier():
+        _lib.sync()
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        tr.step(x, y)
+    barrier()
+    flush = Buffer(64 << 20, _lib.F32)  # 256 MiB > 126 MB L2
+    e = []
+    for _ in range(2 * args.steps):
+        ev = C.c_void_p()
+        lib.nsk_event_create(1, C.byref(ev))
+        e.append(ev.value)
+    tr.stage(x, y)
+    barrier()
+    dev = _lib.ctx.device
+    with Clocks(dev) as clk:
+        for i in range(args.steps):
+            flush.fill(float(i))
+            lib.nsk_event_record(e[2 * i], st)
+            tr.run_staged()
+            lib.nsk_event_record(e[2 * i + 1], st)
+        barrier()
+    ms_steps = []
+    for i in range(args.steps):
+        ms = C.c_float()
+        _lib.check(lib.nsk_event_elapsed_ms(e[2 * i], e[2 * i + 1], C.byref(ms)))
+        ms_steps.append(ms.value)
+    total_ms = sum(ms_steps)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t[0])
+    ms_per_step = total_ms / args.steps
+    value = world * BATCH * args.steps / (total_ms / 1000.0)
+
+    # e2e through the public call: host batch in (pinned H2D), loss out (D2H) every step
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        loss = float(tr.step(x, y))
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e = world * BATCH * args.steps / e2e_s
+
+    if rank != 0:
+        return
+    pk_burst, pk_sus, hbm, src = peaks()
+    flops, kms = time_conv_kernel(lib, _lib)
+    achieved = flops / (kms / 1000.0) / 1e12
+    step_tflops = value * resnet18_train_flops_per_image() / 1e12 / world
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) images, uniform labels, random init)",
+        "config": {"workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C2/C5",
+                   "model": "resnet18-cifar (11,173,962 params)", "global_batch": BATCH * world,
+                   "per_gpu_batch": BATCH, "seq_len": None, "image": [3, 32, 32], "parallelism": f"dp{world}",
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)",
+                   "final_loss": loss},
+        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(x.nbytes + y.nbytes),
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(tr.launches_per_step * args.steps),
+        "step_tflops_per_gpu": step_tflops,
+        "step_frac_of_peak": step_tflops / pk_sus,
+        "roofline": {"bound": "tensor", "kernel": "umma_kernel<64,2,4> conv2d fprop 3x3 64->64, 256x32x32",
+                     "achieved": achieved, "peak": pk_burst, "unit": "TFLOP/s", "frac": achieved / pk_burst,
+                     "traffic": profiled_traffic(), "peak_source": f"{src} bf16_tflops (burst, kernel timed alone)",
+                     "algorithmic_flops_per_launch": flops, "launch_ms": kms},
+        "clocks": clk.summary(),
+    }
+    if world == 1:
+        cores = cpu_cores()
+        sample = 16
+        ips, times = run_oracle(sample, 2, warmup=1)
+        line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
+                                "sample": f"{sample} images/step x {len(times)} timed steps (1 warm-up) of the "
+                                          "B=256 workload, float64 oracle port"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    ours_arm(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -118,6 +118,8 @@ class Trainer:
     # -- the step body (recorded on the tape) --
     def _body(self) -> DeviceScalar:
         s = self.s
+        if self.dp is not None:
+            self.dp.begin_step()
         x = data_from_device(self.x_dev)
         y = data_from_device(self.y_dev)
         logits = self.model.forward(x)
