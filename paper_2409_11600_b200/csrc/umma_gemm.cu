@@ -5,7 +5,7 @@
 //                       plain_matmul pkg/src/nsk/tensor.py:232-234 (via gradient_rule autodiff.py:265-267)
 //                       conv2d (absent in the reference; restated in oracle/restated.py)
 //
-// One CTA computes one 128 x BN output tile (or one K-split of it):
+// Persistent: one CTA per SM walks 128 x BN output tiles (or K-splits); double-buffered TMEM accumulators.
 //   warp 0 lane 0 : TMA producer   (STAGES-deep smem ring, mbarrier full/empty)
 //   warp 1 lane 0 : MMA issuer     (tcgen05.mma kind::f16 | kind::tf32, fp32 accum in TMEM)
 //   warp 2        : TMEM allocator
@@ -45,7 +45,9 @@ struct UmmaProb {
   int out_f32;
   const float* bias;
   float beta;
-  int Mpad;         // wgrad workspace rows per split
+  int Mpad;         // wgrad workspace row pitch (M padded to the tile)
+  // persistent schedule: units = mt * nt * (classes | splits), n-tile fastest
+  int mt, nt, units;
 };
 
 template <int ESZ>
@@ -61,7 +63,8 @@ struct Smem {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 1) + 16 + 1024;
+  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 4) + 16 + 1024;
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
@@ -72,6 +75,36 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+struct Unit {
+  int m0, n0, z;  // tile origin and class (conv) / split (wgrad)
+  int kb, nk;     // first k-step and number of k-steps
+};
+
+__device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
+  Unit w;
+  const int mn = p.mt * p.nt;
+  w.z = u / mn;
+  const int r = u - w.z * mn;
+  const int mi = r / p.nt;
+  w.m0 = mi * 128;
+  w.n0 = (r - mi * p.nt) * BN;
+  if (p.mode == MODE_WGRAD) {
+    w.kb = w.z * p.k_per_split;
+    int ke = min(p.k_steps, w.kb + p.k_per_split);
+    w.nk = ke > w.kb ? ke - w.kb : 0;
+  } else if (p.mode == MODE_CONV) {
+    w.kb = 0;
+    w.nk = p.ntaps[w.z] * p.cchunks;
+  } else {
+    w.kb = 0;
+    w.nk = p.k_steps;
+  }
+  return w;
+}
+
+// Persistent warp-specialised tcgen05 kernel: each CTA walks work units u = blockIdx.x, +gridDim.x, ...
+// The smem ring runs continuously across units; two TMEM accumulators let the epilogue of unit j
+// overlap the MMAs of unit j+1.
 template <int BN, int ESZ, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UmmaProb p) {
@@ -81,36 +114,29 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* accum = empty + STAGES;
-  uint32_t* tmem_slot = (uint32_t*)(accum + 1);
+  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
+  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int cls = (p.mode == MODE_CONV) ? blockIdx.z : 0;
-  const int m0 = blockIdx.x * 128;
-  const int n0 = blockIdx.y * BN;
-
-  int kb = 0, ke = p.k_steps;
-  if (p.mode == MODE_WGRAD) {
-    kb = blockIdx.z * p.k_per_split;
-    ke = min(p.k_steps, kb + p.k_per_split);
-  } else if (p.mode == MODE_CONV) {
-    ke = p.ntaps[cls] * p.cchunks;
-  }
-  const int nk = ke > kb ? ke - kb : 0;
+  const int units = p.units;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
   }
   if (warp == 2) {
-    tmem_alloc(tmem_slot, BN < 32 ? 32 : BN);
+    tmem_alloc(tmem_slot, S::TMEM_COLS);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -120,73 +146,75 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     // ---------------- TMA producer ----------------
-    int n_img = 0, h_img = 0, w_img = 0;
-    if (p.mode == MODE_CONV) {
-      int hw = p.Ho * p.Wo;
-      n_img = m0 / hw;
-      int rem = m0 - n_img * hw;
-      h_img = rem / p.Wo;
-      w_img = rem - h_img * p.Wo;
-    }
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
-      uint8_t* sa = smem + s * S::STAGE_BYTES;
-      uint8_t* sb = sa + S::A_BYTES;
-      const int kk = kb + i;
-      uint32_t bytes = S::A_BYTES + S::B_BYTES;
-      if (p.mode == MODE_WGRAD && m0 / 64 + 1 >= p.atoms_total) bytes -= 8192;  // second M atom out of range
-      mbar_expect_tx(&full[s], bytes);
-      // ---- A ----
-      if (p.mode == MODE_GEMM) {
-        if (!p.a_mn) {
-          tma_load_2d(&tmA, &full[s], sa, kk * T::KE, m0);
-        } else {
+    int i = 0;  // global k-step counter (smem ring position)
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = decode_unit(p, u, BN);
+      int n_img = 0, h_img = 0, w_img = 0;
+      if (p.mode == MODE_CONV) {
+        const int hw = p.Ho * p.Wo;
+        n_img = w.m0 / hw;
+        const int rem = w.m0 - n_img * hw;
+        h_img = rem / p.Wo;
+        w_img = rem - h_img * p.Wo;
+      }
+      const bool half_a = (p.mode == MODE_WGRAD) && (w.m0 / 64 + 1 >= p.atoms_total);
+      for (int kk = w.kb; kk < w.kb + w.nk; ++kk, ++i) {
+        const int s = i % STAGES;
+        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * S::STAGE_BYTES;
+        uint8_t* sb = sa + S::A_BYTES;
+        mbar_expect_tx(&full[s], S::A_BYTES + S::B_BYTES - (half_a ? 8192 : 0));
+        // ---- A ----
+        if (p.mode == MODE_GEMM) {
+          if (!p.a_mn) {
+            tma_load_2d(&tmA, &full[s], sa, kk * T::KE, w.m0);
+          } else {
 #pragma unroll
-          for (int a = 0; a < 128 / T::KE; ++a)
-            tma_load_2d(&tmA, &full[s], sa + a * (T::KS * 128), m0 + a * T::KE, kk * T::KS);
-        }
-      } else if (p.mode == MODE_CONV) {
-        const int tap = kk / p.cchunks;
-        const int c0 = (kk - tap * p.cchunks) * 64;
-        tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[cls][tap], h_img * p.cs + p.tdh[cls][tap], n_img);
-      } else {  // WGRAD: A = x, MN-major atoms of 64 channels at tap offsets; K = 64 dy pixels
-        const int pix0 = kk * 64;
-        int hw = p.Ho * p.Wo;
-        int nn = pix0 / hw;
-        int rem = pix0 - nn * hw;
-        int hh = rem / p.Wo;
-        int ww = rem - hh * p.Wo;
+            for (int a = 0; a < 128 / T::KE; ++a)
+              tma_load_2d(&tmA, &full[s], sa + a * (T::KS * 128), w.m0 + a * T::KE, kk * T::KS);
+          }
+        } else if (p.mode == MODE_CONV) {
+          const int tap = kk / p.cchunks;
+          const int c0 = (kk - tap * p.cchunks) * 64;
+          tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[w.z][tap], h_img * p.cs + p.tdh[w.z][tap],
+                      n_img);
+        } else {  // WGRAD: A = x, MN-major atoms of 64 channels at tap offsets; K = 64 dy pixels
+          const int pix0 = kk * 64;
+          const int hw = p.Ho * p.Wo;
+          const int nn = pix0 / hw;
+          const int rem = pix0 - nn * hw;
+          const int hh = rem / p.Wo;
+          const int ww = rem - hh * p.Wo;
 #pragma unroll
-        for (int a = 0; a < 2; ++a) {
-          const int ga = m0 / 64 + a;
-          if (ga < p.atoms_total) {
-            const int tap = ga / p.cin_atoms;
-            const int c0 = (ga - tap * p.cin_atoms) * 64;
-            tma_load_4d(&tmA, &full[s], sa + a * 8192, c0, ww * p.cs + p.tdw[0][tap], hh * p.cs + p.tdh[0][tap], nn);
+          for (int a = 0; a < 2; ++a) {
+            const int ga = w.m0 / 64 + a;
+            if (ga < p.atoms_total) {
+              const int tap = ga / p.cin_atoms;
+              const int c0 = (ga - tap * p.cin_atoms) * 64;
+              tma_load_4d(&tmA, &full[s], sa + a * 8192, c0, ww * p.cs + p.tdw[0][tap], hh * p.cs + p.tdh[0][tap],
+                          nn);
+            }
           }
         }
-      }
-      // ---- B ----
-      if (p.mode == MODE_GEMM || p.mode == MODE_WGRAD) {
-        if (!p.b_mn) {
-          tma_load_2d(&tmB, &full[s], sb, kk * T::KE, n0);
-        } else {
+        // ---- B ----
+        if (p.mode == MODE_GEMM || p.mode == MODE_WGRAD) {
+          if (!p.b_mn) {
+            tma_load_2d(&tmB, &full[s], sb, kk * T::KE, w.n0);
+          } else {
 #pragma unroll
-          for (int b = 0; b < BN / T::KE; ++b)
-            tma_load_2d(&tmB, &full[s], sb + b * (T::KS * 128), n0 + b * T::KE, kk * T::KS);
-        }
-      } else {  // CONV
-        const int tap = kk / p.cchunks;
-        const int c0 = (kk - tap * p.cchunks) * 64;
-        if (p.bmode == BMODE_2D) {
-          // fprop: W[Kout][taps*Cin] K-major
-          tma_load_2d(&tmB, &full[s], sb, p.tw[cls][tap] * (p.cchunks * 64) + c0, n0);
+            for (int b = 0; b < BN / T::KE; ++b)
+              tma_load_2d(&tmB, &full[s], sb + b * (T::KS * 128), w.n0 + b * T::KE, kk * T::KS);
+          }
         } else {
-          // dgrad: W viewed as 3D (Cin, taps, Kout); N = Cin (MN-major), K = Kout rows
+          const int tap = kk / p.cchunks;
+          const int c0 = (kk - tap * p.cchunks) * 64;
+          if (p.bmode == BMODE_2D) {
+            tma_load_2d(&tmB, &full[s], sb, p.tw[w.z][tap] * (p.cchunks * 64) + c0, w.n0);
+          } else {
 #pragma unroll
-          for (int b = 0; b < BN / 64; ++b)
-            tma_load_3d(&tmB, &full[s], sb + b * 8192, n0 + b * 64, p.tw[cls][tap], c0);
+            for (int b = 0; b < BN / 64; ++b)
+              tma_load_3d(&tmB, &full[s], sb + b * 8192, w.n0 + b * 64, p.tw[w.z][tap], c0);
+          }
         }
       }
     }
@@ -199,134 +227,152 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t b_lbo = b_mn ? (T::KS * 128) : 16;
     const uint32_t a_step = a_mn ? (T::UK * 128) : 32;
     const uint32_t b_step = b_mn ? (T::UK * 128) : 32;
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % STAGES;
-      mbar_wait(&full[s], (i / STAGES) & 1);
+    int i = 0, j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = decode_unit(p, u, BN);
+      const int acc = j & 1;
+      if (j >= 2) mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
-      const uint32_t sb = sa + S::A_BYTES;
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int k = 0; k < w.nk; ++k, ++i) {
+        const int s = i % STAGES;
+        mbar_wait(&full[s], (i / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
+        const uint32_t sb = sa + S::A_BYTES;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint64_t ad = sdesc_sw128(sa + j * a_step, a_lbo, 1024);
-        uint64_t bd = sdesc_sw128(sb + j * b_step, b_lbo, 1024);
-        if (ESZ == 2)
-          umma_bf16(tmem_base, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
-        else
-          umma_tf32(tmem_base, ad, bd, idesc, (i > 0 || j > 0) ? 1u : 0u);
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t ad = sdesc_sw128(sa + q * a_step, a_lbo, 1024);
+          const uint64_t bd = sdesc_sw128(sb + q * b_step, b_lbo, 1024);
+          if (ESZ == 2)
+            umma_bf16(d_tmem, ad, bd, idesc, (k > 0 || q > 0) ? 1u : 0u);
+          else
+            umma_tf32(d_tmem, ad, bd, idesc, (k > 0 || q > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);
       }
-      umma_commit(&empty[s]);
+      umma_commit(&tfull[acc]);
     }
-    umma_commit(accum);
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;  // tile row == TMEM lane
-    const int m = m0 + r;
-    if (nk > 0) {
-      mbar_wait(accum, 0);
-      tc_fence_after();
-    }
-    bool row_ok;
-    long long row_off;
-    if (p.mode == MODE_WGRAD) {
-      row_ok = m < p.M;
-      row_off = ((long long)blockIdx.z * p.Mpad + m) * (long long)p.ldc;
-    } else if (p.mode == MODE_CONV) {
-      row_ok = m < p.M;
-      int hw = p.Ho * p.Wo;
-      int nn = m / hw;
-      int rem = m - nn * hw;
-      int ii = rem / p.Wo;
-      int jj = rem - ii * p.Wo;
-      int ph = cls >> 1, pw = cls & 1;
-      long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
-      row_off = pix * p.ldc;
-    } else {
-      row_ok = m < p.M;
-      row_off = (long long)m * p.ldc;
-    }
     const bool vec_ok = ((p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0);
-    int nchunks = (p.N - n0 + 31) / 32;
-    if (nchunks > BN / 32) nchunks = BN / 32;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = decode_unit(p, u, BN);
+      const int acc = j & 1;
+      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      tc_fence_after();
+      const int m = w.m0 + r;
+      const bool row_ok = m < p.M;
+      long long row_off;
+      if (p.mode == MODE_WGRAD) {
+        row_off = (long long)w.z * p.N * p.Mpad + m;  // transposed partials: ws[split][n][m]
+      } else if (p.mode == MODE_CONV) {
+        const int hw = p.Ho * p.Wo;
+        const int nn = m / hw;
+        const int rem = m - nn * hw;
+        const int ii = rem / p.Wo;
+        const int jj = rem - ii * p.Wo;
+        const int ph = w.z >> 1, pw = w.z & 1;
+        const long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
+        row_off = pix * p.ldc;
+      } else {
+        row_off = (long long)m * p.ldc;
+      }
+      int nchunks = (p.N - w.n0 + 31) / 32;
+      if (nchunks > BN / 32) nchunks = BN / 32;
 #pragma unroll 1
-    for (int c = 0; c < nchunks; ++c) {
-      uint32_t v[32];
-      if (nk > 0) {
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + c * 32, v);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = 0;
-      }
-      if (!row_ok) continue;
-      const int col0 = n0 + c * 32;
-      float f[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(v[t]);
-      if (p.bias) {
-#pragma unroll
-        for (int t = 0; t < 32; ++t)
-          if (col0 + t < p.N) f[t] += p.bias[col0 + t];
-      }
-      const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
-      if (p.out_f32) {
-        float* o = (float*)p.out + row_off + col0;
-        if (p.beta != 0.f) {
-          for (int t = 0; t < 32; ++t)
-            if (col0 + t < p.N) f[t] += p.beta * o[t];
-        }
-        if (full_chunk) {
-#pragma unroll
-          for (int t = 0; t < 32; t += 4) *(float4*)(o + t) = make_float4(f[t], f[t + 1], f[t + 2], f[t + 3]);
+      for (int c = 0; c < nchunks; ++c) {
+        uint32_t v[32];
+        if (w.nk > 0) {
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
+          tmem_ld_wait();
         } else {
-          for (int t = 0; t < 32; ++t)
-            if (col0 + t < p.N) o[t] = f[t];
-        }
-      } else {
-        __nv_bfloat16* o = (__nv_bfloat16*)p.out + row_off + col0;
-        if (full_chunk) {
 #pragma unroll
-          for (int t = 0; t < 32; t += 8) {
-            uint4 u;
-            u.x = pack_bf16x2(f[t], f[t + 1]);
-            u.y = pack_bf16x2(f[t + 2], f[t + 3]);
-            u.z = pack_bf16x2(f[t + 4], f[t + 5]);
-            u.w = pack_bf16x2(f[t + 6], f[t + 7]);
-            *(uint4*)(o + t) = u;
+          for (int t = 0; t < 32; ++t) v[t] = 0;
+        }
+        if (!row_ok) continue;
+        const int col0 = w.n0 + c * 32;
+        float f[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(v[t]);
+        if (p.mode == MODE_WGRAD) {
+          float* o = (float*)p.out + row_off + (long long)col0 * p.Mpad;
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) o[(long long)t * p.Mpad] = f[t];
+          continue;
+        }
+        if (p.bias) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) f[t] += p.bias[col0 + t];
+        }
+        const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
+        if (p.out_f32) {
+          float* o = (float*)p.out + row_off + col0;
+          if (p.beta != 0.f) {
+            for (int t = 0; t < 32; ++t)
+              if (col0 + t < p.N) f[t] += p.beta * o[t];
+          }
+          if (full_chunk) {
+#pragma unroll
+            for (int t = 0; t < 32; t += 4) *(float4*)(o + t) = make_float4(f[t], f[t + 1], f[t + 2], f[t + 3]);
+          } else {
+            for (int t = 0; t < 32; ++t)
+              if (col0 + t < p.N) o[t] = f[t];
           }
         } else {
-          for (int t = 0; t < 32; ++t)
-            if (col0 + t < p.N) o[t] = __float2bfloat16_rn(f[t]);
+          __nv_bfloat16* o = (__nv_bfloat16*)p.out + row_off + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int t = 0; t < 32; t += 8) {
+              uint4 u4;
+              u4.x = pack_bf16x2(f[t], f[t + 1]);
+              u4.y = pack_bf16x2(f[t + 2], f[t + 3]);
+              u4.z = pack_bf16x2(f[t + 4], f[t + 5]);
+              u4.w = pack_bf16x2(f[t + 6], f[t + 7]);
+              *(uint4*)(o + t) = u4;
+            }
+          } else {
+            for (int t = 0; t < 32; ++t)
+              if (col0 + t < p.N) o[t] = __float2bfloat16_rn(f[t]);
+          }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, BN < 32 ? 32 : BN);
+    tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
 }
 
-// wgrad split-K reduction: ws[split][Mpad][N] (rows = (tap, cin), cols = cout)
-//   -> dw[cout][tap][cin] (+= if beta).  The transpose keeps the cin index fastest.
+// wgrad split-K reduction: ws[split][N][Mpad] (rows = cout, cols = (tap, cin)) -> dw[cout][tap][cin] (+= if beta).
+// Both sides are contiguous in the (tap, cin) index: fully coalesced, fixed summation order.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M, int N, float* dw,
                                     float beta) {
-  long long total = (long long)M * N;
+  const long long total = (long long)M * N;
+  const long long plane = (long long)N * Mpad;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    int n = (int)(idx / M);  // cout
-    int m = (int)(idx - (long long)n * M);
+    const int n = (int)(idx / M);
+    const int m = (int)(idx - (long long)n * M);
+    const float* src = ws + (long long)n * Mpad + m;
     float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[((long long)s * Mpad + m) * N + n];
-    float* d = dw + (long long)n * M + m;
+    for (int s = 0; s < splits; ++s) acc += src[s * plane];
+    float* d = dw + idx;
     *d = beta != 0.f ? acc + beta * *d : acc;
   }
 }
 
 template <int BN, int ESZ, int STAGES>
-int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const UmmaProb& p, dim3 grid, cudaStream_t st) {
+int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStream_t st) {
   using S = Smem<BN, ESZ, STAGES>;
   auto kern = umma_kernel<BN, ESZ, STAGES>;
   static bool configured = false;
@@ -335,20 +381,27 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const UmmaProb& p, d
     if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(umma)");
     configured = true;
   }
+  int grid = nsk::sm_count();
+  if (grid > p.units) grid = p.units;
+  if (grid < 1) grid = 1;
   kern<<<grid, 256, S::TOTAL, st>>>(a, b, p);
   NSK_LAUNCH_CHECK("umma_kernel");
   return NSK_OK;
 }
 
 template <int ESZ>
-int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, const UmmaProb& p, dim3 grid, cudaStream_t st) {
-  switch (BN) {
+int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
+                cudaStream_t st) {
+  p.mt = mt;
+  p.nt = nt;
+  p.units = mt * nt * nz;
+  switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 4>(a, b, p, grid, st);
+      return launch_umma<64, ESZ, 8>(a, b, p, st);
     case 128:
-      return launch_umma<128, ESZ, 3>(a, b, p, grid, st);
+      return launch_umma<128, ESZ, 6>(a, b, p, st);
     case 256:
-      return launch_umma<256, ESZ, 3>(a, b, p, grid, st);
+      return launch_umma<256, ESZ, 4>(a, b, p, st);
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
 }
@@ -441,9 +494,9 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
   p.out_f32 = c_f32;
   p.bias = bias;
   p.beta = beta;
-  dim3 grid((M + 127) / 128, (N + BN - 1) / BN, 1);
-  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
-  return dispatch_bn<4>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+  const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
+  return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
 }
 
 // y[n,p,q,k] = sum_{c,r,s} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]   (NHWC / KRSC, bf16)
@@ -487,8 +540,7 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
   p.out = y;
   p.ldc = d->K;
   p.out_f32 = y_f32;
-  dim3 grid((p.M + 127) / 128, (d->K + BN - 1) / BN, 1);
-  return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream);
 }
 
 // dx[n,h,w,c] = sum_{k,r,s : h = p*st-pad+r} dy[n,p,q,k] * w[k,r,s,c]
@@ -549,8 +601,7 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   p.out = dx;
   p.ldc = d->C;
   p.out_f32 = 0;
-  dim3 grid((p.M + 127) / 128, (d->C + BN - 1) / BN, ncls);
-  return dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream);
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream);
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
@@ -561,10 +612,10 @@ uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
   const int mt = Mpad / 128;
   const int BN = pick_bn(d->K);
   const int nt = (d->K + BN - 1) / BN;
-  int target = 2 * nsk::sm_count();
+  int target = nsk::sm_count();  // one persistent wave of (m, n, split) units
   int splits = target / (mt * nt);
   if (splits < 1) splits = 1;
-  int max_splits = k_steps / 4 > 0 ? k_steps / 4 : 1;
+  int max_splits = k_steps / 8 > 0 ? k_steps / 8 : 1;
   if (splits > max_splits) splits = max_splits;
   return (uint64_t)splits * Mpad * d->K * sizeof(float);
 }
@@ -625,8 +676,7 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   p.ldc = d->K;
   p.out_f32 = 1;
   p.Mpad = Mpad;
-  dim3 grid(mt, nt, splits);
-  if ((rc = dispatch_bn<2>(BN, ma, mb, p, grid, (cudaStream_t)stream))) return rc;
+  if ((rc = dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, (cudaStream_t)stream))) return rc;
   long long total = (long long)M * d->K;
   wgrad_reduce_kernel<<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>((const float*)ws, splits, Mpad, M,
                                                                                    d->K, dw, beta);
