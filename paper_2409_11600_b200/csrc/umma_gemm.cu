@@ -381,7 +381,8 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStre
     if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(umma)");
     configured = true;
   }
-  int grid = nsk::sm_count();
+  const int per_sm = (2 * S::TOTAL <= 227 * 1024) ? 2 : 1;  // small-N tiles: two co-resident CTAs per SM
+  int grid = per_sm * nsk::sm_count();
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   kern<<<grid, 256, S::TOTAL, st>>>(a, b, p);
@@ -397,9 +398,9 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
   p.units = mt * nt * nz;
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 8>(a, b, p, st);
+      return launch_umma<64, ESZ, 4>(a, b, p, st);
     case 128:
-      return launch_umma<128, ESZ, 6>(a, b, p, st);
+      return launch_umma<128, ESZ, 3>(a, b, p, st);
     case 256:
       return launch_umma<256, ESZ, 4>(a, b, p, st);
   }

@@ -1,11 +1,12 @@
 """Scratch: time a graphed ResNet-18 step at B=256."""
 import ctypes as C
+import os
 import sys
 import time
 
 import numpy as np
 
-sys.path.insert(0, ".")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2409_11600_b200 import _lib  # noqa: E402
 from paper_2409_11600_b200.models import ResNet18  # noqa: E402
 from paper_2409_11600_b200.runtime import Session  # noqa: E402

@@ -7,7 +7,7 @@ import time
 import torch
 import torch.nn.functional as F
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # repo root
 lib = ctypes.CDLL(os.path.join(ROOT, "paper_2409_11600_b200", "libnskb.so"))
 lib.nsk_last_error.restype = ctypes.c_char_p
 lib.nsk_conv2d_wgrad_workspace.restype = ctypes.c_uint64
