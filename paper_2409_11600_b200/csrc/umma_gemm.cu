@@ -48,7 +48,19 @@ struct UmmaProb {
   int Mpad;         // wgrad workspace row pitch (M padded to the tile)
   // persistent schedule: units = mt * nt * (classes | splits), n-tile fastest
   int mt, nt, units;
+  // row-reuse conv schedule (stride-1 gathers, tiles of whole image rows, W % 8 == 0): taps are grouped
+  // by column offset dw; one TMA box of Ht + (dh_max - dh_min) rows feeds every tap of the group, each
+  // tap's A operand being a view shifted by whole rows (W*128 B, a multiple of the 1 KB swizzle atom).
+  int rr;
+  int ngroups[4];
+  signed char gdw[4][kMaxTaps], gdhmin[4][kMaxTaps], gnt[4][kMaxTaps];
+  signed char gdh[4][kMaxTaps][3], gw[4][kMaxTaps][3];
+  int ext_rows;  // rows of the A box in rr mode (Ht + dh range)
+  int probe;     // diagnostics (env NSK_PROBE): bit0 skip MMAs, bit1 skip stores, bit2 skip B loads
 };
+
+constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
+constexpr int kStgPitch = 80;          // epilogue staging row pitch (64 B of bf16 + 16 B pad)
 
 template <int ESZ>
 struct KT {
@@ -57,13 +69,15 @@ struct KT {
   static constexpr int UK = 32 / ESZ;   // UMMA K per instruction (16 bf16 / 8 tf32)
 };
 
-template <int BN, int ESZ, int STAGES>
+template <int BN, int ESZ, int STAGES, bool RR = false>
 struct Smem {
-  static constexpr int A_BYTES = 128 * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int A_BYTES = RR ? kRRMaxA : 128 * 128;
+  static constexpr int B1_BYTES = BN * 128;               // one tap's B tile
+  static constexpr int B_BYTES = B1_BYTES * (RR ? 3 : 1);  // rr: up to 3 taps per column group
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + 8 * (2 * STAGES + 4) + 16 + 1024;
+  static constexpr int STG_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
+  static constexpr int TOTAL = STG_OFF + 4 * 32 * 80 + 1024;  // + epilogue staging (4 warps x 32 rows x 80 B)
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
@@ -94,7 +108,7 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
     w.nk = ke > w.kb ? ke - w.kb : 0;
   } else if (p.mode == MODE_CONV) {
     w.kb = 0;
-    w.nk = p.ntaps[w.z] * p.cchunks;
+    w.nk = (p.rr ? p.ngroups[w.z] : p.ntaps[w.z]) * p.cchunks;
   } else {
     w.kb = 0;
     w.nk = p.k_steps;
@@ -105,10 +119,10 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 // Persistent warp-specialised tcgen05 kernel: each CTA walks work units u = blockIdx.x, +gridDim.x, ...
 // The smem ring runs continuously across units; two TMEM accumulators let the epilogue of unit j
 // overlap the MMAs of unit j+1.
-template <int BN, int ESZ, int STAGES>
+template <int BN, int ESZ, int STAGES, bool RR>
 __global__ void __launch_bounds__(256, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UmmaProb p) {
-  using S = Smem<BN, ESZ, STAGES>;
+  using S = Smem<BN, ESZ, STAGES, RR>;
   using T = KT<ESZ>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -117,6 +131,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint8_t* stage_base = smem + S::STG_OFF;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -163,7 +178,27 @@ __global__ void __launch_bounds__(256, 1)
         if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * S::STAGE_BYTES;
         uint8_t* sb = sa + S::A_BYTES;
-        mbar_expect_tx(&full[s], S::A_BYTES + S::B_BYTES - (half_a ? 8192 : 0));
+        if constexpr (RR) {
+          // one row-extended A box for the column group, then the B tile of each tap in the group
+          const int ng = p.ngroups[w.z];
+          const int chunk = kk / ng;
+          const int g = kk - chunk * ng;
+          const int c0 = chunk * 64;
+          const int nt = p.gnt[w.z][g];
+          mbar_expect_tx(&full[s], (uint32_t)(p.ext_rows * p.Wt * 128 + nt * S::B1_BYTES));
+          tma_load_4d(&tmA, &full[s], sa, c0, w_img + p.gdw[w.z][g], h_img + p.gdhmin[w.z][g], n_img);
+          for (int t = 0; t < nt; ++t) {
+            if (p.bmode == BMODE_2D) {
+              tma_load_2d(&tmB, &full[s], sb + t * S::B1_BYTES, p.gw[w.z][g][t] * (p.cchunks * 64) + c0, w.n0);
+            } else {
+#pragma unroll
+              for (int b = 0; b < BN / 64; ++b)
+                tma_load_3d(&tmB, &full[s], sb + t * S::B1_BYTES + b * 8192, w.n0 + b * 64, p.gw[w.z][g][t], c0);
+            }
+          }
+          continue;
+        }
+        mbar_expect_tx(&full[s], S::A_BYTES + ((p.probe & 4) ? 0 : S::B_BYTES) - (half_a ? 8192 : 0));
         // ---- A ----
         if (p.mode == MODE_GEMM) {
           if (!p.a_mn) {
@@ -197,6 +232,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
         // ---- B ----
+        if (p.probe & 4) continue;
         if (p.mode == MODE_GEMM || p.mode == MODE_WGRAD) {
           if (!p.b_mn) {
             tma_load_2d(&tmB, &full[s], sb, kk * T::KE, w.n0);
@@ -240,10 +276,29 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
         const uint32_t sb = sa + S::A_BYTES;
+        if constexpr (RR) {
+          const int ng = p.ngroups[w.z];
+          const int g = k % ng;
+          const int nt = p.gnt[w.z][g];
+          for (int t = 0; t < nt; ++t) {
+            // tap view: rows shifted by (dh - dh_min) whole image rows of Wt pixels
+            const uint32_t at = sa + (uint32_t)((p.gdh[w.z][g][t] - p.gdhmin[w.z][g]) * p.Wt * 128);
+            const uint32_t bt = sb + t * S::B1_BYTES;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t ad = sdesc_sw128(at + q * a_step, a_lbo, 1024);
+              const uint64_t bd = sdesc_sw128(bt + q * b_step, b_lbo, 1024);
+              umma_bf16(d_tmem, ad, bd, idesc, (k > 0 || t > 0 || q > 0) ? 1u : 0u);
+            }
+          }
+          umma_commit(&empty[s]);
+          continue;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const uint64_t ad = sdesc_sw128(sa + q * a_step, a_lbo, 1024);
           const uint64_t bd = sdesc_sw128(sb + q * b_step, b_lbo, 1024);
+          if (p.probe & 1) continue;
           if (ESZ == 2)
             umma_bf16(d_tmem, ad, bd, idesc, (k > 0 || q > 0) ? 1u : 0u);
           else
@@ -293,15 +348,17 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int t = 0; t < 32; ++t) v[t] = 0;
         }
-        if (!row_ok) continue;
         const int col0 = w.n0 + c * 32;
+        if (p.probe & 2) continue;
         float f[32];
 #pragma unroll
         for (int t = 0; t < 32; ++t) f[t] = __uint_as_float(v[t]);
         if (p.mode == MODE_WGRAD) {
-          float* o = (float*)p.out + row_off + (long long)col0 * p.Mpad;
-          for (int t = 0; t < 32; ++t)
-            if (col0 + t < p.N) o[(long long)t * p.Mpad] = f[t];
+          if (row_ok) {
+            float* o = (float*)p.out + row_off + (long long)col0 * p.Mpad;
+            for (int t = 0; t < 32; ++t)
+              if (col0 + t < p.N) o[(long long)t * p.Mpad] = f[t];
+          }
           continue;
         }
         if (p.bias) {
@@ -311,34 +368,48 @@ __global__ void __launch_bounds__(256, 1)
         }
         const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
         if (p.out_f32) {
-          float* o = (float*)p.out + row_off + col0;
-          if (p.beta != 0.f) {
-            for (int t = 0; t < 32; ++t)
-              if (col0 + t < p.N) f[t] += p.beta * o[t];
-          }
-          if (full_chunk) {
-#pragma unroll
-            for (int t = 0; t < 32; t += 4) *(float4*)(o + t) = make_float4(f[t], f[t + 1], f[t + 2], f[t + 3]);
-          } else {
-            for (int t = 0; t < 32; ++t)
-              if (col0 + t < p.N) o[t] = f[t];
-          }
-        } else {
-          __nv_bfloat16* o = (__nv_bfloat16*)p.out + row_off + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int t = 0; t < 32; t += 8) {
-              uint4 u4;
-              u4.x = pack_bf16x2(f[t], f[t + 1]);
-              u4.y = pack_bf16x2(f[t + 2], f[t + 3]);
-              u4.z = pack_bf16x2(f[t + 4], f[t + 5]);
-              u4.w = pack_bf16x2(f[t + 6], f[t + 7]);
-              *(uint4*)(o + t) = u4;
+          if (row_ok) {
+            float* o = (float*)p.out + row_off + col0;
+            if (p.beta != 0.f) {
+              for (int t = 0; t < 32; ++t)
+                if (col0 + t < p.N) f[t] += p.beta * o[t];
             }
-          } else {
-            for (int t = 0; t < 32; ++t)
-              if (col0 + t < p.N) o[t] = __float2bfloat16_rn(f[t]);
+            if (full_chunk) {
+#pragma unroll
+              for (int t = 0; t < 32; t += 4) *(float4*)(o + t) = make_float4(f[t], f[t + 1], f[t + 2], f[t + 3]);
+            } else {
+              for (int t = 0; t < 32; ++t)
+                if (col0 + t < p.N) o[t] = f[t];
+            }
           }
+        } else if (full_chunk) {
+          // bf16: stage this warp's 32 rows x 32 columns in shared memory, then write 16-byte pieces so
+          // one store instruction covers 8 rows x 64 contiguous bytes instead of 32 scattered rows.
+          uint8_t* stg = stage_base + q * (32 * kStgPitch);
+#pragma unroll
+          for (int t = 0; t < 32; t += 8) {
+            uint4 u4;
+            u4.x = pack_bf16x2(f[t], f[t + 1]);
+            u4.y = pack_bf16x2(f[t + 2], f[t + 3]);
+            u4.z = pack_bf16x2(f[t + 4], f[t + 5]);
+            u4.w = pack_bf16x2(f[t + 6], f[t + 7]);
+            *(uint4*)(stg + lane * kStgPitch + t * 2) = u4;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 4; ++it) {
+            const int piece = it * 32 + lane;
+            const int pr = piece >> 2, part = piece & 3;
+            const long long ro = __shfl_sync(0xffffffffu, row_off, pr);
+            const int ok = __shfl_sync(0xffffffffu, (int)row_ok, pr);
+            if (ok)
+              *(uint4*)((__nv_bfloat16*)p.out + ro + col0 + part * 8) = *(const uint4*)(stg + pr * kStgPitch + part * 16);
+          }
+          __syncwarp();
+        } else if (row_ok) {
+          __nv_bfloat16* o = (__nv_bfloat16*)p.out + row_off + col0;
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) o[t] = __float2bfloat16_rn(f[t]);
         }
       }
       tc_fence_before();
@@ -371,10 +442,10 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, in
   }
 }
 
-template <int BN, int ESZ, int STAGES>
+template <int BN, int ESZ, int STAGES, bool RR = false>
 int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStream_t st) {
-  using S = Smem<BN, ESZ, STAGES>;
-  auto kern = umma_kernel<BN, ESZ, STAGES>;
+  using S = Smem<BN, ESZ, STAGES, RR>;
+  auto kern = umma_kernel<BN, ESZ, STAGES, RR>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
@@ -396,6 +467,17 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
   p.mt = mt;
   p.nt = nt;
   p.units = mt * nt * nz;
+  if (p.rr) {
+    if constexpr (ESZ == 2) {
+      switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
+        case 64:
+          return launch_umma<64, 2, 4, true>(a, b, p, st);
+        case 128:
+          return launch_umma<128, 2, 2, true>(a, b, p, st);
+      }
+    }
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "row-reuse conv needs bf16 and N <= 128");
+  }
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
       return launch_umma<64, ESZ, 4>(a, b, p, st);
@@ -438,6 +520,42 @@ int nhwc_map(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int c_
   uint32_t es[4] = {1, (uint32_t)cs, (uint32_t)cs, 1};
   return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, ptr, dims, strides, box, es,
                           CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Switch a single-class stride-1 conv gather to the row-reuse schedule when the tile shape allows it:
+// group class-0 taps by column offset, one A box of Ht + (dh range) rows per group. `act` is the
+// gathered NHWC tensor [N, Hin, Win, Cin].
+bool try_rowreuse(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int Win, int Cin, int BN) {
+  const char* env = getenv("NSK_CONV_RR");
+  if (!env || env[0] != '1') return false;  // opt-in until it beats the per-tap schedule
+  if (p.cs != 1 || p.Nt != 1 || p.Wt != p.Wo || (p.Wo % 8) || BN > 128 || p.ntaps[0] < 1) return false;
+  int dhmin = 127, dhmax = -128;
+  for (int t = 0; t < p.ntaps[0]; ++t) {
+    dhmin = p.tdh[0][t] < dhmin ? p.tdh[0][t] : dhmin;
+    dhmax = p.tdh[0][t] > dhmax ? p.tdh[0][t] : dhmax;
+  }
+  const int ext = p.Ht + dhmax - dhmin;
+  if (ext * p.Wt * 128 > kRRMaxA || ext > 256) return false;
+  int ng = 0;
+  for (int t = 0; t < p.ntaps[0]; ++t) {
+    int g = 0;
+    while (g < ng && p.gdw[0][g] != p.tdw[0][t]) ++g;
+    if (g == ng) {
+      p.gdw[0][g] = p.tdw[0][t];
+      p.gdhmin[0][g] = (signed char)dhmin;
+      p.gnt[0][g] = 0;
+      ++ng;
+    }
+    if (p.gnt[0][g] >= 3) return false;
+    p.gdh[0][g][p.gnt[0][g]] = p.tdh[0][t];
+    p.gw[0][g][p.gnt[0][g]] = p.tw[0][t];
+    ++p.gnt[0][g];
+  }
+  if (nhwc_map(ma, act, N, Hin, Win, Cin, 64, p.Wt, ext, 1, 1)) return false;
+  p.ngroups[0] = ng;
+  p.ext_rows = ext;
+  p.rr = 1;
+  return true;
 }
 
 int check_desc(const NskConvDesc* d) {
@@ -496,6 +614,7 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
   p.bias = bias;
   p.beta = beta;
   const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
+  if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
   return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
 }
@@ -541,6 +660,8 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
   p.out = y;
   p.ldc = d->K;
   p.out_f32 = y_f32;
+  try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN);
+  if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream);
 }
 
@@ -602,6 +723,7 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   p.out = dx;
   p.ldc = d->C;
   p.out_f32 = 0;
+  if (ncls == 1) try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN);
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream);
 }
 
