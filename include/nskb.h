@@ -170,6 +170,9 @@ int nsk_nhwc_to_nchw(int dtype_in, const void* x, float* y, int N, int C, int H,
 /* 3x3 (or RxS) im2col for small-channel stems: NHWC bf16 [N,H,W,C] -> [N*P*Q, Kp] bf16 with zero padding */
 int nsk_im2col(const void* x, void* out, int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q,
                int Kp, void* stream);
+/* fused NCHW float32 (host image layout) -> im2col bf16 rows for image stems (Kp % 8 == 0) */
+int nsk_im2col_nchw(const float* x, void* out, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
+                    int Q, int Kp, void* stream);
 /* adjoint of nsk_im2col: dx[n,h,w,c] (bf16) = sum of the fp32 dcols entries that read x[n,h,w,c] (gather) */
 int nsk_col2im(const void* dcols, void* dx, int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q,
                int Kp, void* stream);

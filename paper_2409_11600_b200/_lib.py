@@ -95,7 +95,8 @@ SIGNATURES = {
     "nsk_nchw_to_nhwc": (i32, [vp, vp, i32, i32, i32, i32, i32, vp]),
     "nsk_nhwc_to_nchw": (i32, [i32, vp, vp, i32, i32, i32, i32, i32, vp]),
     "nsk_im2col": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
-    "nsk_col2im": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
+    "nsk_im2col_nchw": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
+    "nsk_col2im":(i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
     "nsk_augment_crop_flip": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, i32, vp]),
     "nsk_embedding_fwd": (i32, [vp, vp, u64, i32, i32, vp, i32, vp, vp]),
     "nsk_embedding_bwd": (i32, [vp, i32, vp, u64, i32, vp, vp]),

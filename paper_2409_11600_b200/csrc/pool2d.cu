@@ -170,6 +170,42 @@ __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
   }
 }
 
+// Fused layout change + im2col for image stems: x is the host-layout NCHW float32 batch; each thread
+// writes 8 consecutive columns (one 16-byte store) of out[(n,p,q), k], k = (r*S + s)*C + c.
+__global__ void im2col_nchw_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int N, int C, int H,
+                                   int W, int R, int S, int st, int pad, int P, int Q, int Kp) {
+  const int groups = Kp / 8;
+  const long long n = (long long)N * P * Q * groups;
+  const int RSC = R * S * C;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % groups);
+    const long long pix = i / groups;
+    const int q = (int)(pix % Q);
+    const long long t = pix / Q;
+    const int p = (int)(t % P);
+    const long long b = t / P;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kk = g * 8 + e;
+      float val = 0.f;
+      if (kk < RSC) {
+        const int c = kk % C, rs = kk / C;
+        const int s = rs % S, r = rs / S;
+        const int h = p * st - pad + r, w = q * st - pad + s;
+        if (h >= 0 && h < H && w >= 0 && w < W) val = x[((b * C + c) * H + h) * W + w];
+      }
+      v[e] = val;
+    }
+    uint4 u;
+    u.x = pack_bf16x2(v[0], v[1]);
+    u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]);
+    u.w = pack_bf16x2(v[6], v[7]);
+    *(uint4*)(out + pix * Kp + g * 8) = u;
+  }
+}
+
 // col2im (gather form, deterministic): dx[n,h,w,c] = sum_{r,s: h = p*st-pad+r, w = q*st-pad+s} dcols[(n,p,q), k]
 __global__ void col2im_kernel(const float* __restrict__ dcols, __nv_bfloat16* __restrict__ dx, int N, int H,
                               int W, int C, int R, int S, int st, int pad, int P, int Q, int Kp) {
@@ -293,6 +329,16 @@ int nsk_im2col(const void* x, void* out, int N, int H, int W, int C, int R, int 
   im2col_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
       (const __nv_bfloat16*)x, (__nv_bfloat16*)out, N, H, W, C, R, S, stride, pad, P, Q, Kp);
   NSK_LAUNCH_CHECK("im2col");
+  return NSK_OK;
+}
+
+int nsk_im2col_nchw(const float* x, void* out, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
+                    int Q, int Kp, void* stream) {
+  if (Kp % 8) return nsk::set_error(NSK_ERR_UNSUPPORTED, "im2col_nchw: Kp must be a multiple of 8");
+  long long n = (long long)N * P * Q * (Kp / 8);
+  im2col_nchw_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)out, N, C, H, W, R,
+                                                                               S, stride, pad, P, Q, Kp);
+  NSK_LAUNCH_CHECK("im2col_nchw");
   return NSK_OK;
 }
 

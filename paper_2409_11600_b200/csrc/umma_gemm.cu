@@ -428,17 +428,37 @@ __global__ void __launch_bounds__(256, 1)
 // Both sides are contiguous in the (tap, cin) index: fully coalesced, fixed summation order.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M, int N, float* dw,
                                     float beta) {
-  const long long total = (long long)M * N;
+  // 4 consecutive (tap, cin) entries per thread (M % 4 == 0 since Cin % 64 == 0), splits folded in order
+  const long long total4 = (long long)M * N / 4;
   const long long plane = (long long)N * Mpad;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
+  for (long long i4 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i4 < total4;
+       i4 += (long long)gridDim.x * blockDim.x) {
+    const long long idx = i4 * 4;
     const int n = (int)(idx / M);
     const int m = (int)(idx - (long long)n * M);
     const float* src = ws + (long long)n * Mpad + m;
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += src[s * plane];
-    float* d = dw + idx;
-    *d = beta != 0.f ? acc + beta * *d : acc;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int s = 0;
+    for (; s + 4 <= splits; s += 4) {
+      float4 v0 = __ldg((const float4*)(src + (s + 0) * plane));
+      float4 v1 = __ldg((const float4*)(src + (s + 1) * plane));
+      float4 v2 = __ldg((const float4*)(src + (s + 2) * plane));
+      float4 v3 = __ldg((const float4*)(src + (s + 3) * plane));
+      acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+      acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
+      acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
+      acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
+    }
+    for (; s < splits; ++s) {
+      float4 v = __ldg((const float4*)(src + s * plane));
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4* d = (float4*)(dw + idx);
+    if (beta != 0.f) {
+      float4 o = *d;
+      acc.x += beta * o.x; acc.y += beta * o.y; acc.z += beta * o.z; acc.w += beta * o.w;
+    }
+    *d = acc;
   }
 }
 
@@ -801,8 +821,10 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   p.Mpad = Mpad;
   if ((rc = dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, (cudaStream_t)stream))) return rc;
   long long total = (long long)M * d->K;
-  wgrad_reduce_kernel<<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>((const float*)ws, splits, Mpad, M,
-                                                                                   d->K, dw, beta);
+  if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: dw and workspace must be 16-byte aligned");
+  wgrad_reduce_kernel<<<nsk::grid_for(total / 4, 256), 256, 0, (cudaStream_t)stream>>>((const float*)ws, splits, Mpad,
+                                                                                       M, d->K, dw, beta);
   NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
   return NSK_OK;
 }

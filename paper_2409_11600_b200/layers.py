@@ -56,11 +56,20 @@ def conv_out(h: int, k: int, stride: int, pad: int) -> int:
     return (h + 2 * pad - k) // stride + 1
 
 
-def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool) -> Tensor:
-    """y[n,p,q,k] = sum_{r,s,c} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]  (NHWC x KRSC -> NHWC, bf16)."""
+def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str = "nhwc") -> Tensor:
+    """y[n,p,q,k] = sum_{r,s,c} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]  (NHWC x KRSC -> NHWC, bf16).
+
+    ``layout="nchw"`` accepts a host-layout float32 image batch [N, C, H, W] directly (image stems:
+    the layout change is fused into the im2col gather; no input gradient)."""
     if x.rank != 4 or w.rank != 4:
         raise NskTypeError(f"conv2d needs NHWC input and KRSC filters, got {list(x.shape)} and {list(w.shape)}")
-    n, h, wd, c = x.shape
+    nchw = layout == "nchw"
+    if nchw:
+        n, c, h, wd = x.shape
+        if x.dtype != F32:
+            raise NskTypeError("conv2d(layout='nchw') expects a float32 image batch")
+    else:
+        n, h, wd, c = x.shape
     k, r, s, c2 = w.shape
     if c != c2:
         raise NskTypeError(f"conv2d channel mismatch: input has {c}, filters expect {c2}")
@@ -71,9 +80,9 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool) -> Tensor:
     y = empty_tensor(pool, (n, p, q, k), BF16)
     lib = _lib.lib()
     st = _lib.stream()
-    xp, xtmp = _temp_bf16(x, pool)
+    xp, xtmp = (x.ptr, None) if nchw else _temp_bf16(x, pool)
     wp = w.bf16_ptr() if w.dtype == F32 else w.ptr
-    if c % 64 == 0:
+    if c % 64 == 0 and not nchw:
         check(lib.nsk_conv2d_fprop(C.byref(desc), xp, wp, y.ptr, 0, st))
         saved = (x, w)
         attrs = {"desc": desc, "stem": False}
@@ -84,7 +93,10 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool) -> Tensor:
         rsc = r * s * c
         kp = (rsc + 63) // 64 * 64
         cols = empty_tensor(pool, (n * p * q, kp), BF16)
-        check(lib.nsk_im2col(xp, cols.ptr, n, h, wd, c, r, s, stride, pad, p, q, kp, st))
+        if nchw:
+            check(lib.nsk_im2col_nchw(xp, cols.ptr, n, c, h, wd, r, s, stride, pad, p, q, kp, st))
+        else:
+            check(lib.nsk_im2col(xp, cols.ptr, n, h, wd, c, r, s, stride, pad, p, q, kp, st))
         if xtmp is not None:
             release_tensor(pool, xtmp)
         wpk = empty_tensor(pool, (k, kp), BF16)
@@ -94,7 +106,7 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool) -> Tensor:
         release_tensor(pool, wpk)
         _internal_tensor(cols)
         saved = (cols, w)
-        attrs = {"desc": desc, "stem": True, "kp": kp}
+        attrs = {"desc": desc, "stem": True, "kp": kp, "nchw": nchw}
     record("conv2d", y, x, w, saved=saved, attrs=attrs)
     return y
 
@@ -110,6 +122,8 @@ def _r_conv2d(node, g, pool, sinks):
     if node.inputs[0].requires_grad:
         dx = empty_tensor(pool, tuple(node.inputs[0].tensor.shape), BF16)
         wb = w.bf16_ptr() if w.dtype == F32 else w.ptr
+        if node.attrs.get("nchw"):
+            raise NskRuntimeError("conv2d(layout='nchw') input is image data and has no gradient")
         if node.attrs["stem"]:
             # dcols[M, Kp] = dy[M, K] . Wp[K, Kp] (Wp MN-major), then the col2im gather
             kp = node.attrs["kp"]

@@ -59,10 +59,8 @@ class SmallCNN:
 
     def forward(self, x_nchw: Tensor) -> Tensor:
         pool, push = self.s.pool, self.s.push_named
-        x = layers.nchw_to_nhwc(x_nchw, pool)
-        push("cnn.x", x)
-        h = autodiff.rec_elementwise("relu", autodiff.rec_bias_add(layers.conv2d(x, self.w1, 1, 1, pool), self.b1,
-                                                                   pool), None, pool)
+        c1 = layers.conv2d(x_nchw, self.w1, 1, 1, pool, layout="nchw")
+        h = autodiff.rec_elementwise("relu", autodiff.rec_bias_add(c1, self.b1, pool), None, pool)
         push("cnn.h1", h)
         h = autodiff.rec_elementwise("relu", autodiff.rec_bias_add(layers.conv2d(h, self.w2, 2, 1, pool), self.b2,
                                                                    pool), None, pool)
@@ -101,9 +99,11 @@ class ResNet18:
 
     def forward(self, x_nchw: Tensor | None = None, x_nhwc: Tensor | None = None) -> Tensor:
         pool, push = self.s.pool, self.s.push_named
-        x = x_nhwc if x_nhwc is not None else layers.nchw_to_nhwc(x_nchw, pool)
-        push("rn.x", x)
-        h = layers.batchnorm(layers.conv2d(x, self.stem_w, 1, 1, pool), self.stem_bn, pool, relu=True)
+        if x_nhwc is not None:
+            stem = layers.conv2d(x_nhwc, self.stem_w, 1, 1, pool)
+        else:  # host-layout batch: the NCHW->NHWC change is fused into the stem's im2col gather
+            stem = layers.conv2d(x_nchw, self.stem_w, 1, 1, pool, layout="nchw")
+        h = layers.batchnorm(stem, self.stem_bn, pool, relu=True)
         push("rn.stem", h)
         for i, blk in enumerate(self.blocks):
             st = blk["stride"]
