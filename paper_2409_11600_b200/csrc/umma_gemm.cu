@@ -102,7 +102,7 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
   const int mi = r / p.nt;
   w.m0 = mi * 128;
   w.n0 = (r - mi * p.nt) * BN;
-  if (p.mode == MODE_WGRAD) {
+  if (p.mode == MODE_WGRAD || p.k_per_split > 0) {  // wgrad, or a split-K GEMM
     w.kb = w.z * p.k_per_split;
     int ke = min(p.k_steps, w.kb + p.k_per_split);
     w.nk = ke > w.kb ? ke - w.kb : 0;
@@ -334,7 +334,8 @@ __global__ void __launch_bounds__(256, 1)
         const long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
         row_off = pix * p.ldc;
       } else {
-        row_off = (long long)m * p.ldc;
+        // split-K GEMM: fp32 partials of split z into ws[z][M][N] (p.out / p.ldc set up by the host)
+        row_off = ((long long)(p.k_per_split > 0 ? w.z : 0) * p.M + m) * p.ldc;
       }
       int nchunks = (p.N - w.n0 + 31) / 32;
       if (nchunks > BN / 32) nchunks = BN / 32;
@@ -460,6 +461,52 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, in
     }
     *d = acc;
   }
+}
+
+// split-K GEMM fold: C[m, n] = sum_z ws[z][m][n] (+ bias[n]) (+ beta * C[m, n]), fp32 or bf16 out
+__global__ void splitk_fold_kernel(const float* __restrict__ ws, int splits, int M, int N, void* C, long long ldc,
+                                   int c_f32, const float* __restrict__ bias, float beta) {
+  const long long total = (long long)M * N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N), n = (int)(i - (long long)m * N);
+    float acc = 0.f;
+    for (int z = 0; z < splits; ++z) acc += ws[(long long)z * total + i];
+    if (bias) acc += bias[n];
+    if (c_f32) {
+      float* o = (float*)C + (long long)m * ldc + n;
+      *o = beta != 0.f ? acc + beta * *o : acc;
+    } else {
+      ((__nv_bfloat16*)C)[(long long)m * ldc + n] = __float2bfloat16_rn(acc);
+    }
+  }
+}
+
+// Library-owned grow-only scratch for split-K partials. Grows only outside stream capture (the first,
+// eager execution of a captured step sizes it).
+int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
+  static float* buf = nullptr;
+  static size_t cap = 0;
+  if (floats > cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return nsk::set_error(NSK_ERR_UNSUPPORTED, "gemm: split-K scratch must be sized before graph capture");
+    if (buf) {
+      cudaStreamSynchronize(st);
+      cudaFree(buf);
+    }
+    size_t want = floats < (1u << 20) ? (1u << 20) : floats;
+    if (cudaMalloc(&buf, want * sizeof(float)) != cudaSuccess) {
+      cudaGetLastError();
+      buf = nullptr;
+      cap = 0;
+      return nsk::set_error(NSK_ERR_OOM, "out of memory: gemm split-K scratch");
+    }
+    cap = want;
+  }
+  *out = buf;
+  return NSK_OK;
 }
 
 template <int BN, int ESZ, int STAGES, bool RR = false>
@@ -635,8 +682,34 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
   p.beta = beta;
   const int mt = (M + 127) / 128, nt = (N + BN - 1) / BN;
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
-  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
-  return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, (cudaStream_t)stream);
+  // Few output tiles but a long K (e.g. the stem's weight gradient, K = all pixels): split K across
+  // work units, fp32 partials in a library scratch, fixed-order fold (deterministic).
+  int splits = 1;
+  if (mt * nt * 2 <= nsk::sm_count() && p.k_steps >= 16) {
+    splits = nsk::sm_count() / (mt * nt);
+    if (splits > p.k_steps / 8) splits = p.k_steps / 8;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (splits > 1) {
+    const int per = (p.k_steps + splits - 1) / splits;
+    splits = (p.k_steps + per - 1) / per;
+    float* ws = nullptr;
+    if ((rc = gemm_scratch((size_t)splits * M * N, st, &ws))) return rc;
+    p.k_per_split = per;
+    p.out = ws;
+    p.ldc = N;
+    p.out_f32 = 1;
+    p.bias = nullptr;
+    p.beta = 0.f;
+    rc = esz == 2 ? dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, st) : dispatch_bn<4>(BN, ma, mb, p, mt, nt, splits, st);
+    if (rc) return rc;
+    const long long total = (long long)M * N;
+    splitk_fold_kernel<<<nsk::grid_for(total, 256), 256, 0, st>>>(ws, splits, M, N, C, ldc, c_f32, bias, beta);
+    NSK_LAUNCH_CHECK("splitk_fold_kernel");
+    return NSK_OK;
+  }
+  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, st);
+  return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, st);
 }
 
 // y[n,p,q,k] = sum_{c,r,s} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]   (NHWC / KRSC, bf16)
