@@ -562,6 +562,14 @@ int pick_bn(int N) {
   return 256;
 }
 
+// conv tiles: the widest N tile that still gives every SM a work unit (small late-stage grids
+// otherwise leave most of the 148 SMs idle: 4x4x512 at B=256 is only 32 M tiles)
+int pick_bn_units(int N, int m_tiles, int classes) {
+  int bn = pick_bn(N);
+  while (bn > 64 && 2 * m_tiles * classes * ((N + bn - 1) / bn) < nsk::sm_count()) bn /= 2;
+  return bn;
+}
+
 // pixel tile (Wt, Ht, Nt) covering `rows` consecutive output pixels in (n,h,w) raster order
 bool pixel_tile(int Wo, int Ho, int rows, int* Wt, int* Ht, int* Nt) {
   if (Wo > rows || rows % Wo != 0) return false;
@@ -720,7 +728,7 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
   int Wt, Ht, Nt;
   if (!pixel_tile(Q, P, 128, &Wt, &Ht, &Nt))
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d fprop: output width must tile 128 pixels");
-  const int BN = pick_bn(d->K);
+  const int BN = pick_bn_units(d->K, (d->N * P * Q + 127) / 128, 1);
   CUtensorMap ma, mb;
   if ((rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
   {
@@ -772,7 +780,7 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   int Wt, Ht, Nt;
   if (!pixel_tile(Wg, Hg, 128, &Wt, &Ht, &Nt))
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: input width must tile 128 pixels");
-  const int BN = pick_bn(d->C);
+  const int BN = pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, st * st);
   CUtensorMap ma, mb;
   if ((rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
   {
@@ -828,7 +836,7 @@ uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
   const int mt = Mpad / 128;
   const int BN = pick_bn(d->K);
   const int nt = (d->K + BN - 1) / BN;
-  int target = nsk::sm_count();  // one persistent wave of (m, n, split) units
+  int target = nsk::sm_count() * (BN <= 128 ? 2 : 1);  // one persistent wave (2 CTAs per SM for BN <= 128)
   int splits = target / (mt * nt);
   if (splits < 1) splits = 1;
   int max_splits = k_steps / 8 > 0 ? k_steps / 8 : 1;
