@@ -57,7 +57,7 @@ class Clocks:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -212,6 +212,8 @@ def ours_arm(args, rank, world, local_rank):
 
             dist.barrier()
 
+    dev = _lib.ctx.device
+    clk = Clocks(dev).__enter__()  # sampled from warm-up through the timed region (GPU under load)
     for _ in range(max(args.warmup, 3)):
         tr.step(x, y)
     barrier()
@@ -223,14 +225,13 @@ def ours_arm(args, rank, world, local_rank):
         e.append(ev.value)
     tr.stage(x, y)
     barrier()
-    dev = _lib.ctx.device
-    with Clocks(dev) as clk:
-        for i in range(args.steps):
-            flush.fill(float(i))
-            lib.nsk_event_record(e[2 * i], st)
-            tr.run_staged()
-            lib.nsk_event_record(e[2 * i + 1], st)
-        barrier()
+    for i in range(args.steps):
+        flush.fill(float(i))
+        lib.nsk_event_record(e[2 * i], st)
+        tr.run_staged()
+        lib.nsk_event_record(e[2 * i + 1], st)
+    barrier()
+    clk.__exit__(None, None, None)
     ms_steps = []
     for i in range(args.steps):
         ms = C.c_float()
@@ -283,7 +284,7 @@ def ours_arm(args, rank, world, local_rank):
         "gpu_launches": int(tr.launches_per_step * args.steps),
         "step_tflops_per_gpu": step_tflops,
         "step_frac_of_peak": step_tflops / pk_sus,
-        "roofline": {"bound": "tensor", "kernel": "umma_kernel<64,2,4> conv2d fprop 3x3 64->64, 256x32x32",
+        "roofline": {"bound": "tensor", "kernel": "umma_kernel<64,2,2,rr> conv2d fprop 3x3 64->64, 256x32x32",
                      "achieved": achieved, "peak": pk_burst, "unit": "TFLOP/s", "frac": achieved / pk_burst,
                      "traffic": profiled_traffic(), "peak_source": f"{src} bf16_tflops (burst, kernel timed alone)",
                      "algorithmic_flops_per_launch": flops, "launch_ms": kms},

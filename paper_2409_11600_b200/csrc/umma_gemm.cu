@@ -538,7 +538,7 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
     if constexpr (ESZ == 2) {
       switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
         case 64:
-          return launch_umma<64, 2, 4, true>(a, b, p, st);
+          return launch_umma<64, 2, 2, true>(a, b, p, st);
         case 128:
           return launch_umma<128, 2, 2, true>(a, b, p, st);
       }
@@ -602,7 +602,8 @@ int nhwc_map(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int c_
 // gathered NHWC tensor [N, Hin, Win, Cin].
 bool try_rowreuse(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int Win, int Cin, int BN) {
   const char* env = getenv("NSK_CONV_RR");
-  if (!env || env[0] != '1') return false;  // opt-in until it beats the per-tap schedule
+  if (env && env[0] == '0') return false;
+  if (BN != 64 && !(env && env[0] == '1')) return false;  // default: N=64 tiles (2 CTAs/SM); wider tiles lose stages
   if (p.cs != 1 || p.Nt != 1 || p.Wt != p.Wo || (p.Wo % 8) || BN > 128 || p.ntaps[0] < 1) return false;
   int dhmin = 127, dhmax = -128;
   for (int t = 0; t < p.ntaps[0]; ++t) {
