@@ -139,8 +139,9 @@ int nsk_argmax_correct(const float* logits, const float* labels, int m, int c, i
 int nsk_sgd_multi(int n_tensors, float* const* w, const float* const* g, float* const* v, void* const* w_bf16,
                   const uint64_t* numel, double lr, double momentum, float grad_scale, void* stream);
 int nsk_adamw_multi(int n_tensors, float* const* w, const float* const* g, float* const* m, float* const* v,
-                    void* const* w_bf16, const uint64_t* numel, int step, double lr, double wd, double beta1,
+                    void* const* w_bf16, const uint64_t* numel, int* step_dev, double lr, double wd, double beta1,
                     double beta2, double eps, const float* grad_scale_dev, void* stream);
+/* (step_dev: device int, incremented by the call before use -> bias corrections for t = 1, 2, ...) */
 int nsk_sqnorm_multi(int n_tensors, const float* const* g, const uint64_t* numel, double* out, void* stream);
 /* (out must hold 1 + 1024 doubles; out[0] = sum of squares in float64) */
 /* scale_dev[0] = (norm > max_norm) ? max_norm/norm : 1, norm = sqrt(*sqnorm) ; optional in-place scaling */
@@ -182,11 +183,23 @@ int nsk_augment_crop_flip(const uint8_t* img, const int32_t* offs, void* out, in
                           const float* mean, const float* std, int Cp, void* stream);
 
 /* ---- sequence ops (embed.cu, gru.cu) ---- */
-int nsk_embedding_fwd(const float* table, const int32_t* tokens, uint64_t n, int E, int dtype_out, void* out,
-                      int V, int* err_flag, void* stream);
-int nsk_embedding_bwd(const void* dout, int dtype_in, const int32_t* tokens, uint64_t n, int E, float* dtable,
+/* rows of `table` [V, E] gathered by float32 token ids (reference data tensors are float32); with seq_T > 0
+ * ids are [B][T] and output row t*B+b holds token [b][t] (time-major for the recurrence). err_flag gets the
+ * first bad row (non-integer or out of [0, V)). Backward scatter-adds into dtable (fp32 atomics). */
+int nsk_embedding_fwd(const float* table, const float* tokens, uint64_t n, int E, int V, int seq_T, int dtype_out,
+                      void* out, int* err_flag, void* stream);
+int nsk_embedding_bwd(const void* dout, int dtype_in, const float* tokens, uint64_t n, int E, int seq_T, float* dtable,
                       void* stream);
-
+/* fused GRU recurrence (one cooperative persistent launch for all T steps):
+ * gx [T, B, 3H] input projections incl. b (gates r, z, n), U [3H, H], c [3H];
+ * hs [T+1, B, H] with hs[0] = h0 (caller-filled); gates [T, B, 4H] = (r, z, n, h.U_n^T + c_n) */
+int nsk_gru_fwd(const float* gx, const float* U, const float* c, int T, int B, int H, float* hs, float* gates,
+                void* stream);
+/* BPTT: dhs [T, B, H] external gradients of h_1..h_T; writes dgx [T, B, 3H] (d pre-activations of gx),
+ * dgh [T, B, 3H] (d of h.U^T + c: r, z, n-part), dh0 [B, H]. ws: nsk_gru_bwd_workspace bytes. */
+uint64_t nsk_gru_bwd_workspace(int T, int B, int H);
+int nsk_gru_bwd(const float* dhs, const float* U, const float* hs, const float* gates, int T, int B, int H, float* dgx,
+                float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream);
 
 /* ---- communication (comm.cu): NCCL over NVLink / NVSwitch ---- */
 int nsk_comm_unique_id(uint8_t* out128);

@@ -201,3 +201,74 @@ class ResNet18Oracle:
         loss, grads, _ = self.loss_and_grads(x_nchw, y, bf16=bf16)
         self.opt.sgd(self.params, grads, lr, momentum)
         return loss
+
+
+def _sig(z):
+    return R.stable_sigmoid(z).astype(np.float64)
+
+
+class GRUOracle:
+    """C3 GRU classifier composed from the reference primitives, float64.
+
+    Same declaration order and seed draws as paper_2409_11600_b200.models.GRUClassifier:
+    E = xavier(E, V) (gathered as E^T rows), W_r, W_z, W_n = xavier(H, E), b = 0, U_r, U_z, U_n =
+    xavier(H, H), c = 0, head = xavier(classes, H), head bias 0.
+    """
+
+    def __init__(self, seed=0, vocab=32768, embed=512, hidden=512, classes=2):
+        rng = np.random.default_rng(seed)
+        draw = lambda r, c: R.xavier_uniform(r, c, int(rng.integers(0, 2**31 - 1)))  # noqa: E731
+        self.H = hidden
+        self.params = {"table": np.ascontiguousarray(draw(embed, vocab).T)}
+        self.params["w"] = np.concatenate([draw(hidden, embed) for _ in range(3)])
+        self.params["b"] = np.zeros(3 * hidden, np.float32)
+        self.params["u"] = np.concatenate([draw(hidden, hidden) for _ in range(3)])
+        self.params["c"] = np.zeros(3 * hidden, np.float32)
+        self.params["head_w"] = draw(classes, hidden)
+        self.params["head_b"] = np.zeros(classes, np.float32)
+        self.order = ["table", "w", "b", "u", "c", "head_w", "head_b"]
+
+    def loss_and_grads(self, tokens, y):
+        p = {k: v.astype(np.float64) for k, v in self.params.items()}
+        H = self.H
+        tok = np.asarray(tokens).astype(np.int64)  # [B, T]
+        B, T = tok.shape
+        W, b, U, c = p["w"], p["b"], p["u"], p["c"]
+        xs = [p["table"][tok[:, t]] for t in range(T)]
+        h = np.zeros((B, H))
+        cache = []
+        for t in range(T):
+            gx = xs[t] @ W.T + b
+            gh = h @ U.T + c
+            r = _sig(gx[:, :H] + gh[:, :H])
+            z = _sig(gx[:, H:2 * H] + gh[:, H:2 * H])
+            a = gh[:, 2 * H:]
+            n = np.tanh(gx[:, 2 * H:] + r * a)
+            hn = n - z * n + z * h
+            cache.append((h, r, z, n, a))
+            h = hn
+        logits = (h @ p["head_w"].T + p["head_b"]).astype(np.float32)
+        loss, probs = R.cross_entropy(logits, y)
+        g = R.cross_entropy_grad(probs, y).astype(np.float64)
+        grads = {"head_b": g.sum(axis=0), "head_w": g.T @ h}
+        dh = g @ p["head_w"]
+        gW, gU = np.zeros_like(W), np.zeros_like(U)
+        gb, gc = np.zeros_like(b), np.zeros_like(c)
+        gtable = np.zeros_like(p["table"])
+        for t in reversed(range(T)):
+            hp, r, z, n, a = cache[t]
+            dn = dh * (1 - z)
+            dz = dh * (hp - n)
+            dnp = dn * (1 - n * n)
+            drp = dnp * a * r * (1 - r)
+            dzp = dz * z * (1 - z)
+            dgx = np.concatenate([drp, dzp, dnp], axis=1)
+            dgh = np.concatenate([drp, dzp, dnp * r], axis=1)
+            gW += dgx.T @ xs[t]
+            gb += dgx.sum(axis=0)
+            gU += dgh.T @ hp
+            gc += dgh.sum(axis=0)
+            np.add.at(gtable, tok[:, t], dgx @ W)
+            dh = dh * z + dgh @ U
+        grads.update({"w": gW, "b": gb, "u": gU, "c": gc, "table": gtable})
+        return loss, grads, logits

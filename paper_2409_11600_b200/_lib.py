@@ -81,7 +81,7 @@ SIGNATURES = {
     "nsk_fill_like_scalar": (i32, [vp, vp, u64, vp]),
     "nsk_argmax_correct": (i32, [vp, vp, i32, i32, vp, vp]),
     "nsk_sgd_multi": (i32, [i32, vp, vp, vp, vp, vp, f64, f64, f32, vp]),
-    "nsk_adamw_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, i32, f64, f64, f64, f64, f64, vp, vp]),
+    "nsk_adamw_multi": (i32, [i32, vp, vp, vp, vp, vp, vp, vp, f64, f64, f64, f64, f64, vp, vp]),
     "nsk_sqnorm_multi": (i32, [i32, vp, vp, vp, vp]),
     "nsk_clip_scale": (i32, [vp, f32, vp, vp]),
     "nsk_scale_multi": (i32, [i32, vp, vp, vp, vp]),
@@ -98,10 +98,10 @@ SIGNATURES = {
     "nsk_im2col_nchw": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
     "nsk_col2im":(i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
     "nsk_augment_crop_flip": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, vp, vp, i32, vp]),
-    "nsk_embedding_fwd": (i32, [vp, vp, u64, i32, i32, vp, i32, vp, vp]),
-    "nsk_embedding_bwd": (i32, [vp, i32, vp, u64, i32, vp, vp]),
-    "nsk_gru_fwd": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp]),
-    "nsk_gru_bwd": (i32, [vp, vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, u64, vp]),
+    "nsk_embedding_fwd": (i32, [vp, vp, u64, i32, i32, i32, i32, vp, vp, vp]),
+    "nsk_embedding_bwd": (i32, [vp, i32, vp, u64, i32, i32, vp, vp]),
+    "nsk_gru_fwd": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
+    "nsk_gru_bwd": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
     "nsk_gru_bwd_workspace": (u64, [i32, i32, i32]),
     "nsk_comm_unique_id": (i32, [vp]),
     "nsk_comm_init": (i32, [i32, i32, vp, C.POINTER(vp)]),

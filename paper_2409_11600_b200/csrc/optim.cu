@@ -32,9 +32,20 @@ __global__ void sgd_kernel(float* const* w, const float* const* g, float* const*
   }
 }
 
+// the optimizer step counter lives on the device so a captured step graph replays with t = 1, 2, 3, ...
+__global__ void step_inc_kernel(int* step) { step[0] += 1; }
+
 __global__ void adamw_kernel(float* const* w, const float* const* g, float* const* m, float* const* v, void* const* wb,
-                             const uint64_t* numel, double lr, double wd, double b1, double b2, double eps, double bc1,
-                             double bc2, const float* gscale_dev) {
+                             const uint64_t* numel, double lr, double wd, double b1, double b2, double eps,
+                             const int* step_dev, const float* gscale_dev) {
+  __shared__ double bc[2];
+  if (threadIdx.x == 0) {
+    const double st = (double)step_dev[0];
+    bc[0] = 1.0 - pow(b1, st);  // same libm pow as the reference's b1 ** t (nn.py:116-117)
+    bc[1] = 1.0 - pow(b2, st);
+  }
+  __syncthreads();
+  const double bc1 = bc[0], bc2 = bc[1];
   const int t = blockIdx.y;
   const uint64_t n = numel[t];
   float* W = w[t];
@@ -125,13 +136,12 @@ int nsk_sgd_multi(int nt, float* const* w, const float* const* g, float* const* 
 }
 
 int nsk_adamw_multi(int nt, float* const* w, const float* const* g, float* const* m, float* const* v,
-                    void* const* wb, const uint64_t* numel, int step, double lr, double wd, double beta1,
+                    void* const* wb, const uint64_t* numel, int* step_dev, double lr, double wd, double beta1,
                     double beta2, double eps, const float* grad_scale_dev, void* stream) {
   if (nt < 1) return NSK_OK;
-  double b1 = beta1, b2 = beta2;
-  double bc1 = 1.0 - pow(b1, (double)step), bc2 = 1.0 - pow(b2, (double)step);
+  step_inc_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_dev);
   dim3 grid(blocks_x(nt), nt);
-  adamw_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, m, v, wb, numel, lr, wd, b1, b2, eps, bc1, bc2,
+  adamw_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, m, v, wb, numel, lr, wd, beta1, beta2, eps, step_dev,
                                                        grad_scale_dev);
   NSK_LAUNCH_CHECK("adamw_multi");
   return NSK_OK;

@@ -314,3 +314,124 @@ def nchw_to_nhwc(x: Tensor, pool: Pool, channels_pad: int | None = None) -> Tens
 @rule("layout")
 def _r_layout(node, g, pool, sinks):
     raise NskRuntimeError("nchw_to_nhwc is a data-preparation op and has no gradient")
+
+
+# --- sequence ops: embedding + fused GRU -------------------------------------------------------------
+
+def embedding(tokens: Tensor, table: Tensor, pool: Pool) -> Tensor:
+    """tokens [B, T] (float ids, as loaded) -> rows of table [V, E], time-major [T*B, E] float32.
+
+    Equals onehot(tokens) @ E exactly (a one-term float64 sum), the reference's embedding path
+    (tensor.py:299-317 + :213-229); range errors keep onehot's message."""
+    from .tensor import check_index_values, device_index_check
+
+    if tokens.rank != 2 or table.rank != 2:
+        raise NskTypeError(f"embedding needs [B, T] tokens and a [V, E] table, got {list(tokens.shape)}, "
+                           f"{list(table.shape)}")
+    b, t = tokens.shape
+    v, e = table.shape
+    if tokens.host_src is not None:
+        check_index_values(tokens.host_src, v, "onehot")
+    else:
+        device_index_check(Tensor((b * t,), tokens.buffer), v, "onehot")
+    out = empty_tensor(pool, (t * b, e), F32)
+    check(_lib.lib().nsk_embedding_fwd(table.ptr, tokens.ptr, b * t, e, v, t, F32, out.ptr, None, _lib.stream()))
+    record("embedding", out, tokens, table, saved=(tokens,), attrs={"T": t, "V": v})
+    return out
+
+
+@rule("embedding")
+def _r_embedding(node, g, pool, sinks):
+    (tokens,) = node.saved
+    v, e = node.inputs[1].tensor.shape
+    if sinks[1] is not None:
+        out_ptr, dt = sinks[1].ptr, SUNK  # scatter-add straight into the cached gradient
+    else:
+        dt = empty_tensor(pool, (v, e), F32)
+        dt.buffer.fill(0.0)
+        out_ptr = dt.ptr
+    check(_lib.lib().nsk_embedding_bwd(g.ptr, g.dtype, tokens.ptr, tokens.numel, e, node.attrs["T"], out_ptr,
+                                       _lib.stream()))
+    return [None, dt]
+
+
+GRU_WS = Workspace()
+
+
+def gru(x: Tensor, w: Tensor, b: Tensor, u: Tensor, c: Tensor, steps: int, pool: Pool) -> Tensor:
+    """Fused GRU over a time-major input x [T*B, E] -> final hidden state h_T [B, H] (h_0 = 0).
+
+    w [3H, E], b [3H], u [3H, H], c [3H] stack the (r, z, n) gates. Same function as the reference
+    composition r = s(x W_r^T + b_r + h U_r^T + c_r), z likewise, n = tanh(x W_n^T + b_n + r (h U_n^T + c_n)),
+    h' = n - z n + z h; input projections for all steps are one tcgen05 GEMM."""
+    from .tensor import _gemm
+
+    tb, e = x.shape
+    h3, e2 = w.shape
+    h = h3 // 3
+    if e2 != e or h3 % 3 or u.shape != (h3, h) or b.shape != (h3,) or c.shape != (h3,) or tb % steps:
+        raise NskTypeError("gru: inconsistent shapes")
+    bsz = tb // steps
+    lib, st = _lib.lib(), _lib.stream()
+    gx = empty_tensor(pool, (tb, h3), F32)
+    _gemm(x.ptr, 0, e, w.ptr, 0, e, tb, h3, e, gx.ptr, h3, dtype=F32, bias_ptr=b.ptr)
+    hs = _internal_tensor(empty_tensor(pool, ((steps + 1) * bsz, h), F32))
+    check(lib.nsk_fill_f32(hs.ptr, bsz * h, 0.0, st))
+    gates = _internal_tensor(empty_tensor(pool, (tb, 4 * h), F32))
+    check(lib.nsk_gru_fwd(gx.ptr, u.ptr, c.ptr, steps, bsz, h, hs.ptr, gates.ptr, st))
+    release_tensor(pool, gx)
+    out = empty_tensor(pool, (bsz, h), F32)
+    check(lib.nsk_memcpy_d2d(out.ptr, hs.ptr + 4 * steps * bsz * h, 4 * bsz * h, st))
+    record("gru", out, x, w, b, u, c, saved=(x, hs, gates, w, u), attrs={"T": steps, "B": bsz, "H": h, "E": e})
+    return out
+
+
+@rule("gru")
+def _r_gru(node, g, pool, sinks):
+    from .tensor import _gemm, _Operands
+
+    x, hs, gates, w, u = node.saved
+    T, B, H, E = (node.attrs[k] for k in ("T", "B", "H", "E"))
+    H3, TB = 3 * H, T * B
+    lib, st = _lib.lib(), _lib.stream()
+    dhs = empty_tensor(pool, (TB, H), F32)
+    check(lib.nsk_fill_f32(dhs.ptr, (T - 1) * B * H, 0.0, st))
+    check(lib.nsk_memcpy_d2d(dhs.ptr + 4 * (T - 1) * B * H, g.ptr, 4 * B * H, st))
+    dgx = empty_tensor(pool, (TB, H3), F32)
+    dgh = empty_tensor(pool, (TB, H3), F32)
+    dh0 = empty_tensor(pool, (B, H), F32)
+    ws = GRU_WS.get(lib.nsk_gru_bwd_workspace(T, B, H))
+    check(lib.nsk_gru_bwd(dhs.ptr, u.ptr, hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr, ws.nbytes,
+                          st))
+    release_tensor(pool, dhs)
+    release_tensor(pool, dh0)
+    outs = [None] * 5
+
+    def target(i, shape):
+        if sinks[i] is not None:
+            return sinks[i].ptr, 1.0, SUNK
+        t = empty_tensor(pool, shape, F32)
+        return t.ptr, 0.0, t
+
+    # bf16 operands, fp32 accumulation for the batched weight / input gradients (K = T*B steps)
+    hprev = Tensor((TB, H), Buffer(TB * H, F32, base=hs.buffer, offset=0))
+    with _Operands(pool, BF16, dgx, dgh, x, w, hprev) as (pgx, pgh, px, pw, ph):
+        if node.inputs[0].requires_grad:
+            dx = empty_tensor(pool, (TB, E), F32)
+            _gemm(pgx, 0, H3, pw, 1, E, TB, E, H3, dx.ptr, E, dtype=BF16)  # dx = dgx . W
+            outs[0] = dx
+        if node.inputs[1].requires_grad:
+            ptr, beta, outs[1] = target(1, (H3, E))
+            _gemm(pgx, 1, H3, px, 1, E, H3, E, TB, ptr, E, dtype=BF16, beta=beta)  # dW = dgx^T . x
+        if node.inputs[3].requires_grad:
+            ptr, beta, outs[3] = target(3, (H3, H))
+            _gemm(pgh, 1, H3, ph, 1, H, H3, H, TB, ptr, H, dtype=BF16, beta=beta)  # dU = dgh^T . h_{t-1}
+    if node.inputs[2].requires_grad:
+        ptr, beta, outs[2] = target(2, (H3,))
+        check(lib.nsk_colsum(F32, dgx.ptr, ptr, TB, H3, beta, st))
+    if node.inputs[4].requires_grad:
+        ptr, beta, outs[4] = target(4, (H3,))
+        check(lib.nsk_colsum(F32, dgh.ptr, ptr, TB, H3, beta, st))
+    release_tensor(pool, dgx)
+    release_tensor(pool, dgh)
+    return outs

@@ -138,3 +138,50 @@ def resnet18_train_flops_per_image() -> float:
             h, cin = ho, cout
     macs += 512 * 10
     return 2.0 * (3 * macs - stem)
+
+
+class GRUClassifier:
+    """C3: token embedding -> fused GRU (h_0 = 0) -> linear head on h_T -> cross-entropy.
+
+    Parameters follow the reference composition: the embedding is onehot(tok) @ E with
+    E = xavier_uniform(E, V) (stored transposed as a [V, E] gather table), and each gate has its own
+    xavier_uniform(H, E) input weight and xavier_uniform(H, H) recurrent weight (seed draws in the order
+    r, z, n), stacked here into W [3H, E] / U [3H, H]; biases b, c start at zero.
+    """
+
+    def __init__(self, session: Session, vocab: int = 32768, embed: int = 512, hidden: int = 512,
+                 classes: int = 2):
+        s = session
+        self.s = s
+        self.input_classes = vocab  # Trainer validates token ids on the host
+        e_vals = nn.xavier_values(embed, vocab, s.new_seed())
+        self.table = self._param(np.ascontiguousarray(e_vals.T))
+        self.w = self._param(np.concatenate([nn.xavier_values(hidden, embed, s.new_seed()) for _ in range(3)]))
+        self.b = self._param(np.zeros(3 * hidden, np.float32))
+        self.u = self._param(np.concatenate([nn.xavier_values(hidden, hidden, s.new_seed()) for _ in range(3)]))
+        self.c = self._param(np.zeros(3 * hidden, np.float32))
+        self.head_w = self._param(nn.xavier_values(classes, hidden, s.new_seed()))
+        self.head_b = self._param(np.zeros(classes, np.float32))
+
+    def _param(self, values):
+        name = self.s.new_param_name()
+        t = autodiff.make_param(self.s.pool, values, name)
+        self.s.param_group.add(name, t)
+        return t
+
+    def forward(self, tokens: Tensor) -> Tensor:
+        pool, push = self.s.pool, self.s.push_named
+        steps = tokens.shape[1]
+        x = layers.embedding(tokens, self.table, pool)
+        push("gru.x", x)
+        h = layers.gru(x, self.w, self.b, self.u, self.c, steps, pool)
+        push("gru.h", h)
+        logits = nn.linear(h, self.head_w, self.head_b, pool)
+        push("gru.logits", logits)
+        return logits
+
+
+def gru_train_flops_per_seq(steps: int = 128, embed: int = 512, hidden: int = 512, classes: int = 2) -> float:
+    """Dense-GEMM training FLOPs per sequence (1.208 GFLOP at T=128, E=H=512)."""
+    fwd = steps * (3 * hidden * embed + 3 * hidden * hidden) + classes * hidden
+    return 2.0 * 3 * fwd

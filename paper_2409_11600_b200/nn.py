@@ -65,6 +65,15 @@ class ParamGroup:
         self.grad_scale = 1.0  # data-parallel averaging (1/world) folded into the update
         self.flat = None
         self.auto_flatten = True
+        self.step_dev = None
+        self._scale_buf = None
+
+    def scale_dev(self) -> Buffer:
+        """Device float holding grad_scale (data-parallel 1/N), created once outside graph capture."""
+        if self._scale_buf is None:
+            self._scale_buf = Buffer(1, F32)
+            self._scale_buf.fill(float(self.grad_scale))
+        return self._scale_buf
 
     def add(self, name: str, tensor: Tensor) -> None:
         self.params.append((name, tensor))
@@ -206,20 +215,21 @@ def sgd_step(group: ParamGroup, cache: GradCache, lr: float, momentum: float = 0
     group._after_update()
 
 
-def adamw_step(group: ParamGroup, cache: GradCache, hp: Hyperparams, grad_scale_dev: int | None = None) -> None:
+def adamw_step(group: ParamGroup, cache: GradCache, hp: Hyperparams, grad_scale_dev: int | None = None,
+               apply_group_scale: bool = True) -> None:
     """Decoupled weight decay, then the bias-corrected Adam update (nn.py:102-119)."""
     group.step_count += 1
-    t = group.step_count
     tab, nt = group._table("adamw", cache, ("m", "v"))
-    scale_ptr = grad_scale_dev
-    if scale_ptr is None and group.grad_scale != 1.0:
-        slot = SCALARS.take()
-        arr = np.array([group.grad_scale], np.float32)
-        check(_lib.lib().nsk_memcpy_h2d(SCALARS.ptr(slot), arr.ctypes.data, 4, _lib.stream()))
+    if group.step_dev is None:  # device copy of step_count: captured graphs replay with t = 1, 2, ...
+        group.step_dev = Buffer(1, F32)
+        arr = np.array([group.step_count - 1], np.int32)
+        check(_lib.lib().nsk_memcpy_h2d(group.step_dev.ptr, arr.ctypes.data, 4, _lib.stream()))
         _lib.sync()
-        scale_ptr = SCALARS.ptr(slot)
+    scale_ptr = grad_scale_dev
+    if scale_ptr is None and apply_group_scale and group.grad_scale != 1.0:
+        scale_ptr = group.scale_dev().ptr
     check(_lib.lib().nsk_adamw_multi(nt, tab["w"].ptr, tab["g"].ptr, tab["m"].ptr, tab["v"].ptr,
-                                     tab["b"].ptr, tab["n"].ptr, t, float(hp.learning_rate),
+                                     tab["b"].ptr, tab["n"].ptr, group.step_dev.ptr, float(hp.learning_rate),
                                      float(hp.weight_decay), float(hp.beta1), float(hp.beta2), float(hp.epsilon),
                                      scale_ptr, _lib.stream()))
     group._after_update()
@@ -252,7 +262,7 @@ def clip_grad_norm(cache: GradCache, max_norm: float) -> DeviceScalar:
     tab = _CLIP.tables.get(key)
     if tab is None:
         tab = (DeviceTable(ptrs), DeviceTable(sizes))
-        _CLIP.tables = {key: tab}
+        _CLIP.tables[key] = tab
     if _CLIP.sq is None:
         _CLIP.sq = Buffer(2 * 1025, F32)
     slot = SCALARS.take()
@@ -262,3 +272,24 @@ def clip_grad_norm(cache: GradCache, max_norm: float) -> DeviceScalar:
     check(lib.nsk_clip_scale(_CLIP.sq.ptr, float(max_norm), SCALARS.ptr(slot), st))
     check(lib.nsk_scale_multi(len(ptrs), tab[0].ptr, tab[1].ptr, SCALARS.ptr(slot), st))
     return DeviceScalar(slot)
+
+
+def xavier_values(rows: int, cols: int, seed: int) -> np.ndarray:
+    """The float32 values xavier_uniform_init draws (nn.py:60-71), without making a tensor."""
+    a = math.sqrt(6.0 / (rows + cols))
+    return np.random.default_rng(seed).uniform(-a, a, size=(rows, cols)).astype(np.float32)
+
+
+def scale_grads(cache: GradCache, scale_dev: Buffer) -> None:
+    """In-place g *= scale for every cached gradient (data-parallel averaging ahead of clipping)."""
+    if cache.arena is not None and len(cache.offsets) == len(cache.grads):
+        ptrs, sizes = [cache.arena.ptr], [cache.arena.capacity]
+    else:
+        ptrs = [b.ptr for b in cache.grads.values()]
+        sizes = [b.capacity for b in cache.grads.values()]
+    key = ("scale",) + tuple(ptrs)
+    tab = _CLIP.tables.get(key)
+    if tab is None:
+        tab = (DeviceTable(ptrs), DeviceTable(sizes))
+        _CLIP.tables[key] = tab
+    check(_lib.lib().nsk_scale_multi(len(ptrs), tab[0].ptr, tab[1].ptr, scale_dev.ptr, _lib.stream()))

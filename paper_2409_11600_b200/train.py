@@ -109,6 +109,10 @@ class Trainer:
         for t in (self.x_dev, self.y_dev):
             t.refs = 1  # external hold: the traversal never returns these to the pool
         self.y_dev.host_src = self.y_pin.array
+        # token models: ids are validated on the host at staging time (sync-free inside the step)
+        self.input_classes = getattr(model, "input_classes", None)
+        if self.input_classes is not None:
+            self.x_dev.host_src = self.x_pin.array
         self.steps_done = 0
         self.graph: StepGraph | None = None
         self.loss_slot: int | None = None
@@ -133,10 +137,11 @@ class Trainer:
             nn.sgd_step(s.param_group, s.grad_cache, self.opt[1], self.opt[2])
         elif kind == "adamw":
             hp, clip = self.opt[1], self.opt[2]
-            scale = None
+            if self.dp is not None:  # average before the norm is taken (clip sees the global gradient)
+                nn.scale_grads(s.grad_cache, s.param_group.scale_dev())
             if clip is not None:
-                scale = nn.clip_grad_norm(s.grad_cache, clip)
-            nn.adamw_step(s.param_group, s.grad_cache, hp)
+                nn.clip_grad_norm(s.grad_cache, clip)
+            nn.adamw_step(s.param_group, s.grad_cache, hp, apply_group_scale=False)
         else:
             raise NskRuntimeError(f"unknown optimizer {kind!r}")
         s.grad_cache.zero_after_step()
@@ -148,6 +153,8 @@ class Trainer:
         """Host batch -> pinned -> device (async on the compute stream)."""
         y = np.asarray(y_host, dtype=np.float32).reshape(-1)
         check_index_values(y, self.classes, "target")
+        if self.input_classes is not None:
+            check_index_values(np.asarray(x_host, dtype=np.float32), self.input_classes, "onehot")
         lib, st = _lib.lib(), _lib.stream()
         if self._copied is None:
             ev = C.c_void_p()

@@ -1,0 +1,66 @@
+"""C3: fused GRU classifier (embedding -> GRU -> head -> CE) vs the float64 oracle composed from reference primitives."""
+
+import numpy as np
+import pytest
+
+from oracle import models as om
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("V,E,H,T,B", [(50, 64, 64, 6, 4), (1000, 128, 128, 32, 16)])
+def test_gru_loss_and_gradients_match_oracle(session, V, E, H, T, B):
+    from paper_2409_11600_b200 import autodiff, nn
+    from paper_2409_11600_b200.models import GRUClassifier
+
+    rng = np.random.default_rng(V + T)
+    tokens = rng.integers(0, V, (B, T)).astype(np.float32)
+    y = rng.integers(0, 2, B).astype(np.float32)
+    model = GRUClassifier(session, vocab=V, embed=E, hidden=H)
+    ref = om.GRUOracle(seed=0, vocab=V, embed=E, hidden=H)
+    for (n, t), key in zip(session.param_group.params, ref.order):
+        np.testing.assert_array_equal(t.data, ref.params[key])
+    pool = session.pool
+    logits = model.forward(autodiff.make_data(pool, tokens))
+    dl = logits.data
+    loss = nn.cross_entropy(logits, autodiff.make_data(pool, y), pool)
+    session.push_named("loss", loss)
+    lv = loss.item()
+    autodiff.backward(session.tape(), session.grad_cache, pool)
+    ref_loss, grads, ref_logits = ref.loss_and_grads(tokens, y)
+    tf32 = T * B * E * 3 * H >= (1 << 24)  # large input projections run on the tensor cores in tf32
+    assert rel(dl, ref_logits) < (2e-3 if tf32 else 1e-4)
+    assert lv == pytest.approx(ref_loss, rel=1e-4 if tf32 else 1e-5)
+    exact = 3e-3 if tf32 else 1e-4  # fp32 SIMT / colsum paths (inherit the tf32 forward when it is used)
+    tol = {"table": 1e-2, "w": 1e-2, "u": 1e-2, "b": exact, "c": exact, "head_w": exact, "head_b": exact}
+    for (n, _t), key in zip(session.param_group.params, ref.order):
+        e = rel(session.grad_cache.get(n), grads[key])
+        assert e < tol[key], (key, e)
+
+
+def test_gru_trainer_graph_replay_with_adamw_clip(dev):
+    """AdamW + clip_grad_norm step captured as one graph replays like eager (device step counter)."""
+    from paper_2409_11600_b200 import nn
+    from paper_2409_11600_b200.models import GRUClassifier
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    rng = np.random.default_rng(3)
+    V, T, B = 500, 16, 8
+    xs = [rng.integers(0, V, (B, T)).astype(np.float32) for _ in range(5)]
+    ys = [rng.integers(0, 2, B).astype(np.float32) for _ in range(5)]
+    losses = {}
+    for mode in (False, True):
+        s = Session(seed=0)
+        model = GRUClassifier(s, vocab=V, embed=64, hidden=64)
+        opt = ("adamw", nn.Hyperparams(learning_rate=1e-3, weight_decay=1e-4), 5.0)
+        tr = Trainer(s, model, (B, T), 2, optimizer=opt, graph=mode, warmup=2)
+        losses[mode] = [float(tr.step(x, y)) for x, y in zip(xs, ys)]
+        if mode:
+            assert tr.graph is not None
+    np.testing.assert_allclose(losses[True], losses[False], rtol=1e-5)
