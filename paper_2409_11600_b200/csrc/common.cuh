@@ -43,6 +43,10 @@ int sm_count();
 int encode_tmap(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* gaddr,
                 const uint64_t* dims, const uint64_t* strides_bytes, const uint32_t* box,
                 const uint32_t* elem_strides, CUtensorMapSwizzle swz);
+// im2col-mode map over an NHWC bf16 tensor: 64 channels (128 B, 128B-swizzled) x `pixels` output
+// positions per load, traversing the (W, H) bounding box [lower, dim - 1 + upper] with `stride`.
+int encode_tmap_im2col(CUtensorMap* map, const void* gaddr, int N, int H, int W, int C, const int* lower_wh,
+                       const int* upper_wh, int pixels, int stride);
 
 inline unsigned grid_for(int64_t n, int block, int per_thread = 1) {
   int64_t g = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
@@ -113,6 +117,17 @@ __device__ __forceinline__ void tma_load_4d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
       "[%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// im2col-mode load: (c, w, h, n) is the bounding-box position of the first pixel; (ow, oh) the filter-tap
+// offset added to every pixel of the column.
+__device__ __forceinline__ void tma_load_4d_im2col(const CUtensorMap* map, uint64_t* bar, void* dst, int c, int w,
+                                                   int h, int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
       : "memory");
 }
 

@@ -82,6 +82,43 @@ int encode_tmap(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* 
   return NSK_OK;
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeIm2colFn g_encode_i2c = nullptr;
+
+int encode_tmap_im2col(CUtensorMap* map, const void* gaddr, int N, int H, int W, int C, const int* lower_wh,
+                       const int* upper_wh, int pixels, int stride) {
+  if (!g_encode_i2c) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || fn == nullptr) return set_error(NSK_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+    g_encode_i2c = (EncodeIm2colFn)fn;
+  }
+  cuuint64_t d[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t s[3] = {(cuuint64_t)C * 2, (cuuint64_t)W * C * 2, (cuuint64_t)H * W * C * 2};
+  cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+  CUresult r = g_encode_i2c(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(gaddr), d, s, lower_wh,
+                            upper_wh, 64, (cuuint32_t)pixels, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    char buf[256];
+    snprintf(buf, sizeof buf,
+             "cuTensorMapEncodeIm2col failed (%d): NHWC %d,%d,%d,%d corners (%d,%d)..(%d,%d) pixels %d stride %d",
+             (int)r, N, H, W, C, lower_wh[0], lower_wh[1], upper_wh[0], upper_wh[1], pixels, stride);
+    return set_error(NSK_ERR_SHAPE, buf);
+  }
+  // Drivers up to 13.1 mis-handle a descriptor flag for im2col maps over tensors below 128 KiB (the same
+  // adjustment CUTLASS applies in copy_traits_sm90_im2col.hpp); clear it for small tensors.
+  int drv = 0;
+  cudaDriverGetVersion(&drv);
+  if (drv <= 13010 && (uint64_t)N * H * W * C * 2 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+  return NSK_OK;
+}
+
 // ---- caching allocator ---------------------------------------------------------
 struct Block {
   size_t size;          // class size (bytes actually reserved)

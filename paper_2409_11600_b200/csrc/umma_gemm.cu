@@ -57,6 +57,9 @@ struct UmmaProb {
   signed char gdh[4][kMaxTaps][3], gw[4][kMaxTaps][3];
   int ext_rows;  // rows of the A box in rr mode (Ht + dh range)
   int probe;     // diagnostics (env NSK_PROBE): bit0 skip MMAs, bit1 skip stores, bit2 skip B loads
+  // im2col-mode A operand (any output width): the tile's first pixel sits at bounding-box position
+  // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
+  int i2c, lw, lh;
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
@@ -211,8 +214,12 @@ __global__ void __launch_bounds__(256, 1)
         } else if (p.mode == MODE_CONV) {
           const int tap = kk / p.cchunks;
           const int c0 = (kk - tap * p.cchunks) * 64;
-          tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[w.z][tap], h_img * p.cs + p.tdh[w.z][tap],
-                      n_img);
+          if (p.i2c)
+            tma_load_4d_im2col(&tmA, &full[s], sa, c0, p.lw + w_img * p.cs, p.lh + h_img * p.cs, n_img,
+                               (uint16_t)(p.tdw[w.z][tap] - p.lw), (uint16_t)(p.tdh[w.z][tap] - p.lh));
+          else
+            tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[w.z][tap], h_img * p.cs + p.tdh[w.z][tap],
+                        n_img);
         } else {  // WGRAD: A = x, MN-major atoms of 64 channels at tap offsets; K = 64 dy pixels
           const int pix0 = kk * 64;
           const int hw = p.Ho * p.Wo;
@@ -226,8 +233,12 @@ __global__ void __launch_bounds__(256, 1)
             if (ga < p.atoms_total) {
               const int tap = ga / p.cin_atoms;
               const int c0 = (ga - tap * p.cin_atoms) * 64;
-              tma_load_4d(&tmA, &full[s], sa + a * 8192, c0, ww * p.cs + p.tdw[0][tap], hh * p.cs + p.tdh[0][tap],
-                          nn);
+              if (p.i2c)
+                tma_load_4d_im2col(&tmA, &full[s], sa + a * 8192, c0, p.lw + ww * p.cs, p.lh + hh * p.cs, nn,
+                                   (uint16_t)(p.tdw[0][tap] - p.lw), (uint16_t)(p.tdh[0][tap] - p.lh));
+              else
+                tma_load_4d(&tmA, &full[s], sa + a * 8192, c0, ww * p.cs + p.tdw[0][tap], hh * p.cs + p.tdh[0][tap],
+                            nn);
             }
           }
         }
@@ -634,6 +645,33 @@ bool try_rowreuse(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin,
   return true;
 }
 
+// im2col-mode A map for a gather over `act` [N, Hin, Win, Cin]: an output grid Gh x Gw walked with
+// coordinate stride p.cs, taps of every class in p.tdh/p.tdw. The bounding box starts at the smallest tap
+// offset (TMA im2col offsets are unsigned) and is sized so it holds exactly Gh x Gw positions per image.
+int i2c_map(UmmaProb& p, CUtensorMap* m, const void* act, int N, int Hin, int Win, int Cin, int Gh, int Gw, int ncls,
+            int pixels) {
+  int mh = 127, mw = 127;
+  for (int c = 0; c < ncls; ++c)
+    for (int t = 0; t < p.ntaps[c]; ++t) {
+      mh = p.tdh[c][t] < mh ? p.tdh[c][t] : mh;
+      mw = p.tdw[c][t] < mw ? p.tdw[c][t] : mw;
+    }
+  if (mh == 127) mh = mw = 0;
+  const int lower[2] = {mw, mh};
+  const int upper[2] = {mw + (Gw - 1) * p.cs - (Win - 1), mh + (Gh - 1) * p.cs - (Hin - 1)};
+  int rc = nsk::encode_tmap_im2col(m, act, N, Hin, Win, Cin, lower, upper, pixels, p.cs);
+  if (rc) return rc;
+  p.i2c = 1;
+  p.lw = mw;
+  p.lh = mh;
+  return NSK_OK;
+}
+
+bool force_i2c() {
+  const char* env = getenv("NSK_CONV_I2C");
+  return env && env[0] == '1';
+}
+
 int check_desc(const NskConvDesc* d) {
   if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride < 1)
     return nsk::set_error(NSK_ERR_SHAPE, "conv2d: invalid descriptor");
@@ -726,12 +764,11 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
   int rc = check_desc(d);
   if (rc) return rc;
   const int P = d->P, Q = d->Q;
-  int Wt, Ht, Nt;
-  if (!pixel_tile(Q, P, 128, &Wt, &Ht, &Nt))
-    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d fprop: output width must tile 128 pixels");
+  int Wt = 0, Ht = 0, Nt = 0;
+  const bool i2c = !pixel_tile(Q, P, 128, &Wt, &Ht, &Nt) || force_i2c();
   const int BN = pick_bn_units(d->K, (d->N * P * Q + 127) / 128, 1);
   CUtensorMap ma, mb;
-  if ((rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
+  if (!i2c && (rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
   {
     const int RS = d->R * d->S;
     uint64_t dims[2] = {(uint64_t)RS * d->C, (uint64_t)d->K};
@@ -762,7 +799,11 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
   p.out = y;
   p.ldc = d->K;
   p.out_f32 = y_f32;
-  try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN);
+  if (i2c) {
+    if ((rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 128))) return rc;
+  } else {
+    try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN);
+  }
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream);
 }
@@ -778,12 +819,11 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   if (d->H % st || d->W % st) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: H, W must divide stride");
   // output grid of each class
   const int Hg = d->H / st, Wg = d->W / st;
-  int Wt, Ht, Nt;
-  if (!pixel_tile(Wg, Hg, 128, &Wt, &Ht, &Nt))
-    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad: input width must tile 128 pixels");
+  int Wt = 0, Ht = 0, Nt = 0;
+  const bool i2c = !pixel_tile(Wg, Hg, 128, &Wt, &Ht, &Nt) || force_i2c();
   const int BN = pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, st * st);
   CUtensorMap ma, mb;
-  if ((rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
+  if (!i2c && (rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
   {
     const int RS = d->R * d->S;
     uint64_t dims[3] = {(uint64_t)d->C, (uint64_t)RS, (uint64_t)d->K};
@@ -825,7 +865,11 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   p.out = dx;
   p.ldc = d->C;
   p.out_f32 = 0;
-  if (ncls == 1) try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN);
+  if (i2c) {
+    if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls, 128))) return rc;
+  } else if (ncls == 1) {
+    try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN);
+  }
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream);
 }
 
@@ -851,15 +895,15 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   int rc = check_desc(d);
   if (rc) return rc;
   const int P = d->P, Q = d->Q;
-  int Wt, Ht, Nt;
-  if (!pixel_tile(Q, P, 64, &Wt, &Ht, &Nt))
-    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: output width must tile 64 pixels");
+  int Wt = 0, Ht = 0, Nt = 0;
   const long long pix = (long long)d->N * P * Q;
-  if (pix % 64) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: N*P*Q must be a multiple of 64");
+  // the tiled path needs whole-row 64-pixel tiles; im2col mode walks any grid (the K tail past the last
+  // pixel reads zeros on both operands)
+  const bool i2c = !pixel_tile(Q, P, 64, &Wt, &Ht, &Nt) || (pix % 64) || force_i2c();
   const int RS = d->R * d->S;
   const int M = RS * d->C;
   const int Mpad = ((M + 127) / 128) * 128;
-  const int k_steps = (int)(pix / 64);
+  const int k_steps = (int)((pix + 63) / 64);
   const int BN = pick_bn(d->K);
   const int mt = Mpad / 128, nt = (d->K + BN - 1) / BN;
   int splits = (int)(ws_bytes / ((uint64_t)Mpad * d->K * sizeof(float)));
@@ -869,7 +913,7 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   const int per = (k_steps + splits - 1) / splits;
   splits = (k_steps + per - 1) / per;
   CUtensorMap ma, mb;
-  if ((rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
+  if (!i2c && (rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
   {
     uint64_t dims[2] = {(uint64_t)d->K, (uint64_t)pix};
     uint64_t str[1] = {(uint64_t)d->K * 2};
@@ -895,6 +939,8 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
       p.tdh[0][t] = (signed char)(r - d->pad);
       p.tdw[0][t] = (signed char)(s - d->pad);
     }
+  p.ntaps[0] = RS;
+  if (i2c && (rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 64))) return rc;
   p.atoms_total = M / 64;
   p.cin_atoms = d->C / 64;
   p.out = ws;

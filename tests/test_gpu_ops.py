@@ -129,8 +129,33 @@ CONV_CASES = [
 ]
 
 
-@pytest.mark.parametrize("case", CONV_CASES)
+# ImageNet-shape grids (56/28/14/7 wide): output rows do not tile 128 pixels, so these run through the
+# im2col-mode TMA path; odd batches leave a partial last M tile and a K tail in wgrad.
+CONV_CASES_I2C = [
+    (2, 56, 56, 64, 64, 3, 1, 1),
+    (2, 56, 56, 64, 256, 1, 1, 0),
+    (2, 56, 56, 128, 128, 3, 2, 1),
+    (2, 56, 56, 256, 512, 1, 2, 0),
+    (3, 28, 28, 128, 128, 3, 1, 1),
+    (4, 14, 14, 256, 256, 3, 1, 1),
+    (2, 14, 14, 256, 256, 3, 2, 1),
+    (5, 7, 7, 512, 512, 3, 1, 1),
+]
+
+
+@pytest.mark.parametrize("case", CONV_CASES + CONV_CASES_I2C)
 def test_conv2d_fprop_dgrad_wgrad(session, case):
+    _conv_case(session, case)
+
+
+@pytest.mark.parametrize("case", CONV_CASES[:7])
+def test_conv2d_forced_im2col_mode(session, case, monkeypatch):
+    """The im2col-mode TMA path on the CIFAR grids too (NSK_CONV_I2C=1), against the same oracle."""
+    monkeypatch.setenv("NSK_CONV_I2C", "1")
+    _conv_case(session, case)
+
+
+def _conv_case(session, case):
     from paper_2409_11600_b200 import autodiff, layers
     from paper_2409_11600_b200._lib import BF16
 
