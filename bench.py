@@ -1,6 +1,6 @@
 """Benchmark: CIFAR-10-shape ResNet-18 training step on B200 (BASELINE.json metric / config C2, C5).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--model resnet18|resnet50]
     (N > 1: python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N)
 
 One step = forward + cross-entropy + backward + SGD(lr 0.1, momentum 0.9) + zero_grad on a
@@ -30,7 +30,20 @@ sys.path.insert(0, ROOT)
 
 METRIC = "train images/sec, CIFAR-10-shape ResNet at 1/2/4/8 B200; conv/GEMM % of peak"
 BATCH = 256
-FLOPS_PER_IMG = None  # filled from the model definition
+
+# --model: resnet18 is the headline (BASELINE.json configs[1] / C2, C5); resnet50 is config C4
+# (ImageNet-shape 3x224x224, batch 256/GPU, bf16), reported on its own line when asked for.
+MODELS = {
+    "resnet18": {"image": (3, 32, 32), "classes": 10, "oracle_sample": 16,
+                 "workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C2/C5",
+                 "model": "resnet18-cifar (11,173,962 params)",
+                 # dominant tensor-core kernel timed alone: stage-1 3x3 conv fprop 64->64 at 32x32
+                 "conv": (32, 64, 64, 3, 1, 1)},
+    "resnet50": {"image": (3, 224, 224), "classes": 1000, "oracle_sample": 1,
+                 "workload": "ImageNet-shape ResNet-50 v1.5 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C4",
+                 "model": "resnet50-v1.5 (25,557,032 params)",
+                 "conv": (56, 64, 64, 3, 1, 1)},
+}
 
 
 def peaks():
@@ -92,10 +105,11 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def synthetic_batch(seed: int, b: int = BATCH):
+def synthetic_batch(seed: int, b: int = BATCH, model: str = "resnet18"):
+    spec = MODELS[model]
     rng = np.random.default_rng(seed)
-    x = rng.standard_normal((b, 3, 32, 32)).astype(np.float32)
-    y = rng.integers(0, 10, b).astype(np.float32)
+    x = rng.standard_normal((b,) + spec["image"]).astype(np.float32)
+    y = rng.integers(0, spec["classes"], b).astype(np.float32)
     return x, y
 
 
@@ -106,12 +120,12 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def run_oracle(sample_imgs: int, steps: int, warmup: int = 1):
+def run_oracle(sample_imgs: int, steps: int, warmup: int = 1, model: str = "resnet18"):
     """The reference CPU path (oracle port, float64) on a bounded sample: returns (img/s, per-step seconds)."""
     from oracle import models as om
 
-    ref = om.ResNet18Oracle(seed=0)
-    x, y = synthetic_batch(1234, sample_imgs)
+    ref = om.ResNet18Oracle(seed=0) if model == "resnet18" else om.ResNet50Oracle(seed=0)
+    x, y = synthetic_batch(1234, sample_imgs, model)
     for _ in range(warmup):
         ref.train_step(x, y, lr=0.1, momentum=0.9)
     times = []
@@ -128,14 +142,15 @@ def reference_arm(args, rank):
         return
     cores = cpu_cores()
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    sample = 16
-    ips, times = run_oracle(sample, max(1, min(args.steps, 3)), warmup=1)
+    spec = MODELS[args.model]
+    sample = spec["oracle_sample"]
+    ips, times = run_oracle(sample, max(1, min(args.steps, 3)), warmup=1, model=args.model)
     line = {
         "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": args.gpus, "steps": len(times),
         "warmup": 1, "ms_per_step": 1000.0 * statistics.median(times) * BATCH / sample,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD), reference CPU path "
+        "config": {"workload": spec["workload"] + ", reference CPU path "
                                "(oracle port: reference arithmetic + restated conv/BN, float64)",
                    "global_batch": BATCH, "sample_images_per_step": sample, "parallelism": "cpu"},
         "cpu_baseline": {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
@@ -145,17 +160,19 @@ def reference_arm(args, rank):
     print(json.dumps(line), flush=True)
 
 
-def time_conv_kernel(lib, _lib, iters=20):
-    """Dominant tensor-core kernel timed alone: stage-1 3x3 conv fprop 64->64, B=256 at 32x32."""
+def time_conv_kernel(lib, _lib, conv, iters=20):
+    """Dominant tensor-core kernel timed alone (conv fprop of the model's heaviest layer shape, B=256)."""
     from paper_2409_11600_b200._lib import BF16, ConvDesc
     from paper_2409_11600_b200.tensor import Buffer
 
-    d = ConvDesc(BATCH, 32, 32, 64, 64, 3, 3, 1, 1, 32, 32)
-    x = Buffer(BATCH * 32 * 32 * 64, BF16)
+    hw, c, k, r, st_, pad = conv
+    p = (hw + 2 * pad - r) // st_ + 1
+    d = ConvDesc(BATCH, hw, hw, c, k, r, r, st_, pad, p, p)
+    x = Buffer(BATCH * hw * hw * c, BF16)
     x.fill(0.5)
-    w = Buffer(64 * 9 * 64, BF16)
+    w = Buffer(k * r * r * c, BF16)
     w.fill(0.01)
-    y = Buffer(BATCH * 32 * 32 * 64, BF16)
+    y = Buffer(BATCH * p * p * k, BF16)
     st = _lib.stream()
     for _ in range(3):
         _lib.check(lib.nsk_conv2d_fprop(C.byref(d), x.ptr, w.ptr, y.ptr, 0, st))
@@ -170,7 +187,7 @@ def time_conv_kernel(lib, _lib, iters=20):
     ms = C.c_float()
     lib.nsk_event_elapsed_ms(e0, e1, C.byref(ms))
     per_ms = ms.value / iters
-    flops = 2.0 * BATCH * 32 * 32 * 64 * 64 * 9
+    flops = 2.0 * BATCH * p * p * k * c * r * r
     return flops, per_ms
 
 
@@ -186,7 +203,7 @@ def profiled_traffic():
 
 def ours_arm(args, rank, world, local_rank):
     from paper_2409_11600_b200 import _lib
-    from paper_2409_11600_b200.models import ResNet18, resnet18_train_flops_per_image
+    from paper_2409_11600_b200 import models
     from paper_2409_11600_b200.runtime import Session
     from paper_2409_11600_b200.tensor import Buffer
     from paper_2409_11600_b200.train import Trainer
@@ -195,15 +212,18 @@ def ours_arm(args, rank, world, local_rank):
     lib = _lib.lib()
     st = _lib.stream()
     dp = None
+    spec = MODELS[args.model]
     s = Session(seed=0)
-    model = ResNet18(s)
+    model = models.ResNet18(s) if args.model == "resnet18" else models.ResNet50(s)
+    flops_per_img = (models.resnet18_train_flops_per_image() if args.model == "resnet18"
+                     else models.resnet50_train_flops_per_image())
     if world > 1:
         from paper_2409_11600_b200.dp import DataParallel
 
         dp = DataParallel(s, rank, world)
         dp.broadcast_params()
-    x, y = synthetic_batch(1000 + rank)
-    tr = Trainer(s, model, x.shape, 10, optimizer=("sgd", 0.1, 0.9), graph=True, warmup=2, dp=dp)
+    x, y = synthetic_batch(1000 + rank, BATCH, args.model)
+    tr = Trainer(s, model, x.shape, spec["classes"], optimizer=("sgd", 0.1, 0.9), graph=True, warmup=2, dp=dp)
 
     def barrier():
         _lib.sync()
@@ -267,16 +287,16 @@ def ours_arm(args, rank, world, local_rank):
     if rank != 0:
         return
     pk_burst, pk_sus, hbm, src = peaks()
-    flops, kms = time_conv_kernel(lib, _lib)
+    flops, kms = time_conv_kernel(lib, _lib, spec["conv"])
     achieved = flops / (kms / 1000.0) / 1e12
-    step_tflops = value * resnet18_train_flops_per_image() / 1e12 / world
+    step_tflops = value * flops_per_img / 1e12 / world
     line = {
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) images, uniform labels, random init)",
-        "config": {"workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C2/C5",
-                   "model": "resnet18-cifar (11,173,962 params)", "global_batch": BATCH * world,
-                   "per_gpu_batch": BATCH, "seq_len": None, "image": [3, 32, 32], "parallelism": f"dp{world}",
+        "config": {"workload": spec["workload"],
+                   "model": spec["model"], "global_batch": BATCH * world,
+                   "per_gpu_batch": BATCH, "seq_len": None, "image": list(spec["image"]), "parallelism": f"dp{world}",
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "final_loss": loss},
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(x.nbytes + y.nbytes),
@@ -284,16 +304,17 @@ def ours_arm(args, rank, world, local_rank):
         "gpu_launches": int(tr.launches_per_step * args.steps),
         "step_tflops_per_gpu": step_tflops,
         "step_frac_of_peak": step_tflops / pk_sus,
-        "roofline": {"bound": "tensor", "kernel": "umma_kernel<64,2,2,rr> conv2d fprop 3x3 64->64, 256x32x32",
+        "roofline": {"bound": "tensor",
+                     "kernel": "umma_kernel conv2d fprop {3}x{3} {1}->{2} s{4}, 256x{0}x{0}".format(*spec["conv"]),
                      "achieved": achieved, "peak": pk_burst, "unit": "TFLOP/s", "frac": achieved / pk_burst,
-                     "traffic": profiled_traffic(), "peak_source": f"{src} bf16_tflops (burst, kernel timed alone)",
+                     "traffic": profiled_traffic() if args.model == "resnet18" else None, "peak_source": f"{src} bf16_tflops (burst, kernel timed alone)",
                      "algorithmic_flops_per_launch": flops, "launch_ms": kms},
         "clocks": clk.summary(),
     }
     if world == 1:
         cores = cpu_cores()
-        sample = 16
-        ips, times = run_oracle(sample, 2, warmup=1)
+        sample = spec["oracle_sample"]
+        ips, times = run_oracle(sample, 2, warmup=1, model=args.model)
         line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
                                 "sample": f"{sample} images/step x {len(times)} timed steps (1 warm-up) of the "
                                           "B=256 workload, float64 oracle port"}
@@ -306,6 +327,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="resnet18", choices=sorted(MODELS))
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

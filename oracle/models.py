@@ -1,4 +1,5 @@
-"""CPU oracle training steps for the small CNN (C1) and CIFAR ResNet-18 (C2). TEST INFRASTRUCTURE ONLY.
+"""CPU oracle training steps for the small CNN (C1), CIFAR ResNet-18 (C2), ImageNet ResNet-50 (C4) and the
+GRU classifier (C3). TEST INFRASTRUCTURE ONLY.
 
 Parameters are declared in the same order, with the same names and seed
 draws, as paper_2409_11600_b200.models (one ``default_rng(seed).integers(0,
@@ -195,6 +196,116 @@ class ResNet18Oracle:
         dc0 = q(dc0)
         grads["stem_bn"] = np.stack([dg, db])
         grads["stem_w"] = X.conv2d_wgrad(x, dc0, W["stem_w"].shape, 1, 1)
+        return loss, grads, logits
+
+    def train_step(self, x_nchw, y, lr=0.1, momentum=0.9, bf16=False):
+        loss, grads, _ = self.loss_and_grads(x_nchw, y, bf16=bf16)
+        self.opt.sgd(self.params, grads, lr, momentum)
+        return loss
+
+
+class ResNet50Oracle:
+    """ImageNet ResNet-50 v1.5 training step (same declaration as paper_2409_11600_b200.models.ResNet50)."""
+
+    STAGES = ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2))
+
+    def __init__(self, seed=0, classes=1000):
+        d = _Decl(seed)
+        d.conv("stem_w", 64, 7, 7, 3)
+        d.bn("stem_bn", 64)
+        self.blocks = []
+        cin = 64
+        i = 0
+        for width, nblocks, stride in self.STAGES:
+            cout = 4 * width
+            for b in range(nblocks):
+                st = stride if b == 0 else 1
+                pre = f"b{i}_"
+                d.conv(pre + "w1", width, 1, 1, cin)
+                d.bn(pre + "bn1", width)
+                d.conv(pre + "w2", width, 3, 3, width)
+                d.bn(pre + "bn2", width)
+                d.conv(pre + "w3", cout, 1, 1, width)
+                d.bn(pre + "bn3", cout)
+                if b == 0:
+                    d.conv(pre + "wsc", cout, 1, 1, cin)
+                    d.bn(pre + "bnsc", cout)
+                self.blocks.append((pre, st, b == 0))
+                cin = cout
+                i += 1
+        d.linear("fc_w", classes, 2048)
+        d.zeros("fc_b", classes)
+        self.params = d.params
+        self.order = d.order
+        self.opt = _Opt(self.params)
+
+    def _ops(self, bf16):
+        q = X.round_bf16 if bf16 else (lambda a: np.asarray(a, np.float64))
+        p = self.params
+        W = {k: q(v) for k, v in p.items() if v.ndim == 4}
+
+        def conv_bn(h, wk, bnk, st, pad, relu, res=None):
+            c = q(X.conv2d_fwd(h, W[wk], st, pad))
+            y_, cache = X.batchnorm_fwd(c, p[bnk][0], p[bnk][1], relu=relu, residual=res)
+            return q(y_), cache
+
+        def bn_conv_bwd(dy, cache, y_out, relu, bnk, wk, hin, st, pad, grads, need_dx=True):
+            dc, dg, db, dres = X.batchnorm_bwd(dy, cache, y_out=y_out, relu=relu)
+            dc = q(dc)
+            grads[bnk] = np.stack([dg, db])
+            grads[wk] = X.conv2d_wgrad(hin, dc, W[wk].shape, st, pad)
+            dx = q(X.conv2d_dgrad(dc, W[wk], hin.shape, st, pad)) if need_dx else None
+            return dx, q(dres)
+
+        return q, conv_bn, bn_conv_bwd
+
+    def block_fwd(self, i, hin, bf16=False):
+        """Bottleneck block i on input hin (NHWC): returns (output, cache for block_bwd)."""
+        q, conv_bn, _ = self._ops(bf16)
+        pre, st, proj = self.blocks[i]
+        o1, k1 = conv_bn(hin, pre + "w1", pre + "bn1", 1, 0, True)
+        o2, k2 = conv_bn(o1, pre + "w2", pre + "bn2", st, 1, True)
+        if proj:
+            sc, ks = conv_bn(hin, pre + "wsc", pre + "bnsc", st, 0, False)
+        else:
+            sc, ks = hin, None
+        h, k3 = conv_bn(o2, pre + "w3", pre + "bn3", 1, 0, True, res=sc)
+        return h, (i, hin, o1, k1, o2, k2, ks, h, k3)
+
+    def block_bwd(self, dh, cache, grads, bf16=False):
+        """Gradient of block `cache[0]` w.r.t. its input (parameter gradients into `grads`)."""
+        q, _, bn_conv_bwd = self._ops(bf16)
+        i, hin, o1, k1, o2, k2, ks, hout, k3 = cache
+        pre, st, proj = self.blocks[i]
+        do2, dres = bn_conv_bwd(dh, k3, hout, True, pre + "bn3", pre + "w3", o2, 1, 0, grads)
+        do1, _ = bn_conv_bwd(do2, k2, o2, True, pre + "bn2", pre + "w2", o1, st, 1, grads)
+        dhin, _ = bn_conv_bwd(do1, k1, o1, True, pre + "bn1", pre + "w1", hin, 1, 0, grads)
+        if proj:
+            dsc, _ = bn_conv_bwd(dres, ks, None, False, pre + "bnsc", pre + "wsc", hin, st, 0, grads)
+            return q(dhin + dsc)
+        return q(dhin + dres)
+
+    def loss_and_grads(self, x_nchw, y, bf16=False):
+        q, conv_bn, bn_conv_bwd = self._ops(bf16)
+        p = self.params
+        x = q(np.transpose(x_nchw, (0, 2, 3, 1)))
+        h0, cache0 = conv_bn(x, "stem_w", "stem_bn", 2, 3, True)
+        h = q(X.maxpool_fwd(h0, 3, 2, 1))
+        caches = []
+        for i in range(len(self.blocks)):
+            h, c = self.block_fwd(i, h, bf16)
+            caches.append(c)
+        feat = X.avgpool_fwd(h).astype(np.float32)
+        fcw = p["fc_w"]
+        logits = R.matmul_t(feat, fcw) + p["fc_b"]
+        loss, probs = R.cross_entropy(logits, y)
+        g = R.cross_entropy_grad(probs, y)
+        grads = {"fc_b": g.astype(np.float64).sum(axis=0), "fc_w": R.plain_matmul(g.T, feat).astype(np.float64)}
+        dh = q(X.avgpool_bwd(R.plain_matmul(g, fcw), h.shape))
+        for c in reversed(caches):
+            dh = self.block_bwd(dh, c, grads, bf16)
+        dh0 = q(X.maxpool_bwd(h0, dh, 3, 2, 1))
+        bn_conv_bwd(dh0, cache0, h0, True, "stem_bn", "stem_w", x, 2, 3, grads, need_dx=False)
         return loss, grads, logits
 
     def train_step(self, x_nchw, y, lr=0.1, momentum=0.9, bf16=False):

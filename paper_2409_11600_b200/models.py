@@ -1,4 +1,5 @@
-"""Model declarations on the drop-in surface: small CNN (C1) and CIFAR ResNet-18 (C2).
+"""Model declarations on the drop-in surface: small CNN (C1), CIFAR ResNet-18 (C2), GRU classifier (C3),
+ImageNet ResNet-50 (C4).
 
 Parameters are created through the session exactly like the reference's
 ``xavier_uniform`` / ``param_zeros`` builtins (builtins.py:85-104): names
@@ -137,6 +138,83 @@ def resnet18_train_flops_per_image() -> float:
                 macs += ho * ho * cout * cin
             h, cin = ho, cout
     macs += 512 * 10
+    return 2.0 * (3 * macs - stem)
+
+
+class ResNet50:
+    """ImageNet ResNet-50 (v1.5, stride on the 3x3): 7x7/2 stem, 3x3/2 max-pool, bottleneck stages [3,4,6,3]
+    (1x1 reduce, 3x3, 1x1 expand x4, BN after every conv, projection shortcut on each stage's first block),
+    global average pool, fc -> 25,557,032 parameters (config C4). Activations NHWC bf16."""
+
+    STAGES = ((64, 3, 1), (128, 4, 2), (256, 6, 2), (512, 3, 2))
+
+    def __init__(self, session: Session, classes: int = 1000):
+        P = Params(session)
+        self.s = session
+        self.stem_w, self.stem_bn = P.conv(64, 7, 7, 3), P.bn(64)
+        self.blocks = []
+        cin = 64
+        for width, nblocks, stride in self.STAGES:
+            cout = 4 * width
+            for b in range(nblocks):
+                st = stride if b == 0 else 1
+                blk = {"stride": st, "w1": P.conv(width, 1, 1, cin), "bn1": P.bn(width),
+                       "w2": P.conv(width, 3, 3, width), "bn2": P.bn(width),
+                       "w3": P.conv(cout, 1, 1, width), "bn3": P.bn(cout)}
+                if b == 0:
+                    blk["wsc"], blk["bnsc"] = P.conv(cout, 1, 1, cin), P.bn(cout)
+                self.blocks.append(blk)
+                cin = cout
+        self.fc_w, self.fc_b = P.linear(classes, 2048), P.zeros(classes)
+
+    def num_params(self) -> int:
+        return sum(t.numel for _n, t in self.s.param_group.params)
+
+    def block(self, i: int, h: Tensor) -> Tensor:
+        """Bottleneck block i: 1x1 reduce -> BN/ReLU -> 3x3 (stride) -> BN/ReLU -> 1x1 expand -> BN (+ shortcut) -> ReLU."""
+        pool = self.s.pool
+        blk = self.blocks[i]
+        st = blk["stride"]
+        o = layers.batchnorm(layers.conv2d(h, blk["w1"], 1, 0, pool), blk["bn1"], pool, relu=True)
+        o = layers.batchnorm(layers.conv2d(o, blk["w2"], st, 1, pool), blk["bn2"], pool, relu=True)
+        if "wsc" in blk:
+            sc = layers.batchnorm(layers.conv2d(h, blk["wsc"], st, 0, pool), blk["bnsc"], pool, relu=False)
+        else:
+            sc = h
+        return layers.batchnorm(layers.conv2d(o, blk["w3"], 1, 0, pool), blk["bn3"], pool, relu=True, residual=sc)
+
+    def forward(self, x_nchw: Tensor) -> Tensor:
+        pool, push = self.s.pool, self.s.push_named
+        stem = layers.conv2d(x_nchw, self.stem_w, 2, 3, pool, layout="nchw")
+        h = layers.maxpool(layers.batchnorm(stem, self.stem_bn, pool, relu=True), 3, 2, 1, pool)
+        push("rn.stem", h)
+        for i in range(len(self.blocks)):
+            h = self.block(i, h)
+            push(f"rn.block{i}", h)
+        feat = layers.avgpool_global(h, pool)
+        logits = nn.linear(feat, self.fc_w, self.fc_b, pool)
+        push("rn.logits", logits)
+        return logits
+
+
+def resnet50_train_flops_per_image(hw: int = 224, classes: int = 1000) -> float:
+    """Algorithmic training FLOPs per image (24.30 GFLOP at 224): forward, wgrad and dgrad
+    MACs x 2, without the stem's dgrad."""
+    h = (hw + 6 - 7) // 2 + 1
+    stem = h * h * 64 * 3 * 49
+    h = (h + 2 - 3) // 2 + 1
+    macs = stem
+    cin = 64
+    for width, nblocks, stride in ResNet50.STAGES:
+        cout = 4 * width
+        for b in range(nblocks):
+            st = stride if b == 0 else 1
+            ho = (h - 1) // st + 1
+            macs += h * h * width * cin + ho * ho * width * width * 9 + ho * ho * cout * width
+            if b == 0:
+                macs += ho * ho * cout * cin
+            h, cin = ho, cout
+    macs += 2048 * classes
     return 2.0 * (3 * macs - stem)
 
 

@@ -82,3 +82,42 @@ def test_conv_and_bn_restatements_match_torch():
     np.testing.assert_allclose(dg, gt.grad.numpy(), rtol=1e-8, atol=1e-10)
     np.testing.assert_allclose(db, bt.grad.numpy(), rtol=1e-8, atol=1e-10)
     np.testing.assert_allclose(dres, rt.grad.numpy(), rtol=1e-8, atol=1e-10)
+
+
+def torch_resnet50_loss(params, order, blocks, x_nchw, y):
+    P = {k: _t(v) for k, v in params.items()}
+
+    def conv(h, k, st, pad):
+        return F.conv2d(h, P[k].permute(0, 3, 1, 2), stride=st, padding=pad)
+
+    def bn(h, k, relu, res=None):
+        out = F.batch_norm(h, None, None, P[k][0], P[k][1], training=True, eps=1e-5)
+        if res is not None:
+            out = out + res
+        return F.relu(out) if relu else out
+
+    x = torch.tensor(x_nchw, dtype=torch.float64)
+    h = F.max_pool2d(bn(conv(x, "stem_w", 2, 3), "stem_bn", True), 3, 2, 1)
+    for pre, st, proj in blocks:
+        o = bn(conv(h, pre + "w1", 1, 0), pre + "bn1", True)
+        o = bn(conv(o, pre + "w2", st, 1), pre + "bn2", True)
+        sc = bn(conv(h, pre + "wsc", st, 0), pre + "bnsc", False) if proj else h
+        h = bn(conv(o, pre + "w3", 1, 0), pre + "bn3", True, res=sc)
+    logits = h.mean(dim=(2, 3)) @ P["fc_w"].T + P["fc_b"]
+    loss = F.cross_entropy(logits, torch.tensor(y, dtype=torch.int64))
+    loss.backward()
+    return float(loss), {k: P[k].grad.numpy() for k in order}
+
+
+def test_resnet50_oracle_matches_torch_f64():
+    """C4 oracle (v1.5 bottlenecks, 7x7/2 stem, 3x3/2 max-pool) vs torch autograd at a reduced 64x64 input."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 3, 64, 64)).astype(np.float32)
+    y = rng.integers(0, 1000, 2).astype(np.float32)
+    ref = om.ResNet50Oracle(seed=0)
+    assert sum(v.size for v in ref.params.values()) == 25_557_032
+    loss, grads, _ = ref.loss_and_grads(x, y, bf16=False)
+    tl, tg = torch_resnet50_loss(ref.params, ref.order, ref.blocks, x, y)
+    assert loss == pytest.approx(tl, rel=1e-6)
+    worst = sorted(((rel(grads[k], tg[k]), k) for k in ref.order), reverse=True)
+    assert worst[0][0] < 1e-4, worst[:5]
