@@ -63,7 +63,8 @@ struct UmmaProb {
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
-constexpr int kStgPitch = 80;          // epilogue staging row pitch (64 B of bf16 + 16 B pad)
+constexpr int kStgPitch = 80;
+constexpr int kProducers = 3;          // TMA issuing threads (warps 0, 2, 3)          // epilogue staging row pitch (64 B of bf16 + 16 B pad)
 
 template <int ESZ>
 struct KT {
@@ -162,8 +163,14 @@ __global__ void __launch_bounds__(256, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
+  // Up to three TMA issuing threads (warps 0, 2, 3) take k-steps round-robin: one thread only sustains about
+  // one TMA box per L2 round trip (tools/tma_rate.cu), so independent issuers multiply the per-SM feed
+  // rate. At most STAGES issuers: a producer is then never more than one empty-barrier phase ahead of the
+  // MMA consumer, which keeps the parity waits unambiguous.
+  constexpr int kProducers = STAGES < 3 ? STAGES : 3;
+  const int prod = warp == 0 ? 0 : warp - 1;
+  if (lane == 0 && (warp == 0 || warp == 2 || warp == 3) && prod < kProducers) {
+    // ---------------- TMA producers ----------------
     int i = 0;  // global k-step counter (smem ring position)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit w = decode_unit(p, u, BN);
@@ -177,6 +184,7 @@ __global__ void __launch_bounds__(256, 1)
       }
       const bool half_a = (p.mode == MODE_WGRAD) && (w.m0 / 64 + 1 >= p.atoms_total);
       for (int kk = w.kb; kk < w.kb + w.nk; ++kk, ++i) {
+        if (i % kProducers != prod) continue;
         const int s = i % STAGES;
         if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * S::STAGE_BYTES;
