@@ -88,6 +88,10 @@ typedef struct NskConvDesc {
 } NskConvDesc;
 
 int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int y_f32, void* stream);
+/* fprop (bf16 y) that also writes per-CTA channel partials [nparts][2][K] (sum, sum of squares of the stored
+ * outputs) for the BatchNorm consuming y; partials must hold 2*SMs x 2 x K floats. */
+int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, void* y, float* partials,
+                           uint64_t partial_floats, int* nparts, void* stream);
 int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream);
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d);
 int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float* dw, float beta, void* ws,
@@ -154,6 +158,10 @@ int nsk_scale_multi(int n_tensors, float* const* g, const uint64_t* numel, const
 uint64_t nsk_bn_workspace(uint64_t rows, int C);
 int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
                float eps, int relu, const void* residual, float* ws, void* stream);
+/* nsk_bn_fwd with the statistics taken from conv partials (nsk_conv2d_fprop_stats) instead of a pass over x */
+int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
+                        float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
+                        float* ws, void* stream);
 /* y_relu: the forward output when the op applied ReLU (mask = y > 0), else NULL. dres (optional) receives the
  * masked gradient flowing to the residual input. dgamma_beta [2, C] (= dgamma_beta*beta_acc + new). */
 int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* gamma_beta, const float* mean,

@@ -60,6 +60,7 @@ SIGNATURES = {
     "nsk_stream_is_capturing": (i32, [vp, C.POINTER(i32)]),
     "nsk_gemm": (i32, [i32, i32, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, i32, vp, f32, vp]),
     "nsk_conv2d_fprop": (i32, [C.POINTER(ConvDesc), vp, vp, vp, i32, vp]),
+    "nsk_conv2d_fprop_stats": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp, u64, C.POINTER(C.c_int), vp]),
     "nsk_conv2d_dgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp]),
     "nsk_conv2d_wgrad_workspace": (u64, [C.POINTER(ConvDesc)]),
     "nsk_conv2d_wgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp, u64, vp]),
@@ -87,6 +88,7 @@ SIGNATURES = {
     "nsk_scale_multi": (i32, [i32, vp, vp, vp, vp]),
     "nsk_bn_workspace": (u64, [u64, i32]),
     "nsk_bn_fwd": (i32, [vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp]),
+    "nsk_bn_fwd_partials": (i32, [vp, i32, vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp]),
     "nsk_bn_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, f32, u64, i32, vp, vp]),
     "nsk_avgpool_fwd": (i32, [i32, vp, vp, i32, i32, i32, vp]),
     "nsk_avgpool_bwd": (i32, [vp, i32, vp, i32, i32, i32, vp]),

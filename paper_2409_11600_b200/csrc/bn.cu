@@ -279,6 +279,25 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   return NSK_OK;
 }
 
+// forward from channel partials produced by the conv that wrote x (nsk_conv2d_fprop_stats): fold + apply,
+// no statistics pass over x
+int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
+                        float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
+                        float* ws, void* stream) {
+  int rc = check(rows, C, x, residual);
+  if (rc) return rc;
+  if (nparts < 1) return nsk::set_error(NSK_ERR_SHAPE, "batchnorm: no statistics partials");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* scale = ws + (size_t)MAXBLK * 2 * C;
+  float* shift = scale + C;
+  bn_fwd_finalize<<<C, FT, 0, st>>>(partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
+                                                        shift, (__nv_bfloat16*)y, rows, C, relu);
+  NSK_LAUNCH_CHECK("bn_fwd_partials");
+  return NSK_OK;
+}
+
 int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* gamma_beta, const float* mean,
                const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
                float* ws, void* stream) {

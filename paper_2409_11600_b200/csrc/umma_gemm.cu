@@ -60,6 +60,9 @@ struct UmmaProb {
   // im2col-mode A operand (any output width): the tile's first pixel sits at bounding-box position
   // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
   int i2c, lw, lh;
+  // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
+  // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
+  float* stats;
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
@@ -84,6 +87,9 @@ struct Smem {
   static constexpr int TOTAL = STG_OFF + 4 * 32 * 80 + 1024;  // + epilogue staging (4 warps x 32 rows x 80 B)
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
+
+// named barrier over the four epilogue warps (128 threads)
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
   asm volatile(
@@ -332,6 +338,12 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int r = q * 32 + lane;  // tile row == TMEM lane
     const bool vec_ok = ((p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0);
+    float* st_acc = (float*)(stage_base + 4 * 32 * kStgPitch);  // [2][N] CTA channel sums (stats mode)
+    float* st_red = st_acc + 2 * p.N;                           // [4 warps][2][32]
+    if (p.stats) {
+      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 128) st_acc[i] = 0.f;
+      epi_bar();
+    }
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = decode_unit(p, u, BN);
@@ -416,6 +428,28 @@ __global__ void __launch_bounds__(256, 1)
             *(uint4*)(stg + lane * kStgPitch + t * 2) = u4;
           }
           __syncwarp();
+          if (p.stats) {
+            // column sums of the staged (bf16-rounded) tile: lane = column, rows of this warp
+            const unsigned okm = __ballot_sync(0xffffffffu, row_ok);
+            float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
+            for (int rr = 0; rr < 32; ++rr) {
+              const float v = __bfloat162float(*(const __nv_bfloat16*)(stg + rr * kStgPitch + lane * 2));
+              if ((okm >> rr) & 1u) {
+                s1 += v;
+                s2 += v * v;
+              }
+            }
+            st_red[q * 64 + lane] = s1;
+            st_red[q * 64 + 32 + lane] = s2;
+            epi_bar();
+            if (q == 0) {  // fixed warp order: deterministic
+              st_acc[col0 + lane] += (st_red[lane] + st_red[64 + lane]) + (st_red[128 + lane] + st_red[192 + lane]);
+              st_acc[p.N + col0 + lane] +=
+                  (st_red[32 + lane] + st_red[96 + lane]) + (st_red[160 + lane] + st_red[224 + lane]);
+            }
+            epi_bar();
+          }
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
             const int piece = it * 32 + lane;
@@ -435,6 +469,11 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (p.stats) {
+      epi_bar();
+      float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
+      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 128) out[i] = st_acc[i];
     }
   }
   __syncthreads();
@@ -529,27 +568,30 @@ int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
 }
 
 template <int BN, int ESZ, int STAGES, bool RR = false>
-int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStream_t st) {
+int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStream_t st, int* grid_out) {
   using S = Smem<BN, ESZ, STAGES, RR>;
   auto kern = umma_kernel<BN, ESZ, STAGES, RR>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL);
+  const int smem = S::TOTAL + (p.stats ? (2 * p.N + 4 * 64) * (int)sizeof(float) : 0);
+  if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
+  static int configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(umma)");
-    configured = true;
+    configured = smem;
   }
-  const int per_sm = (2 * S::TOTAL <= 227 * 1024) ? 2 : 1;  // small-N tiles: two co-resident CTAs per SM
+  const int per_sm = (2 * smem <= 227 * 1024) ? 2 : 1;  // small-N tiles: two co-resident CTAs per SM
   int grid = per_sm * nsk::sm_count();
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
-  kern<<<grid, 256, S::TOTAL, st>>>(a, b, p);
+  if (grid_out) *grid_out = grid;
+  kern<<<grid, 256, smem, st>>>(a, b, p);
   NSK_LAUNCH_CHECK("umma_kernel");
   return NSK_OK;
 }
 
 template <int ESZ>
 int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
-                cudaStream_t st) {
+                cudaStream_t st, int* grid_out = nullptr) {
   p.mt = mt;
   p.nt = nt;
   p.units = mt * nt * nz;
@@ -557,20 +599,20 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
     if constexpr (ESZ == 2) {
       switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
         case 64:
-          return launch_umma<64, 2, 2, true>(a, b, p, st);
+          return launch_umma<64, 2, 2, true>(a, b, p, st, grid_out);
         case 128:
-          return launch_umma<128, 2, 2, true>(a, b, p, st);
+          return launch_umma<128, 2, 2, true>(a, b, p, st, grid_out);
       }
     }
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "row-reuse conv needs bf16 and N <= 128");
   }
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 4>(a, b, p, st);
+      return launch_umma<64, ESZ, 4>(a, b, p, st, grid_out);
     case 128:
-      return launch_umma<128, ESZ, 3>(a, b, p, st);
+      return launch_umma<128, ESZ, 3>(a, b, p, st, grid_out);
     case 256:
-      return launch_umma<256, ESZ, 4>(a, b, p, st);
+      return launch_umma<256, ESZ, 4>(a, b, p, st, grid_out);
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
 }
@@ -767,8 +809,12 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
   return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, st);
 }
 
-// y[n,p,q,k] = sum_{c,r,s} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]   (NHWC / KRSC, bf16)
-int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int y_f32, void* stream) {
+}  // extern "C"
+
+namespace {
+
+int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int y_f32, float* stats,
+               uint64_t stats_floats, int* nparts, void* stream) {
   int rc = check_desc(d);
   if (rc) return rc;
   const int P = d->P, Q = d->Q;
@@ -813,7 +859,28 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
     try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN);
   }
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
-  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream);
+  if (stats) {
+    if (y_f32) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d fprop: channel statistics need a bf16 output");
+    if (stats_floats < (uint64_t)2 * nsk::sm_count() * 2 * d->K)
+      return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
+    p.stats = stats;
+  }
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream, nparts);
+}
+
+}  // namespace
+
+extern "C" {
+
+// y[n,p,q,k] = sum_{c,r,s} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]   (NHWC / KRSC, bf16)
+int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int y_f32, void* stream) {
+  return conv_fprop(d, x, w, y, y_f32, nullptr, 0, nullptr, stream);
+}
+
+// fprop that also emits per-CTA channel partials for the BatchNorm consuming y (nsk_bn_fwd_partials)
+int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, void* y, float* partials,
+                           uint64_t partial_floats, int* nparts, void* stream) {
+  return conv_fprop(d, x, w, y, 0, partials, partial_floats, nparts, stream);
 }
 
 // dx[n,h,w,c] = sum_{k,r,s : h = p*st-pad+r} dy[n,p,q,k] * w[k,r,s,c]

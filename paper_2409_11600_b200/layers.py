@@ -56,11 +56,14 @@ def conv_out(h: int, k: int, stride: int, pad: int) -> int:
     return (h + 2 * pad - k) // stride + 1
 
 
-def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str = "nhwc") -> Tensor:
+def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str = "nhwc",
+           bn_stats: bool = False) -> Tensor:
     """y[n,p,q,k] = sum_{r,s,c} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]  (NHWC x KRSC -> NHWC, bf16).
 
     ``layout="nchw"`` accepts a host-layout float32 image batch [N, C, H, W] directly (image stems:
-    the layout change is fused into the im2col gather; no input gradient)."""
+    the layout change is fused into the im2col gather; no input gradient). ``bn_stats`` (for a conv whose
+    output goes straight into ``batchnorm``, see ``conv_bn``) makes the tcgen05 kernel also emit the BN
+    channel statistics, so the BN needs no separate pass over y."""
     if x.rank != 4 or w.rank != 4:
         raise NskTypeError(f"conv2d needs NHWC input and KRSC filters, got {list(x.shape)} and {list(w.shape)}")
     nchw = layout == "nchw"
@@ -83,7 +86,15 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str 
     xp, xtmp = (x.ptr, None) if nchw else _temp_bf16(x, pool)
     wp = w.bf16_ptr() if w.dtype == F32 else w.ptr
     if c % 64 == 0 and not nchw:
-        check(lib.nsk_conv2d_fprop(C.byref(desc), xp, wp, y.ptr, 0, st))
+        if bn_stats:
+            # per-CTA channel partials for the BatchNorm consuming y (released by batchnorm)
+            parts = empty_tensor(pool, (2 * _lib.ctx.sm_count, 2, k))
+            nparts = C.c_int(0)
+            check(lib.nsk_conv2d_fprop_stats(C.byref(desc), xp, wp, y.ptr, parts.ptr, parts.numel, C.byref(nparts),
+                                             st))
+            y.bn_partials = (parts, nparts.value)
+        else:
+            check(lib.nsk_conv2d_fprop(C.byref(desc), xp, wp, y.ptr, 0, st))
         saved = (x, w)
         attrs = {"desc": desc, "stem": False}
         if xtmp is not None:
@@ -166,6 +177,14 @@ def _r_conv2d(node, g, pool, sinks):
 
 # --- batchnorm (+ residual, + relu) ---------------------------------------------------------------
 
+def conv_bn(x: Tensor, w: Tensor, gb: Tensor, stride: int, pad: int, pool: Pool, relu: bool = False,
+            residual: Tensor | None = None, layout: str = "nhwc") -> Tensor:
+    """conv2d followed by batchnorm (two recorded ops, same gradients); the conv kernel emits the BN
+    channel statistics so the normalisation reads its input once."""
+    return batchnorm(conv2d(x, w, stride, pad, pool, layout=layout, bn_stats=True), gb, pool, relu=relu,
+                     residual=residual)
+
+
 def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: Tensor | None = None,
               eps: float = 1e-5) -> Tensor:
     """Training-mode batch norm over N*H*W per channel, gamma_beta = [2, C]; optional residual add and ReLU."""
@@ -183,8 +202,15 @@ def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: T
     mean = _internal_tensor(empty_tensor(pool, (c,)))
     invstd = _internal_tensor(empty_tensor(pool, (c,)))
     ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
-    check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu),
-                         None if residual is None else residual.ptr, ws.ptr, st))
+    parts = x.bn_partials
+    if parts is not None:
+        check(lib.nsk_bn_fwd_partials(parts[0].ptr, parts[1], x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c,
+                                      float(eps), int(relu), None if residual is None else residual.ptr, ws.ptr, st))
+        release_tensor(pool, parts[0])
+        x.bn_partials = None
+    else:
+        check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu),
+                             None if residual is None else residual.ptr, ws.ptr, st))
     saved = (x, gb, mean, invstd) + ((y,) if relu else ())
     record("batchnorm", y, x, gb, residual, saved=saved, attrs={"relu": relu, "rows": rows, "c": c})
     return y

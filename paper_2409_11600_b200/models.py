@@ -108,12 +108,12 @@ class ResNet18:
         push("rn.stem", h)
         for i, blk in enumerate(self.blocks):
             st = blk["stride"]
-            o = layers.batchnorm(layers.conv2d(h, blk["w1"], st, 1, pool), blk["bn1"], pool, relu=True)
+            o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True)
             if "wsc" in blk:
-                sc = layers.batchnorm(layers.conv2d(h, blk["wsc"], st, 0, pool), blk["bnsc"], pool, relu=False)
+                sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False)
             else:
                 sc = h
-            h = layers.batchnorm(layers.conv2d(o, blk["w2"], 1, 1, pool), blk["bn2"], pool, relu=True, residual=sc)
+            h = layers.conv_bn(o, blk["w2"], blk["bn2"], 1, 1, pool, relu=True, residual=sc)
             push(f"rn.block{i}", h)
         feat = layers.avgpool_global(h, pool)
         logits = nn.linear(feat, self.fc_w, self.fc_b, pool)
@@ -175,13 +175,13 @@ class ResNet50:
         pool = self.s.pool
         blk = self.blocks[i]
         st = blk["stride"]
-        o = layers.batchnorm(layers.conv2d(h, blk["w1"], 1, 0, pool), blk["bn1"], pool, relu=True)
-        o = layers.batchnorm(layers.conv2d(o, blk["w2"], st, 1, pool), blk["bn2"], pool, relu=True)
+        o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True)
+        o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True)
         if "wsc" in blk:
-            sc = layers.batchnorm(layers.conv2d(h, blk["wsc"], st, 0, pool), blk["bnsc"], pool, relu=False)
+            sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False)
         else:
             sc = h
-        return layers.batchnorm(layers.conv2d(o, blk["w3"], 1, 0, pool), blk["bn3"], pool, relu=True, residual=sc)
+        return layers.conv_bn(o, blk["w3"], blk["bn3"], 1, 0, pool, relu=True, residual=sc)
 
     def forward(self, x_nchw: Tensor) -> Tensor:
         pool, push = self.s.pool, self.s.push_named

@@ -451,3 +451,35 @@ def test_augment_crop_flip_indices_bit_exact(dev):
     # index exactness: zero-padded border pixels land exactly where the oracle puts them
     np.testing.assert_array_equal(got[..., :3] == X.round_bf16(-mean / std), X.round_bf16(ref)[..., :3] ==
                                   X.round_bf16(-mean / std))
+
+
+@pytest.mark.parametrize("case", [
+    (8, 32, 32, 64, 64, 3, 1, 1),      # N=64 row-reuse tiles, 2 CTAs/SM
+    (16, 8, 8, 256, 512, 3, 2, 1),     # wide tiles, several n-tiles per CTA
+    (2, 28, 28, 128, 128, 3, 1, 1),    # im2col-mode A, partial last M tile
+    (4, 7, 7, 512, 2048, 1, 1, 0),     # ResNet-50 expand: 2048 channels of partials
+])
+def test_conv_bn_fused_statistics(session, case):
+    """conv_bn: BN statistics from the conv epilogue's channel partials vs the oracle BN of the stored conv output."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+
+    n, h, w, c, k, r, st, pad = case
+    rng = np.random.default_rng(sum(case))
+    x = X.round_bf16(rng.standard_normal((n, h, w, c)))
+    wt = (rng.standard_normal((k, r, r, c)) / np.sqrt(c * r * r)).astype(np.float32)
+    gb = np.stack([rng.uniform(0.5, 1.5, k), rng.uniform(-0.5, 0.5, k)]).astype(np.float32)
+    pool = session.pool
+    xt = autodiff.make_data(pool, x, dtype=BF16)
+    wp = autodiff.make_param(pool, wt, "w")
+    gbt = autodiff.make_param(pool, gb, "gb")
+    conv = layers.conv2d(xt, wp, st, pad, pool, bn_stats=True)
+    assert conv.bn_partials is not None
+    cdata = conv.data.astype(np.float64)
+    y = layers.batchnorm(conv, gbt, pool, relu=True)
+    ref, (_xhat, invstd, _g, mean) = X.batchnorm_fwd(cdata, gb[0], gb[1], relu=True)
+    assert rel(y.data, X.round_bf16(ref)) < 1e-3
+    assert conv.bn_partials is None  # consumed and returned to the pool
+    node_saved = y.node.saved
+    np.testing.assert_allclose(node_saved[2].data, mean, rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(node_saved[3].data, invstd, rtol=1e-4)
