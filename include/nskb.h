@@ -157,14 +157,15 @@ int nsk_scale_multi(int n_tensors, float* const* g, const uint64_t* numel, const
  * y = relu?((x-mean)*invstd*gamma + beta + residual?);  ws: nsk_bn_workspace(rows, C) bytes */
 uint64_t nsk_bn_workspace(uint64_t rows, int C);
 int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
-               float eps, int relu, const void* residual, float* ws, void* stream);
+               float eps, int relu, const void* residual, void* relu_mask, float* ws, void* stream);
 /* nsk_bn_fwd with the statistics taken from conv partials (nsk_conv2d_fprop_stats) instead of a pass over x */
 int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
                         float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
-                        float* ws, void* stream);
-/* y_relu: the forward output when the op applied ReLU (mask = y > 0), else NULL. dres (optional) receives the
- * masked gradient flowing to the residual input. dgamma_beta [2, C] (= dgamma_beta*beta_acc + new). */
-int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* gamma_beta, const float* mean,
+                        void* relu_mask, float* ws, void* stream);
+/* relu_mask (fwd output, bwd input; NULL without ReLU): one byte per 8 channels, bit j = [y > 0] of channel
+ * 8k+j, rows*C/8 bytes. dres (optional) receives the masked gradient flowing to the residual input.
+ * dgamma_beta [2, C] (= dgamma_beta*beta_acc + new). */
+int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float* gamma_beta, const float* mean,
                const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
                float* ws, void* stream);
 int nsk_avgpool_fwd(int dtype_in, const void* x, float* y, int N, int HW, int C, void* stream);

@@ -5,6 +5,8 @@
 // storage, float64 accumulation of the statistics, biased batch variance.
 //   fwd: y = relu( (x - mean) * invstd * gamma + beta  [+ residual] )
 //   bwd: dz = dy * [y > 0];  dbeta = sum dz;  dgamma = sum dz * xhat
+// The ReLU mask [y > 0] is kept as one bit per element (one byte per 8 channels, written by the forward
+// apply), so the backward passes read 1/16 of the bytes a bf16 y would cost.
 //        dx = gamma*invstd*(dz - dbeta/M - xhat*dgamma/M);  dres = dz
 // x / y / dy / dx / residual are NHWC bf16 viewed as [rows, C]; gamma_beta is
 // the fp32 parameter [2, C]. Each pass is a vectorised (8 x bf16) sweep;
@@ -134,7 +136,8 @@ __global__ void __launch_bounds__(FT) bn_fwd_finalize(const float* part, int nbl
 __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __restrict__ x,
                                                       const __nv_bfloat16* __restrict__ res,
                                                       const float* __restrict__ scale, const float* __restrict__ shift,
-                                                      __nv_bfloat16* __restrict__ y, uint64_t rows, int C, int relu) {
+                                                      __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
+                                                      uint64_t rows, int C, int relu) {
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
@@ -150,13 +153,19 @@ __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __res
       f[j] = v;
     }
     st8(y + i * 8, f);
+    if (mask) {
+      unsigned bits = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bits |= (f[j] > 0.f ? 1u : 0u) << j;
+      mask[i] = (uint8_t)bits;
+    }
   }
 }
 
 // bwd pass 1: sum dz and sum dz*x per channel, dz = dy * [y > 0] (relu) or dy
 __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* __restrict__ dy,
                                                            const __nv_bfloat16* __restrict__ x,
-                                                           const __nv_bfloat16* __restrict__ y, uint64_t rows, int C,
+                                                           const uint8_t* __restrict__ mask, uint64_t rows, int C,
                                                            float* part) {
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
@@ -166,11 +175,10 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
     float g[8], xv[8];
     ld8(dy + off, g);
     ld8(x + off, xv);
-    if (y) {
-      float yv[8];
-      ld8(y + off, yv);
+    if (mask) {
+      const unsigned m = __ldg(mask + off / 8);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = yv[j] > 0.f ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = ((m >> j) & 1u) ? g[j] : 0.f;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(FT) bn_bwd_finalize(const float* part, int nbl
 
 __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* __restrict__ dy,
                                                           const __nv_bfloat16* __restrict__ x,
-                                                          const __nv_bfloat16* __restrict__ y,
+                                                          const uint8_t* __restrict__ mask,
                                                           const float* __restrict__ coef,
                                                           __nv_bfloat16* __restrict__ dx,
                                                           __nv_bfloat16* __restrict__ dres, uint64_t rows, int C) {
@@ -221,11 +229,10 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
     float g[8], xv[8];
     ld8(dy + i * 8, g);
     ld8(x + i * 8, xv);
-    if (y) {
-      float yv[8];
-      ld8(y + i * 8, yv);
+    if (mask) {
+      const unsigned m = __ldg(mask + i);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = yv[j] > 0.f ? g[j] : 0.f;
+      for (int j = 0; j < 8; ++j) g[j] = ((m >> j) & 1u) ? g[j] : 0.f;
     }
     if (dres) st8(dres + i * 8, g);
     float o[8];
@@ -260,7 +267,7 @@ uint64_t nsk_bn_workspace(uint64_t rows, int C) {
 }
 
 int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
-               float eps, int relu, const void* residual, float* ws, void* stream) {
+               float eps, int relu, const void* residual, void* relu_mask, float* ws, void* stream) {
   int rc = check(rows, C, x, residual);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -274,7 +281,7 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   bn_fwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
   bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
-                                                        shift, (__nv_bfloat16*)y, rows, C, relu);
+                                                        shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd");
   return NSK_OK;
 }
@@ -283,7 +290,7 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
 // no statistics pass over x
 int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
                         float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
-                        float* ws, void* stream) {
+                        void* relu_mask, float* ws, void* stream) {
   int rc = check(rows, C, x, residual);
   if (rc) return rc;
   if (nparts < 1) return nsk::set_error(NSK_ERR_SHAPE, "batchnorm: no statistics partials");
@@ -293,12 +300,12 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   bn_fwd_finalize<<<C, FT, 0, st>>>(partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
   bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
-                                                        shift, (__nv_bfloat16*)y, rows, C, relu);
+                                                        shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd_partials");
   return NSK_OK;
 }
 
-int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* gamma_beta, const float* mean,
+int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float* gamma_beta, const float* mean,
                const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
                float* ws, void* stream) {
   int rc = check(rows, C, dy, x);
@@ -310,12 +317,12 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* y_relu, const float* g
   float* part = ws;
   float* coef = ws + (size_t)MAXBLK * 2 * C;  // 3*C floats (workspace reserves 4*C)
   bn_bwd_reduce_kernel<<<nb, BT, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                             (const __nv_bfloat16*)y_relu, rows, C, part);
+                                             (const uint8_t*)relu_mask, rows, C, part);
   bn_bwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc,
                                                    coef);
   const uint64_t nv = rows * (uint64_t)C / 8;
   bn_bwd_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)y_relu, coef, (__nv_bfloat16*)dx,
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, coef, (__nv_bfloat16*)dx,
       (__nv_bfloat16*)dres, rows, C);
   NSK_LAUNCH_CHECK("bn_bwd");
   return NSK_OK;

@@ -202,16 +202,20 @@ def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: T
     mean = _internal_tensor(empty_tensor(pool, (c,)))
     invstd = _internal_tensor(empty_tensor(pool, (c,)))
     ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
+    # ReLU mask for the backward: one bit per element (rows*C/8 bytes, held in a float32 buffer)
+    mask = _internal_tensor(empty_tensor(pool, ((x.numel // 8 + 3) // 4,))) if relu else None
+    mp = None if mask is None else mask.ptr
+    rp = None if residual is None else residual.ptr
     parts = x.bn_partials
     if parts is not None:
         check(lib.nsk_bn_fwd_partials(parts[0].ptr, parts[1], x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c,
-                                      float(eps), int(relu), None if residual is None else residual.ptr, ws.ptr, st))
+                                      float(eps), int(relu), rp, mp, ws.ptr, st))
         release_tensor(pool, parts[0])
         x.bn_partials = None
     else:
-        check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu),
-                             None if residual is None else residual.ptr, ws.ptr, st))
-    saved = (x, gb, mean, invstd) + ((y,) if relu else ())
+        check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu), rp, mp,
+                             ws.ptr, st))
+    saved = (x, gb, mean, invstd) + ((mask,) if relu else ())
     record("batchnorm", y, x, gb, residual, saved=saved, attrs={"relu": relu, "rows": rows, "c": c})
     return y
 
@@ -219,7 +223,7 @@ def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: T
 @rule("batchnorm")
 def _r_batchnorm(node, g, pool, sinks):
     x, gb, mean, invstd = node.saved[:4]
-    y = node.saved[4] if node.attrs["relu"] else None
+    mask = node.saved[4] if node.attrs["relu"] else None
     rows, c = node.attrs["rows"], node.attrs["c"]
     lib = _lib.lib()
     st = _lib.stream()
@@ -237,7 +241,7 @@ def _r_batchnorm(node, g, pool, sinks):
     if dx is None:
         scratch_dx = empty_tensor(pool, x.shape, BF16)
     ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
-    check(lib.nsk_bn_bwd(g.ptr, x.ptr, None if y is None else y.ptr, gb.ptr, mean.ptr, invstd.ptr,
+    check(lib.nsk_bn_bwd(g.ptr, x.ptr, None if mask is None else mask.ptr, gb.ptr, mean.ptr, invstd.ptr,
                          (dx or scratch_dx).ptr, None if dres is None else dres.ptr, dgb_ptr, beta, rows, c,
                          ws.ptr, st))
     if scratch_dx is not None:

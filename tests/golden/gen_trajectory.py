@@ -1,0 +1,75 @@
+"""Generate the 100-step loss-trajectory goldens (north star: "the loss trajectory over 100 steps must stay
+within 1%") by running the float64 oracle on a fixed synthetic dataset.
+
+    python tests/golden/gen_trajectory.py [resnet18|smallcnn] [steps]
+
+Dataset: TRAJ_ROWS synthetic images x ~ N(0,1) [3, 32, 32] (seed 7) with learnable labels (argmax of a fixed
+random projection of a 4x4-subsampled view, 30% replaced by random labels so the loss stays away from zero),
+shuffled per epoch exactly like the reference dataset (dataset.py:93-121 via
+oracle.ref_ops.epoch_permutation / batch_rows), batch TRAJ_BATCH, SGD lr 0.01 m 0.9.
+Writes tests/golden/trajectory_<model>.npz with the per-step losses of the float64 oracle (bf16=False, the
+reference's own arithmetic) and of the bf16-emulating oracle (bf16=True). The GPU test replays the same
+schedule through the device Trainer.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from oracle import models as om  # noqa: E402
+from oracle import ref_ops as R  # noqa: E402
+
+TRAJ_ROWS = 1024
+TRAJ_BATCH = 32
+LR, MOMENTUM = 0.01, 0.9
+
+
+def dataset():
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((TRAJ_ROWS, 3, 32, 32)).astype(np.float32)
+    proj = rng.standard_normal((3 * 8 * 8, 10))
+    y = (x[:, :, ::4, ::4].reshape(TRAJ_ROWS, -1) @ proj).argmax(axis=1).astype(np.float32)
+    noise = rng.random(TRAJ_ROWS) < 0.3
+    y[noise] = rng.integers(0, 10, int(noise.sum()))
+    return x, y
+
+
+def schedule(steps: int):
+    """Row indices of each step's batch: per-epoch permutations (seed 11), contiguous batches."""
+    per_epoch = TRAJ_ROWS // TRAJ_BATCH
+    perms = R.epoch_permutation(11, TRAJ_ROWS, (steps + per_epoch - 1) // per_epoch)
+    return [R.batch_rows(perms[s // per_epoch], s % per_epoch, TRAJ_BATCH) for s in range(steps)]
+
+
+def make_oracle(model: str):
+    return om.ResNet18Oracle(seed=0) if model == "resnet18" else om.SmallCNNOracle(seed=0)
+
+
+def main():
+    model = sys.argv[1] if len(sys.argv) > 1 else "resnet18"
+    steps = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+    x, y = dataset()
+    sched = schedule(steps)
+    out = {}
+    for bf16 in (False, True):
+        ref = make_oracle(model)
+        losses = []
+        t0 = time.time()
+        for s, rows in enumerate(sched):
+            losses.append(ref.train_step(x[rows], y[rows], lr=LR, momentum=MOMENTUM, bf16=bf16))
+            if s % 10 == 0:
+                print(model, "bf16" if bf16 else "f64", s, losses[-1], f"{time.time() - t0:.0f}s", flush=True)
+        out["bf16" if bf16 else "f64"] = np.asarray(losses)
+    np.savez_compressed(os.path.join(HERE, f"trajectory_{model}.npz"), **out)
+    print("spread bf16 vs f64:", float(np.max(np.abs(out["bf16"] - out["f64"]) / out["f64"])))
+
+
+if __name__ == "__main__":
+    main()

@@ -228,3 +228,37 @@ def test_resnet50_graphed_training_steps(dev):
         losses[mode] = [float(tr.step(x, y)) for x, y in zip(xs, ys)]
     np.testing.assert_allclose(losses[True], losses[False], rtol=1e-5)
     assert all(np.isfinite(losses[True]))
+
+
+@pytest.mark.parametrize("model", ["smallcnn", "resnet18"])
+def test_loss_trajectory_100_steps(dev, model):
+    """North star: the 100-step loss trajectory stays within 1% of the CPU reference (float64 oracle), on the
+    committed golden (tests/golden/gen_trajectory.py: fixed synthetic dataset, reference epoch shuffling,
+    batch 32, SGD lr 0.01 m 0.9). Bar: every 10-step window mean within 1%; each single step within
+    max(2%, 2x the oracle's own bf16-vs-f64 deviation at that step)."""
+    import importlib.util
+    import os
+
+    from paper_2409_11600_b200.models import ResNet18, SmallCNN
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    spec = importlib.util.spec_from_file_location("gen_trajectory", os.path.join(here, "gen_trajectory.py"))
+    G = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(G)
+    gold = np.load(os.path.join(here, f"trajectory_{model}.npz"))
+    f64, b16 = gold["f64"], gold["bf16"]
+    x, y = G.dataset()
+    sched = G.schedule(len(f64))
+    s = Session(seed=0)
+    net = ResNet18(s) if model == "resnet18" else SmallCNN(s)
+    tr = Trainer(s, net, (G.TRAJ_BATCH, 3, 32, 32), 10, optimizer=("sgd", G.LR, G.MOMENTUM), graph=True, warmup=2)
+    got = np.array([float(tr.step(x[rows], y[rows])) for rows in sched])
+    assert np.all(np.isfinite(got))
+    win = lambda a: a.reshape(-1, 10).mean(axis=1)  # noqa: E731
+    wdev = np.abs(win(got) - win(f64)) / win(f64)
+    assert wdev.max() <= 1e-2, (wdev.max(), np.round(win(got), 4), np.round(win(f64), 4))
+    step_dev = np.abs(got - f64) / f64
+    bar = np.maximum(2e-2, 2 * np.abs(b16 - f64) / f64)
+    assert np.all(step_dev <= bar), (int(np.argmax(step_dev - bar)), step_dev.max())
