@@ -93,6 +93,8 @@ int nsk_conv2d_fprop(const NskConvDesc* d, const void* x, const void* w, void* y
 int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, void* y, float* partials,
                            uint64_t partial_floats, int* nparts, void* stream);
 int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream);
+/* dx = dgrad + beta * dx (bf16, in place): accumulates a second gradient contribution in the epilogue */
+int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, void* stream);
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d);
 int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float* dw, float beta, void* ws,
                      uint64_t ws_bytes, void* stream);

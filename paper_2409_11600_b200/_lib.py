@@ -62,6 +62,7 @@ SIGNATURES = {
     "nsk_conv2d_fprop": (i32, [C.POINTER(ConvDesc), vp, vp, vp, i32, vp]),
     "nsk_conv2d_fprop_stats": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp, u64, C.POINTER(C.c_int), vp]),
     "nsk_conv2d_dgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp]),
+    "nsk_conv2d_dgrad_acc": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp]),
     "nsk_conv2d_wgrad_workspace": (u64, [C.POINTER(ConvDesc)]),
     "nsk_conv2d_wgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp, u64, vp]),
     "nsk_gemm_simt": (i32, [i32, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, f32, vp]),

@@ -170,50 +170,53 @@ __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
   }
 }
 
-// Fused layout change + im2col for image stems: x is the host-layout NCHW float32 batch; each thread
-// writes 8 consecutive columns (one 16-byte store) of out[(n,p,q), k], k = (r*S + s)*C + c.
-// One block per (image, output row): the R input rows it needs (all channels, zero-padded) are staged
-// in shared memory with coalesced loads, then the block writes its Q contiguous im2col rows as 16-byte
-// stores (consecutive threads -> consecutive bytes).
+// Fused layout change + im2col for image stems (x is the host-layout NCHW float32 batch).
+// One thread per (output pixel, 8-column group) of the [N*P*Q, Kp] bf16 cols matrix; column kk = (r*S + s)*C + c
+// (KRSC filter order) gathers x[n, c, p*st - pad + r, q*st - pad + s] from the NCHW float32 batch. The kk ->
+// (c, r, s) decode comes from a shared-memory table so the loop body is loads and converts only.
 __global__ void im2col_nchw_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int N, int C, int H,
                                    int W, int R, int S, int st, int pad, int P, int Q, int Kp) {
-  extern __shared__ float halo[];  // [C][R][Wp]
-  const int Wp = W + 2 * pad;
-  const int groups = Kp / 8;
+  extern __shared__ int tab[];  // [Kp]: (c << 16) | (r << 8) | s, or -1 for padding columns
   const int RSC = R * S * C;
-  for (long long row = blockIdx.x; row < (long long)N * P; row += gridDim.x) {
-    const long long b = row / P;
-    const int p = (int)(row - b * P);
-    __syncthreads();
-    for (int i = threadIdx.x; i < C * R * Wp; i += blockDim.x) {
-      const int wq = i % Wp, cr = i / Wp;
-      const int r = cr % R, c = cr / R;
-      const int h = p * st - pad + r, w = wq - pad;
-      halo[i] = (h >= 0 && h < H && w >= 0 && w < W) ? x[((b * C + c) * H + h) * W + w] : 0.f;
+  for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
+    if (kk < RSC) {
+      const int c = kk % C, rs = kk / C;
+      tab[kk] = (c << 16) | ((rs / S) << 8) | (rs % S);
+    } else {
+      tab[kk] = -1;
     }
-    __syncthreads();
-    __nv_bfloat16* orow = out + row * (long long)Q * Kp;
-    for (int i = threadIdx.x; i < Q * groups; i += blockDim.x) {
-      const int q = i / groups, g = i - q * groups;
-      float v[8];
+  }
+  __syncthreads();
+  const int groups = Kp / 8;
+  const long long total = (long long)N * P * Q * groups;
+  const long long HW = (long long)H * W;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int g = (int)(i % groups);
+    const long long pix = i / groups;
+    const int q = (int)(pix % Q);
+    const long long np = pix / Q;
+    const int p = (int)(np % P);
+    const long long n = np / P;
+    const int h0 = p * st - pad, w0 = q * st - pad;
+    const float* xb = x + n * C * HW;
+    float v[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int kk = g * 8 + e;
-        float val = 0.f;
-        if (kk < RSC) {
-          const int c = kk % C, rs = kk / C;
-          const int s = rs % S, r = rs / S;
-          val = halo[(c * R + r) * Wp + q * st + s];
-        }
-        v[e] = val;
+    for (int e = 0; e < 8; ++e) {
+      const int t = tab[g * 8 + e];
+      float val = 0.f;
+      if (t >= 0) {
+        const int h = h0 + ((t >> 8) & 0xff), w = w0 + (t & 0xff);
+        if (h >= 0 && h < H && w >= 0 && w < W) val = __ldg(xb + (t >> 16) * HW + (long long)h * W + w);
       }
-      uint4 u;
-      u.x = pack_bf16x2(v[0], v[1]);
-      u.y = pack_bf16x2(v[2], v[3]);
-      u.z = pack_bf16x2(v[4], v[5]);
-      u.w = pack_bf16x2(v[6], v[7]);
-      *(uint4*)(orow + (long long)q * Kp + g * 8) = u;
+      v[e] = val;
     }
+    uint4 u;
+    u.x = pack_bf16x2(v[0], v[1]);
+    u.y = pack_bf16x2(v[2], v[3]);
+    u.z = pack_bf16x2(v[4], v[5]);
+    u.w = pack_bf16x2(v[6], v[7]);
+    *(uint4*)(out + pix * Kp + g * 8) = u;
   }
 }
 
@@ -346,11 +349,11 @@ int nsk_im2col(const void* x, void* out, int N, int H, int W, int C, int R, int 
 int nsk_im2col_nchw(const float* x, void* out, int N, int C, int H, int W, int R, int S, int stride, int pad, int P,
                     int Q, int Kp, void* stream) {
   if (Kp % 8) return nsk::set_error(NSK_ERR_UNSUPPORTED, "im2col_nchw: Kp must be a multiple of 8");
-  const size_t smem = (size_t)C * R * (W + 2 * pad) * sizeof(float);
-  if (smem > 48 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "im2col_nchw: image rows too wide");
-  long long rows = (long long)N * P;
-  unsigned grid = (unsigned)(rows < 16LL * nsk::sm_count() ? rows : 16LL * nsk::sm_count());
-  im2col_nchw_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)out, N, C, H, W, R, S, stride, pad,
+  if (R > 255 || S > 255 || C > 32767 || Kp > 8192)
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "im2col_nchw: filter too large");
+  const size_t smem = (size_t)Kp * sizeof(int);
+  const long long n = (long long)N * P * Q * (Kp / 8);
+  im2col_nchw_kernel<<<nsk::grid_for(n, 256), 256, smem, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)out, N, C, H, W, R, S, stride, pad,
                                                                 P, Q, Kp);
   NSK_LAUNCH_CHECK("im2col_nchw");
   return NSK_OK;

@@ -41,11 +41,70 @@ __global__ void simt_gemm_kernel(int a_mn, int b_mn, int M, int N, int K, const 
   }
 }
 
+// Skinny products (few outputs, long K: the classifier layer and its weight gradient): one warp per output,
+// lanes stride K (coalesced along K-major rows), float64 warp reduction.
+__global__ void simt_dot_kernel(int a_mn, int b_mn, int M, int N, int K, const float* __restrict__ A, long long lda,
+                                const float* __restrict__ B, long long ldb, float* C, long long ldc,
+                                const float* __restrict__ bias, float beta) {
+  const int lane = threadIdx.x & 31;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long o = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < (long long)M * N;
+       o += warps) {
+    const int m = (int)(o / N), n = (int)(o - (long long)m * N);
+    double acc = 0.0;
+    for (int k = lane; k < K; k += 32) {
+      const float a = a_mn ? A[(long long)k * lda + m] : A[(long long)m * lda + k];
+      const float b = b_mn ? B[(long long)k * ldb + n] : B[(long long)n * ldb + k];
+      acc += (double)a * (double)b;
+    }
+    acc = warp_sum_d(acc);
+    if (lane == 0) {
+      if (bias) acc += (double)bias[n];
+      float* c = C + (long long)m * ldc + n;
+      const float r = (float)acc;
+      *c = beta != 0.f ? r + beta * *c : r;
+    }
+  }
+}
+
+// Short K (e.g. the classifier's input gradient, K = classes): one thread per output.
+__global__ void simt_short_k_kernel(int a_mn, int b_mn, int M, int N, int K, const float* __restrict__ A,
+                                    long long lda, const float* __restrict__ B, long long ldb, float* C,
+                                    long long ldc, const float* __restrict__ bias, float beta) {
+  for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < (long long)M * N;
+       o += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(o / N), n = (int)(o - (long long)m * N);
+    double acc = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const float a = a_mn ? A[(long long)k * lda + m] : A[(long long)m * lda + k];
+      const float b = b_mn ? B[(long long)k * ldb + n] : B[(long long)n * ldb + k];
+      acc += (double)a * (double)b;
+    }
+    if (bias) acc += (double)bias[n];
+    float* c = C + (long long)m * ldc + n;
+    const float r = (float)acc;
+    *c = beta != 0.f ? r + beta * *c : r;
+  }
+}
+
 }  // namespace
 
 extern "C" int nsk_gemm_simt(int a_mn, int b_mn, int M, int N, int K, const float* A, long long lda, const float* B,
                              long long ldb, float* C, long long ldc, const float* bias, float beta, void* stream) {
   if (M < 1 || N < 1 || K < 1) return nsk::set_error(NSK_ERR_SHAPE, "gemm: empty problem");
+  const long long outs = (long long)M * N;
+  if (K <= 32) {
+    simt_short_k_kernel<<<nsk::grid_for(outs, 256), 256, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B,
+                                                                                   ldb, C, ldc, bias, beta);
+    NSK_LAUNCH_CHECK("simt_short_k");
+    return NSK_OK;
+  }
+  if (outs <= 65536) {
+    simt_dot_kernel<<<nsk::grid_for(outs * 32, 256), 256, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B,
+                                                                                    ldb, C, ldc, bias, beta);
+    NSK_LAUNCH_CHECK("simt_dot");
+    return NSK_OK;
+  }
   dim3 grid((N + TS - 1) / TS, (M + TS - 1) / TS), block(TS, TS);
   simt_gemm_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B, ldb, C, ldc, bias, beta);
   NSK_LAUNCH_CHECK("simt_gemm");

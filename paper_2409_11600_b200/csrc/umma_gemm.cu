@@ -88,6 +88,20 @@ struct Smem {
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
+// bf16x8 beta*old + v (fp32 math, one rounding): the same value the axpy kernel would produce
+__device__ __forceinline__ uint4 bf16x8_axpby(uint4 old, float beta, uint4 v) {
+  const __nv_bfloat162* o2 = (const __nv_bfloat162*)&old;
+  const __nv_bfloat162* v2 = (const __nv_bfloat162*)&v;
+  uint4 r;
+  uint32_t* r32 = (uint32_t*)&r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 a = __bfloat1622float2(o2[i]), b = __bfloat1622float2(v2[i]);
+    r32[i] = pack_bf16x2(beta * a.x + b.x, beta * a.y + b.y);
+  }
+  return r;
+}
+
 // named barrier over the four epilogue warps (128 threads)
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
@@ -456,8 +470,12 @@ __global__ void __launch_bounds__(256, 1)
             const int pr = piece >> 2, part = piece & 3;
             const long long ro = __shfl_sync(0xffffffffu, row_off, pr);
             const int ok = __shfl_sync(0xffffffffu, (int)row_ok, pr);
-            if (ok)
-              *(uint4*)((__nv_bfloat16*)p.out + ro + col0 + part * 8) = *(const uint4*)(stg + pr * kStgPitch + part * 16);
+            if (ok) {
+              uint4* dst = (uint4*)((__nv_bfloat16*)p.out + ro + col0 + part * 8);
+              uint4 val = *(const uint4*)(stg + pr * kStgPitch + part * 16);
+              if (p.beta != 0.f) val = bf16x8_axpby(*dst, p.beta, val);  // accumulate into an existing gradient
+              *dst = val;
+            }
           }
           __syncwarp();
         } else if (row_ok) {
@@ -887,6 +905,11 @@ int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, v
 // stride 1: one launch over all taps; stride 2: four output-parity classes
 // (blockIdx.z), each a stride-1 gather over dy with its subset of taps.
 int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream) {
+  return nsk_conv2d_dgrad_acc(d, dy, w, dx, 0.f, stream);
+}
+
+// dx = dgrad + beta * dx (bf16 in place): a second gradient contribution accumulated in the epilogue
+int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, void* stream) {
   int rc = check_desc(d);
   if (rc) return rc;
   const int P = d->P, Q = d->Q, st = d->stride;
@@ -940,6 +963,7 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
   p.out = dx;
   p.ldc = d->C;
   p.out_f32 = 0;
+  p.beta = beta;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls, 128))) return rc;
   } else if (ncls == 1) {

@@ -14,12 +14,25 @@ namespace {
 
 constexpr int XT = 1024;
 
-__global__ void __launch_bounds__(XT) xent_fwd_kernel(const float* __restrict__ z, const float* __restrict__ tgt, int m,
-                                                      int c, float* __restrict__ probs, float* loss, int* err) {
-  __shared__ double part[XT / 32];
+// One warp per row, XW rows per block; block partial sums of (lse - z_t) go to a library scratch and the last
+// block to finish (ticket) folds them in block order: deterministic, one launch, any batch size.
+constexpr int XW = 8;
+
+struct XentScratch {
+  double* part = nullptr;
+  unsigned* ticket = nullptr;
+  int cap = 0;
+};
+
+__global__ void __launch_bounds__(XW * 32) xent_fwd_kernel(const float* __restrict__ z, const float* __restrict__ tgt,
+                                                           int m, int c, float* __restrict__ probs, float* loss,
+                                                           int* err, double* part, unsigned* ticket) {
+  __shared__ double wpart[XW];
+  __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double wsum = 0.0;
-  for (int row = warp; row < m; row += XT / 32) {
+  const int row = blockIdx.x * XW + warp;
+  double term = 0.0;
+  if (row < m) {
     const float* zr = z + (long long)row * c;
     double mx = -INFINITY;
     for (int j = lane; j < c; j += 32) mx = fmax(mx, (double)zr[j]);
@@ -38,14 +51,24 @@ __global__ void __launch_bounds__(XT) xent_fwd_kernel(const float* __restrict__ 
       if (lane == 0 && err) atomicMin(err, row);
       t = 0;
     }
-    if (lane == 0) wsum += lse - ((double)zr[t] - mx);
+    term = lse - ((double)zr[t] - mx);
   }
-  if (lane == 0) part[warp] = wsum;
+  if (lane == 0) wpart[warp] = term;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < XT / 32; ++i) s += part[i];
+    for (int i = 0; i < XW; ++i) s += wpart[i];
+    part[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += ((volatile double*)part)[b];
     loss[0] = (float)(s / (double)m);
+    *ticket = 0;  // ready for the next launch (graph replays)
   }
 }
 
@@ -133,7 +156,25 @@ extern "C" {
 int nsk_xent_fwd(const float* logits, const float* targets, int m, int c, float* probs, float* loss_out, int* err_flag,
                  void* stream) {
   if (m < 1 || c < 1) return nsk::set_error(NSK_ERR_SHAPE, "cross_entropy: empty logits");
-  xent_fwd_kernel<<<1, XT, 0, (cudaStream_t)stream>>>(logits, targets, m, c, probs, loss_out, err_flag);
+  static XentScratch sc;
+  const int blocks = (m + XW - 1) / XW;
+  if (blocks > sc.cap) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing((cudaStream_t)stream, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return nsk::set_error(NSK_ERR_UNSUPPORTED, "cross_entropy: scratch must be sized before graph capture");
+    if (sc.part) {
+      cudaStreamSynchronize((cudaStream_t)stream);
+      cudaFree(sc.part);
+    }
+    const int cap = blocks < 1024 ? 1024 : blocks;
+    NSK_CUDA(cudaMalloc(&sc.part, cap * sizeof(double) + 64));
+    sc.ticket = (unsigned*)(sc.part + cap);
+    NSK_CUDA(cudaMemset(sc.ticket, 0, sizeof(unsigned)));
+    sc.cap = cap;
+  }
+  xent_fwd_kernel<<<blocks, XW * 32, 0, (cudaStream_t)stream>>>(logits, targets, m, c, probs, loss_out, err_flag,
+                                                                sc.part, sc.ticket);
   NSK_LAUNCH_CHECK("xent_fwd");
   return NSK_OK;
 }

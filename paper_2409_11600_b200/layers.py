@@ -100,9 +100,10 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str 
         if xtmp is not None:
             release_tensor(pool, xtmp)
     else:
-        # small-channel stem: explicit im2col (K = R*S*C padded to 64) + tcgen05 GEMM
+        # small-channel stem: explicit im2col (K = R*S*C padded to a multiple of 8: TMA row pitch; the GEMM's
+        # 64-wide K boxes read zeros past kp) + tcgen05 GEMM
         rsc = r * s * c
-        kp = (rsc + 63) // 64 * 64
+        kp = (rsc + 7) // 8 * 8
         cols = empty_tensor(pool, (n * p * q, kp), BF16)
         if nchw:
             check(lib.nsk_im2col_nchw(xp, cols.ptr, n, c, h, wd, r, s, stride, pad, p, q, kp, st))
@@ -131,7 +132,11 @@ def _r_conv2d(node, g, pool, sinks):
     dx = dw = None
     gp, gtmp = _temp_bf16(g, pool)
     if node.inputs[0].requires_grad:
-        dx = empty_tensor(pool, tuple(node.inputs[0].tensor.shape), BF16)
+        acc = (node.acc_sinks or {}).get(0)
+        xshape = tuple(node.inputs[0].tensor.shape)
+        if acc is not None and (acc.dtype != BF16 or acc.shape != xshape or node.attrs["stem"]):
+            acc = None
+        dx = SUNK if acc is not None else empty_tensor(pool, xshape, BF16)
         wb = w.bf16_ptr() if w.dtype == F32 else w.ptr
         if node.attrs.get("nchw"):
             raise NskRuntimeError("conv2d(layout='nchw') input is image data and has no gradient")
@@ -149,6 +154,8 @@ def _r_conv2d(node, g, pool, sinks):
                                  desc.pad, desc.P, desc.Q, kp, st))
             release_tensor(pool, dcols)
             release_tensor(pool, wpk)
+        elif acc is not None:  # second contribution: accumulate into the pending gradient in the epilogue
+            check(lib.nsk_conv2d_dgrad_acc(C.byref(desc), gp, wb, acc.ptr, 1.0, st))
         else:
             check(lib.nsk_conv2d_dgrad(C.byref(desc), gp, wb, dx.ptr, st))
     if node.inputs[1].requires_grad:
