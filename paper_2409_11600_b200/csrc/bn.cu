@@ -70,6 +70,7 @@ __device__ void block_reduce_store(float* s1, float* s2, int C, float* part) {
 // pass 1 of fwd: sum x and sum x^2 per channel
 __global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __restrict__ x, uint64_t rows, int C,
                                                       float* part) {
+  pdl_wait();
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -117,6 +118,7 @@ __device__ void fold_partials(const float* part, int nblk, int C, int c, double*
 __global__ void __launch_bounds__(FT) bn_fwd_finalize(const float* part, int nblk, uint64_t rows, int C, float eps,
                                                       const float* gb, float* mean, float* invstd, float* scale,
                                                       float* shift) {
+  pdl_wait();
   const int c = blockIdx.x;
   double a, b;
   fold_partials(part, nblk, C, c, &a, &b);
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __res
                                                       const float* __restrict__ scale, const float* __restrict__ shift,
                                                       __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
                                                       uint64_t rows, int C, int relu) {
+  pdl_wait();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
                                                            const __nv_bfloat16* __restrict__ x,
                                                            const uint8_t* __restrict__ mask, uint64_t rows, int C,
                                                            float* part) {
+  pdl_wait();
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
 __global__ void __launch_bounds__(FT) bn_bwd_finalize(const float* part, int nblk, uint64_t rows, int C,
                                                       const float* gb, const float* mean, const float* invstd,
                                                       float* dgb, float beta_acc, float* coef) {
+  pdl_wait();
   const int c = blockIdx.x;
   double sdz, sdzx;
   fold_partials(part, nblk, C, c, &sdz, &sdzx);
@@ -222,6 +227,7 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
                                                           const float* __restrict__ coef,
                                                           __nv_bfloat16* __restrict__ dx,
                                                           __nv_bfloat16* __restrict__ dres, uint64_t rows, int C) {
+  pdl_wait();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
@@ -277,10 +283,10 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   float* part = ws;
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
-  bn_stats_kernel<<<nb, BT, smem, st>>>((const __nv_bfloat16*)x, rows, C, part);
-  bn_fwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  nsk::launch_pdl(bn_stats_kernel, nb, BT, smem, st, (const __nv_bfloat16*)x, rows, C, part);
+  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
+  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
                                                         shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd");
   return NSK_OK;
@@ -297,9 +303,9 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   cudaStream_t st = (cudaStream_t)stream;
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
-  bn_fwd_finalize<<<C, FT, 0, st>>>(partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  bn_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>((const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
+  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
                                                         shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd_partials");
   return NSK_OK;
@@ -316,12 +322,12 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   const size_t smem = 2 * (size_t)RPB * C * sizeof(float);
   float* part = ws;
   float* coef = ws + (size_t)MAXBLK * 2 * C;  // 3*C floats (workspace reserves 4*C)
-  bn_bwd_reduce_kernel<<<nb, BT, smem, st>>>((const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+  nsk::launch_pdl(bn_bwd_reduce_kernel, nb, BT, smem, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
                                              (const uint8_t*)relu_mask, rows, C, part);
-  bn_bwd_finalize<<<C, FT, 0, st>>>(part, nb, rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc,
+  nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, part, nb, rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc,
                                                    coef);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  bn_bwd_apply_kernel<<<nsk::grid_for(nv, BT), BT, 0, st>>>(
+  nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, 
       (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, coef, (__nv_bfloat16*)dx,
       (__nv_bfloat16*)dres, rows, C);
   NSK_LAUNCH_CHECK("bn_bwd");

@@ -11,6 +11,7 @@
 #include <stdint.h>
 #include <string>
 #include <cstdio>
+#include <utility>
 
 // ---- status codes (include/nskb.h) ------------------------------------------
 #define NSK_OK 0
@@ -48,6 +49,28 @@ int encode_tmap(CUtensorMap* map, CUtensorMapDataType dt, int rank, const void* 
 int encode_tmap_im2col(CUtensorMap* map, const void* gaddr, int N, int H, int W, int C, const int* lower_wh,
                        const int* upper_wh, int pixels, int stride);
 
+// Programmatic dependent launch: every libnskb kernel is launched with programmatic stream serialization
+// and starts with pdl_wait() (griddepcontrol.wait), so inside a captured step the next kernel is already
+// launched and resident while its predecessor drains; the wait still orders all memory accesses.
+// NSK_PDL=0 turns the attribute off (plain stream order).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 inline unsigned grid_for(int64_t n, int block, int per_thread = 1) {
   int64_t g = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
   int64_t cap = (int64_t)sm_count() * 16;
@@ -60,6 +83,9 @@ inline unsigned grid_for(int64_t n, int block, int per_thread = 1) {
 
 // ---- device helpers ---------------------------------------------------------
 #ifdef __CUDACC__
+
+// wait for the programmatic predecessor grid (no-op when launched without a programmatic dependency)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);

@@ -90,6 +90,7 @@ constexpr bool binary(int k) { return k == NSK_EW_ADD || k == NSK_EW_SUB || k ==
 template <typename T, bool BWD>
 __global__ void ew_kernel(int kind, const T* __restrict__ a, const T* __restrict__ b, float s, T* __restrict__ out,
                           uint64_t n, bool vec) {
+  pdl_wait();
   using V = Vec<T>;
   const bool needb = BWD ? (kind == NSK_EW_RELU || kind == NSK_EW_SIGMOID || kind == NSK_EW_TANH ||
                             kind == NSK_EW_HADAMARD)
@@ -121,6 +122,7 @@ __global__ void ew_kernel(int kind, const T* __restrict__ a, const T* __restrict
 
 template <typename T>
 __global__ void axpy_kernel(T* y, const T* __restrict__ x, float alpha, uint64_t n, bool vec) {
+  pdl_wait();
   using V = Vec<T>;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -142,12 +144,14 @@ __global__ void axpy_kernel(T* y, const T* __restrict__ x, float alpha, uint64_t
 
 template <typename T>
 __global__ void fill_kernel(T* p, uint64_t n, float v) {
+  pdl_wait();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) Vec<T>::st1(p + i, v);
 }
 
 template <typename S, typename D>
 __global__ void cast_kernel(const S* __restrict__ s, D* __restrict__ d, uint64_t n) {
+  pdl_wait();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
     Vec<D>::st1(d + i, Vec<S>::ld1(s + i));
@@ -156,6 +160,7 @@ __global__ void cast_kernel(const S* __restrict__ s, D* __restrict__ d, uint64_t
 template <typename T>
 __global__ void bias_add_kernel(const T* __restrict__ x, const float* __restrict__ b, T* __restrict__ out,
                                 uint64_t rows, uint64_t cols) {
+  pdl_wait();
   const uint64_t n = rows * cols;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -167,6 +172,7 @@ __global__ void bias_add_kernel(const T* __restrict__ x, const float* __restrict
 template <typename T>
 __global__ void colsum_kernel(const T* __restrict__ g, float* __restrict__ out, uint64_t rows, uint64_t cols,
                               float beta) {
+  pdl_wait();
   __shared__ float red[8][33];
   const uint64_t c = (uint64_t)blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
@@ -183,6 +189,7 @@ __global__ void colsum_kernel(const T* __restrict__ g, float* __restrict__ out, 
 }
 
 __global__ void check_idx_kernel(const float* idx, uint64_t m, int classes, int* err) {
+  pdl_wait();
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     float v = idx[i];
     if (!(v >= 0.f && v < (float)classes && v == floorf(v))) atomicMin(err, (int)i);
@@ -190,6 +197,7 @@ __global__ void check_idx_kernel(const float* idx, uint64_t m, int classes, int*
 }
 
 __global__ void onehot_kernel(const float* idx, uint64_t m, int classes, float* out) {
+  pdl_wait();
   const uint64_t n = m * (uint64_t)classes;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t r = i / classes;
@@ -200,6 +208,7 @@ __global__ void onehot_kernel(const float* idx, uint64_t m, int classes, float* 
 
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ s, T* __restrict__ d, uint64_t rows, uint64_t cols) {
+  pdl_wait();
   __shared__ T tile[32][33];
   uint64_t c = (uint64_t)blockIdx.x * 32 + threadIdx.x;
   uint64_t r = (uint64_t)blockIdx.y * 32 + threadIdx.y;
@@ -220,14 +229,14 @@ extern "C" {
 
 int nsk_fill_f32(float* p, uint64_t n, float value, void* stream) {
   if (n == 0) return NSK_OK;
-  fill_kernel<float><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(p, n, value);
+  nsk::launch_pdl(fill_kernel<float>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, p, n, value);
   NSK_LAUNCH_CHECK("fill_f32");
   return NSK_OK;
 }
 
 int nsk_fill_bf16(void* p, uint64_t n, float value, void* stream) {
   if (n == 0) return NSK_OK;
-  fill_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((__nv_bfloat16*)p, n, value);
+  nsk::launch_pdl(fill_kernel<__nv_bfloat16>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, (__nv_bfloat16*)p, n, value);
   NSK_LAUNCH_CHECK("fill_bf16");
   return NSK_OK;
 }
@@ -237,9 +246,9 @@ int nsk_cast(int sdt, const void* src, int ddt, void* dst, uint64_t n, void* str
   cudaStream_t st = (cudaStream_t)stream;
   unsigned g = nsk::grid_for(n, 256);
   if (sdt == NSK_DTYPE_F32 && ddt == NSK_DTYPE_BF16)
-    cast_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>((const float*)src, (__nv_bfloat16*)dst, n);
+    nsk::launch_pdl(cast_kernel<float, __nv_bfloat16>, g, 256, 0, st, (const float*)src, (__nv_bfloat16*)dst, n);
   else if (sdt == NSK_DTYPE_BF16 && ddt == NSK_DTYPE_F32)
-    cast_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)src, (float*)dst, n);
+    nsk::launch_pdl(cast_kernel<__nv_bfloat16, float>, g, 256, 0, st, (const __nv_bfloat16*)src, (float*)dst, n);
   else if (sdt == ddt)
     NSK_CUDA(cudaMemcpyAsync(dst, src, n * (sdt == NSK_DTYPE_F32 ? 4 : 2), cudaMemcpyDeviceToDevice, st));
   else
@@ -253,10 +262,10 @@ int nsk_eltwise(int kind, int dtype, const void* a, const void* b, float scalar,
   cudaStream_t st = (cudaStream_t)stream;
   bool vec = aligned16(a) && aligned16(out) && (!b || aligned16(b));
   if (dtype == NSK_DTYPE_F32)
-    ew_kernel<float, false><<<nsk::grid_for(n, 256, 4), 256, 0, st>>>(kind, (const float*)a, (const float*)b, scalar,
+    nsk::launch_pdl(ew_kernel<float, false>, nsk::grid_for(n, 256, 4), 256, 0, st, kind, (const float*)a, (const float*)b, scalar,
                                                                        (float*)out, n, vec);
   else
-    ew_kernel<__nv_bfloat16, false><<<nsk::grid_for(n, 256, 8), 256, 0, st>>>(
+    nsk::launch_pdl(ew_kernel<__nv_bfloat16, false>, nsk::grid_for(n, 256, 8), 256, 0, st, 
         kind, (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, scalar, (__nv_bfloat16*)out, n, vec);
   NSK_LAUNCH_CHECK("eltwise");
   return NSK_OK;
@@ -268,10 +277,10 @@ int nsk_eltwise_bwd(int kind, int dtype, const void* g, const void* saved, float
   cudaStream_t st = (cudaStream_t)stream;
   bool vec = aligned16(g) && aligned16(out) && (!saved || aligned16(saved));
   if (dtype == NSK_DTYPE_F32)
-    ew_kernel<float, true><<<nsk::grid_for(n, 256, 4), 256, 0, st>>>(kind, (const float*)g, (const float*)saved,
+    nsk::launch_pdl(ew_kernel<float, true>, nsk::grid_for(n, 256, 4), 256, 0, st, kind, (const float*)g, (const float*)saved,
                                                                       scalar, (float*)out, n, vec);
   else
-    ew_kernel<__nv_bfloat16, true><<<nsk::grid_for(n, 256, 8), 256, 0, st>>>(
+    nsk::launch_pdl(ew_kernel<__nv_bfloat16, true>, nsk::grid_for(n, 256, 8), 256, 0, st, 
         kind, (const __nv_bfloat16*)g, (const __nv_bfloat16*)saved, scalar, (__nv_bfloat16*)out, n, vec);
   NSK_LAUNCH_CHECK("eltwise_bwd");
   return NSK_OK;
@@ -282,9 +291,9 @@ int nsk_axpy(int dtype, void* y, const void* x, float alpha, uint64_t n, void* s
   cudaStream_t st = (cudaStream_t)stream;
   bool vec = aligned16(y) && aligned16(x);
   if (dtype == NSK_DTYPE_F32)
-    axpy_kernel<float><<<nsk::grid_for(n, 256, 4), 256, 0, st>>>((float*)y, (const float*)x, alpha, n, vec);
+    nsk::launch_pdl(axpy_kernel<float>, nsk::grid_for(n, 256, 4), 256, 0, st, (float*)y, (const float*)x, alpha, n, vec);
   else
-    axpy_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256, 8), 256, 0, st>>>((__nv_bfloat16*)y,
+    nsk::launch_pdl(axpy_kernel<__nv_bfloat16>, nsk::grid_for(n, 256, 8), 256, 0, st, (__nv_bfloat16*)y,
                                                                            (const __nv_bfloat16*)x, alpha, n, vec);
   NSK_LAUNCH_CHECK("axpy");
   return NSK_OK;
@@ -295,9 +304,9 @@ int nsk_bias_add(int dtype, const void* x, const float* b, void* out, uint64_t r
   if (n == 0) return NSK_OK;
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == NSK_DTYPE_F32)
-    bias_add_kernel<float><<<nsk::grid_for(n, 256), 256, 0, st>>>((const float*)x, b, (float*)out, rows, cols);
+    nsk::launch_pdl(bias_add_kernel<float>, nsk::grid_for(n, 256), 256, 0, st, (const float*)x, b, (float*)out, rows, cols);
   else
-    bias_add_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256), 256, 0, st>>>((const __nv_bfloat16*)x, b,
+    nsk::launch_pdl(bias_add_kernel<__nv_bfloat16>, nsk::grid_for(n, 256), 256, 0, st, (const __nv_bfloat16*)x, b,
                                                                             (__nv_bfloat16*)out, rows, cols);
   NSK_LAUNCH_CHECK("bias_add");
   return NSK_OK;
@@ -308,16 +317,16 @@ int nsk_colsum(int dtype, const void* g, float* out, uint64_t rows, uint64_t col
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid((unsigned)((cols + 31) / 32)), block(32, 8);
   if (dtype == NSK_DTYPE_F32)
-    colsum_kernel<float><<<grid, block, 0, st>>>((const float*)g, out, rows, cols, beta);
+    nsk::launch_pdl(colsum_kernel<float>, grid, block, 0, st, (const float*)g, out, rows, cols, beta);
   else
-    colsum_kernel<__nv_bfloat16><<<grid, block, 0, st>>>((const __nv_bfloat16*)g, out, rows, cols, beta);
+    nsk::launch_pdl(colsum_kernel<__nv_bfloat16>, grid, block, 0, st, (const __nv_bfloat16*)g, out, rows, cols, beta);
   NSK_LAUNCH_CHECK("colsum");
   return NSK_OK;
 }
 
 int nsk_check_indices(const float* idx, uint64_t m, int classes, int* err_flag, void* stream) {
   if (m == 0) return NSK_OK;
-  check_idx_kernel<<<nsk::grid_for(m, 256), 256, 0, (cudaStream_t)stream>>>(idx, m, classes, err_flag);
+  nsk::launch_pdl(check_idx_kernel, nsk::grid_for(m, 256), 256, 0, (cudaStream_t)stream, idx, m, classes, err_flag);
   NSK_LAUNCH_CHECK("check_indices");
   return NSK_OK;
 }
@@ -329,7 +338,7 @@ int nsk_onehot(const float* idx, uint64_t m, int classes, float* out, int* err_f
   }
   uint64_t n = m * (uint64_t)classes;
   if (n == 0) return NSK_OK;
-  onehot_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(idx, m, classes, out);
+  nsk::launch_pdl(onehot_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, idx, m, classes, out);
   NSK_LAUNCH_CHECK("onehot");
   return NSK_OK;
 }
@@ -338,9 +347,9 @@ int nsk_transpose_2d(int dtype, const void* src, void* dst, uint64_t rows, uint6
   if (rows == 0 || cols == 0) return NSK_OK;
   dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32)), block(32, 8);
   if (dtype == NSK_DTYPE_F32)
-    transpose_kernel<float><<<grid, block, 0, (cudaStream_t)stream>>>((const float*)src, (float*)dst, rows, cols);
+    nsk::launch_pdl(transpose_kernel<float>, grid, block, 0, (cudaStream_t)stream, (const float*)src, (float*)dst, rows, cols);
   else
-    transpose_kernel<__nv_bfloat16><<<grid, block, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(transpose_kernel<__nv_bfloat16>, grid, block, 0, (cudaStream_t)stream, 
         (const __nv_bfloat16*)src, (__nv_bfloat16*)dst, rows, cols);
   NSK_LAUNCH_CHECK("transpose_2d");
   return NSK_OK;

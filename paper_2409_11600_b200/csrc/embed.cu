@@ -35,6 +35,7 @@ __device__ __forceinline__ float ldv<__nv_bfloat16>(const __nv_bfloat16* p) { re
 template <typename T>
 __global__ void embed_fwd_kernel(const float* __restrict__ table, const float* __restrict__ tok, uint64_t n, int E,
                                  int V, int seq_T, T* __restrict__ out, int* err) {
+  pdl_wait();
   const uint64_t total = n * (uint64_t)E;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = i / E;
@@ -53,6 +54,7 @@ __global__ void embed_fwd_kernel(const float* __restrict__ table, const float* _
 template <typename T>
 __global__ void embed_bwd_kernel(const T* __restrict__ dout, const float* __restrict__ tok, uint64_t n, int E,
                                  int seq_T, float* dtable) {
+  pdl_wait();
   const uint64_t total = n * (uint64_t)E;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t r = i / E;
@@ -72,10 +74,10 @@ int nsk_embedding_fwd(const float* table, const float* tokens, uint64_t n, int E
   if (!total) return NSK_OK;
   if (seq_T > 0 && n % (uint64_t)seq_T) return nsk::set_error(NSK_ERR_SHAPE, "embedding: n is not a multiple of T");
   if (dtype_out == NSK_DTYPE_F32)
-    embed_fwd_kernel<float><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(table, tokens, n, E, V, seq_T,
+    nsk::launch_pdl(embed_fwd_kernel<float>, nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream, table, tokens, n, E, V, seq_T,
                                                                                           (float*)out, err_flag);
   else
-    embed_fwd_kernel<__nv_bfloat16><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(embed_fwd_kernel<__nv_bfloat16>, nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream, 
         table, tokens, n, E, V, seq_T, (__nv_bfloat16*)out, err_flag);
   NSK_LAUNCH_CHECK("embedding_fwd");
   return NSK_OK;
@@ -86,10 +88,10 @@ int nsk_embedding_bwd(const void* dout, int dtype_in, const float* tokens, uint6
   uint64_t total = n * (uint64_t)E;
   if (!total) return NSK_OK;
   if (dtype_in == NSK_DTYPE_F32)
-    embed_bwd_kernel<float><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>((const float*)dout, tokens, n,
+    nsk::launch_pdl(embed_bwd_kernel<float>, nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream, (const float*)dout, tokens, n,
                                                                                           E, seq_T, dtable);
   else
-    embed_bwd_kernel<__nv_bfloat16><<<nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(embed_bwd_kernel<__nv_bfloat16>, nsk::grid_for(total, 256), 256, 0, (cudaStream_t)stream, 
         (const __nv_bfloat16*)dout, tokens, n, E, seq_T, dtable);
   NSK_LAUNCH_CHECK("embedding_bwd");
   return NSK_OK;

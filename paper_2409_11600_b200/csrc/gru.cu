@@ -37,6 +37,7 @@ __device__ __forceinline__ float sigm(float x) {
 __global__ void __launch_bounds__(GT, 1) gru_fwd_kernel(const float* __restrict__ gx, const float* __restrict__ U,
                                                         const float* __restrict__ c, int T, int B, int H, int HU,
                                                         float* hs, float* gates) {
+  pdl_wait();
   extern __shared__ float sm[];
   const int HP = H + PAD;
   float* hsm = sm;                    // [B][HP]
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(GT, 1) gru_bwd_kernel(const float* __restrict_
                                                         const float* __restrict__ hs, const float* __restrict__ gates,
                                                         int T, int B, int H, int HU, float* dgx, float* dgh,
                                                         float* dh0, float* dhcur, float* part) {
+  pdl_wait();
   extern __shared__ float sm[];
   const int H3 = 3 * H;
   const int HP = H + PAD;

@@ -15,6 +15,7 @@ namespace {
 
 __global__ void sgd_kernel(float* const* w, const float* const* g, float* const* v, void* const* wb,
                            const uint64_t* numel, double lr, double mu, float gscale) {
+  pdl_wait();
   const int t = blockIdx.y;
   const uint64_t n = numel[t];
   float* W = w[t];
@@ -33,11 +34,13 @@ __global__ void sgd_kernel(float* const* w, const float* const* g, float* const*
 }
 
 // the optimizer step counter lives on the device so a captured step graph replays with t = 1, 2, 3, ...
-__global__ void step_inc_kernel(int* step) { step[0] += 1; }
+__global__ void step_inc_kernel(int* step) {
+  pdl_wait(); step[0] += 1; }
 
 __global__ void adamw_kernel(float* const* w, const float* const* g, float* const* m, float* const* v, void* const* wb,
                              const uint64_t* numel, double lr, double wd, double b1, double b2, double eps,
                              const int* step_dev, const float* gscale_dev) {
+  pdl_wait();
   __shared__ double bc[2];
   if (threadIdx.x == 0) {
     const double st = (double)step_dev[0];
@@ -71,6 +74,7 @@ __global__ void adamw_kernel(float* const* w, const float* const* g, float* cons
 constexpr int NB = 1024;  // partial slots for the norm reduction
 
 __global__ void sqnorm_partial_kernel(const float* const* g, const uint64_t* numel, int nt, double* part) {
+  pdl_wait();
   __shared__ double red[256 / 32];
   double s = 0.0;
   for (int t = 0; t < nt; ++t) {
@@ -92,6 +96,7 @@ __global__ void sqnorm_partial_kernel(const float* const* g, const uint64_t* num
 }
 
 __global__ void sqnorm_final_kernel(double* part, int nb) {
+  pdl_wait();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < nb; ++i) t += part[1 + i];
@@ -100,11 +105,13 @@ __global__ void sqnorm_final_kernel(double* part, int nb) {
 }
 
 __global__ void clip_scale_kernel(const double* sq, float max_norm, float* scale) {
+  pdl_wait();
   double norm = sqrt(sq[0]);
   scale[0] = norm <= (double)max_norm ? 1.f : (float)((double)max_norm / norm);
 }
 
 __global__ void scale_kernel(float* const* g, const uint64_t* numel, const float* scale) {
+  pdl_wait();
   const float s = scale[0];
   if (s == 1.f) return;
   const int t = blockIdx.y;
@@ -130,7 +137,7 @@ int nsk_sgd_multi(int nt, float* const* w, const float* const* g, float* const* 
                   const uint64_t* numel, double lr, double momentum, float grad_scale, void* stream) {
   if (nt < 1) return NSK_OK;
   dim3 grid(blocks_x(nt), nt);
-  sgd_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, v, wb, numel, lr, momentum, grad_scale);
+  nsk::launch_pdl(sgd_kernel, grid, 256, 0, (cudaStream_t)stream, w, g, v, wb, numel, lr, momentum, grad_scale);
   NSK_LAUNCH_CHECK("sgd_multi");
   return NSK_OK;
 }
@@ -139,9 +146,9 @@ int nsk_adamw_multi(int nt, float* const* w, const float* const* g, float* const
                     void* const* wb, const uint64_t* numel, int* step_dev, double lr, double wd, double beta1,
                     double beta2, double eps, const float* grad_scale_dev, void* stream) {
   if (nt < 1) return NSK_OK;
-  step_inc_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_dev);
+  nsk::launch_pdl(step_inc_kernel, 1, 1, 0, (cudaStream_t)stream, step_dev);
   dim3 grid(blocks_x(nt), nt);
-  adamw_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(w, g, m, v, wb, numel, lr, wd, beta1, beta2, eps, step_dev,
+  nsk::launch_pdl(adamw_kernel, grid, 256, 0, (cudaStream_t)stream, w, g, m, v, wb, numel, lr, wd, beta1, beta2, eps, step_dev,
                                                        grad_scale_dev);
   NSK_LAUNCH_CHECK("adamw_multi");
   return NSK_OK;
@@ -151,14 +158,14 @@ int nsk_adamw_multi(int nt, float* const* w, const float* const* g, float* const
 int nsk_sqnorm_multi(int nt, const float* const* g, const uint64_t* numel, double* out, void* stream) {
   int nb = 2 * nsk::sm_count();
   if (nb > NB) nb = NB;
-  sqnorm_partial_kernel<<<nb, 256, 0, (cudaStream_t)stream>>>(g, numel, nt, out);
-  sqnorm_final_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(out, nb);
+  nsk::launch_pdl(sqnorm_partial_kernel, nb, 256, 0, (cudaStream_t)stream, g, numel, nt, out);
+  nsk::launch_pdl(sqnorm_final_kernel, 1, 32, 0, (cudaStream_t)stream, out, nb);
   NSK_LAUNCH_CHECK("sqnorm_multi");
   return NSK_OK;
 }
 
 int nsk_clip_scale(const double* sqnorm, float max_norm, float* scale_dev, void* stream) {
-  clip_scale_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(sqnorm, max_norm, scale_dev);
+  nsk::launch_pdl(clip_scale_kernel, 1, 1, 0, (cudaStream_t)stream, sqnorm, max_norm, scale_dev);
   NSK_LAUNCH_CHECK("clip_scale");
   return NSK_OK;
 }
@@ -166,7 +173,7 @@ int nsk_clip_scale(const double* sqnorm, float max_norm, float* scale_dev, void*
 int nsk_scale_multi(int nt, float* const* g, const uint64_t* numel, const float* scale_dev, void* stream) {
   if (nt < 1) return NSK_OK;
   dim3 grid(blocks_x(nt), nt);
-  scale_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(g, numel, scale_dev);
+  nsk::launch_pdl(scale_kernel, grid, 256, 0, (cudaStream_t)stream, g, numel, scale_dev);
   NSK_LAUNCH_CHECK("scale_multi");
   return NSK_OK;
 }

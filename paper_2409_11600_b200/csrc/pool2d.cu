@@ -25,6 +25,7 @@ __device__ __forceinline__ void stv<__nv_bfloat16>(__nv_bfloat16* p, float v) { 
 // global average pool: x [N, HW, C] -> y [N, C] (fp32), float64 accumulate
 template <typename T>
 __global__ void avgpool_fwd_kernel(const T* __restrict__ x, float* __restrict__ y, int N, int HW, int C) {
+  pdl_wait();
   const long long n_out = (long long)N * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_out; i += (long long)gridDim.x * blockDim.x) {
     long long n = i / C;
@@ -38,6 +39,7 @@ __global__ void avgpool_fwd_kernel(const T* __restrict__ x, float* __restrict__ 
 
 template <typename T>
 __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, T* __restrict__ dx, int N, int HW, int C) {
+  pdl_wait();
   const long long n = (long long)N * HW * C;
   const float inv = 1.f / (float)HW;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -50,6 +52,7 @@ __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, T* __restrict__
 // max pool (NHWC bf16): window k x k, stride, pad (padding = -inf); first maximum wins (numpy argmax convention)
 __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, int N, int H,
                                    int W, int C, int k, int st, int pad, int P, int Q) {
+  pdl_wait();
   const long long n_out = (long long)N * P * Q * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_out; i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % C);
@@ -77,6 +80,7 @@ __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfl
 __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
                                    __nv_bfloat16* __restrict__ dx, int N, int H, int W, int C, int k, int st, int pad,
                                    int P, int Q) {
+  pdl_wait();
   const long long n_in = (long long)N * H * W * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_in; i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % C);
@@ -119,6 +123,7 @@ __global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __
 
 __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int N, int C, int H,
                                     int W, int Cp) {
+  pdl_wait();
   const long long n = (long long)N * H * W * Cp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % Cp);
@@ -134,6 +139,7 @@ __global__ void nchw_to_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* 
 
 template <typename T>
 __global__ void nhwc_to_nchw_kernel(const T* __restrict__ x, float* __restrict__ y, int N, int C, int H, int W, int Cp) {
+  pdl_wait();
   const long long n = (long long)N * C * H * W;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     int w = (int)(i % W);
@@ -149,6 +155,7 @@ __global__ void nhwc_to_nchw_kernel(const T* __restrict__ x, float* __restrict__
 // im2col for small-channel stems: out[(n,p,q), k], k = (r*S + s)*C + c, zero for k >= R*S*C or padding
 __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ out, int N, int H,
                               int W, int C, int R, int S, int st, int pad, int P, int Q, int Kp) {
+  pdl_wait();
   const long long n = (long long)N * P * Q * Kp;
   const int RSC = R * S * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -176,6 +183,7 @@ __global__ void im2col_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
 // (c, r, s) decode comes from a shared-memory table so the loop body is loads and converts only.
 __global__ void im2col_nchw_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int N, int C, int H,
                                    int W, int R, int S, int st, int pad, int P, int Q, int Kp) {
+  pdl_wait();
   extern __shared__ int tab[];  // [Kp]: (c << 16) | (r << 8) | s, or -1 for padding columns
   const int RSC = R * S * C;
   for (int kk = threadIdx.x; kk < Kp; kk += blockDim.x) {
@@ -223,6 +231,7 @@ __global__ void im2col_nchw_kernel(const float* __restrict__ x, __nv_bfloat16* _
 // col2im (gather form, deterministic): dx[n,h,w,c] = sum_{r,s: h = p*st-pad+r, w = q*st-pad+s} dcols[(n,p,q), k]
 __global__ void col2im_kernel(const float* __restrict__ dcols, __nv_bfloat16* __restrict__ dx, int N, int H,
                               int W, int C, int R, int S, int st, int pad, int P, int Q, int Kp) {
+  pdl_wait();
   const long long n = (long long)N * H * W * C;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % C);
@@ -253,6 +262,7 @@ __global__ void col2im_kernel(const float* __restrict__ dcols, __nv_bfloat16* __
 __global__ void augment_kernel(const uint8_t* __restrict__ img, const int32_t* __restrict__ offs,
                                __nv_bfloat16* __restrict__ out, int N, int H, int W, int C, int pad,
                                const float* __restrict__ mean, const float* __restrict__ stdv, int Cp) {
+  pdl_wait();
   const long long n = (long long)N * H * W * Cp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     int c = (int)(i % Cp);
@@ -281,9 +291,9 @@ extern "C" {
 int nsk_avgpool_fwd(int dtype_in, const void* x, float* y, int N, int HW, int C, void* stream) {
   long long n = (long long)N * C;
   if (dtype_in == NSK_DTYPE_F32)
-    avgpool_fwd_kernel<float><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((const float*)x, y, N, HW, C);
+    nsk::launch_pdl(avgpool_fwd_kernel<float>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, (const float*)x, y, N, HW, C);
   else
-    avgpool_fwd_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(avgpool_fwd_kernel<__nv_bfloat16>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
         (const __nv_bfloat16*)x, y, N, HW, C);
   NSK_LAUNCH_CHECK("avgpool_fwd");
   return NSK_OK;
@@ -292,9 +302,9 @@ int nsk_avgpool_fwd(int dtype_in, const void* x, float* y, int N, int HW, int C,
 int nsk_avgpool_bwd(const float* dy, int dtype_out, void* dx, int N, int HW, int C, void* stream) {
   long long n = (long long)N * HW * C;
   if (dtype_out == NSK_DTYPE_F32)
-    avgpool_bwd_kernel<float><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(dy, (float*)dx, N, HW, C);
+    nsk::launch_pdl(avgpool_bwd_kernel<float>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, dy, (float*)dx, N, HW, C);
   else
-    avgpool_bwd_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(avgpool_bwd_kernel<__nv_bfloat16>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
         dy, (__nv_bfloat16*)dx, N, HW, C);
   NSK_LAUNCH_CHECK("avgpool_bwd");
   return NSK_OK;
@@ -303,7 +313,7 @@ int nsk_avgpool_bwd(const float* dy, int dtype_out, void* dx, int N, int HW, int
 int nsk_maxpool_fwd(const void* x, void* y, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
                     void* stream) {
   long long n = (long long)N * P * Q * C;
-  maxpool_fwd_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+  nsk::launch_pdl(maxpool_fwd_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)x, (__nv_bfloat16*)y, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_fwd");
   return NSK_OK;
@@ -312,7 +322,7 @@ int nsk_maxpool_fwd(const void* x, void* y, int N, int H, int W, int C, int k, i
 int nsk_maxpool_bwd(const void* x, const void* dy, void* dx, int N, int H, int W, int C, int k, int stride, int pad,
                     int P, int Q, void* stream) {
   long long n = (long long)N * H * W * C;
-  maxpool_bwd_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+  nsk::launch_pdl(maxpool_bwd_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_bwd");
   return NSK_OK;
@@ -320,7 +330,7 @@ int nsk_maxpool_bwd(const void* x, const void* dy, void* dx, int N, int H, int W
 
 int nsk_nchw_to_nhwc(const float* x, void* y, int N, int C, int H, int W, int Cp, void* stream) {
   long long n = (long long)N * H * W * Cp;
-  nchw_to_nhwc_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)y, N, C, H, W, Cp);
+  nsk::launch_pdl(nchw_to_nhwc_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, x, (__nv_bfloat16*)y, N, C, H, W, Cp);
   NSK_LAUNCH_CHECK("nchw_to_nhwc");
   return NSK_OK;
 }
@@ -328,10 +338,10 @@ int nsk_nchw_to_nhwc(const float* x, void* y, int N, int C, int H, int W, int Cp
 int nsk_nhwc_to_nchw(int dtype_in, const void* x, float* y, int N, int C, int H, int W, int Cp, void* stream) {
   long long n = (long long)N * C * H * W;
   if (dtype_in == NSK_DTYPE_F32)
-    nhwc_to_nchw_kernel<float><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>((const float*)x, y, N, C, H, W,
+    nsk::launch_pdl(nhwc_to_nchw_kernel<float>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, (const float*)x, y, N, C, H, W,
                                                                                          Cp);
   else
-    nhwc_to_nchw_kernel<__nv_bfloat16><<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+    nsk::launch_pdl(nhwc_to_nchw_kernel<__nv_bfloat16>, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
         (const __nv_bfloat16*)x, y, N, C, H, W, Cp);
   NSK_LAUNCH_CHECK("nhwc_to_nchw");
   return NSK_OK;
@@ -340,7 +350,7 @@ int nsk_nhwc_to_nchw(int dtype_in, const void* x, float* y, int N, int C, int H,
 int nsk_im2col(const void* x, void* out, int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q,
                int Kp, void* stream) {
   long long n = (long long)N * P * Q * Kp;
-  im2col_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+  nsk::launch_pdl(im2col_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
       (const __nv_bfloat16*)x, (__nv_bfloat16*)out, N, H, W, C, R, S, stride, pad, P, Q, Kp);
   NSK_LAUNCH_CHECK("im2col");
   return NSK_OK;
@@ -353,7 +363,7 @@ int nsk_im2col_nchw(const float* x, void* out, int N, int C, int H, int W, int R
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "im2col_nchw: filter too large");
   const size_t smem = (size_t)Kp * sizeof(int);
   const long long n = (long long)N * P * Q * (Kp / 8);
-  im2col_nchw_kernel<<<nsk::grid_for(n, 256), 256, smem, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)out, N, C, H, W, R, S, stride, pad,
+  nsk::launch_pdl(im2col_nchw_kernel, nsk::grid_for(n, 256), 256, smem, (cudaStream_t)stream, x, (__nv_bfloat16*)out, N, C, H, W, R, S, stride, pad,
                                                                 P, Q, Kp);
   NSK_LAUNCH_CHECK("im2col_nchw");
   return NSK_OK;
@@ -362,7 +372,7 @@ int nsk_im2col_nchw(const float* x, void* out, int N, int C, int H, int W, int R
 int nsk_col2im(const void* dcols, void* dx, int N, int H, int W, int C, int R, int S, int stride, int pad, int P, int Q,
                int Kp, void* stream) {
   long long n = (long long)N * H * W * C;
-  col2im_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+  nsk::launch_pdl(col2im_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
       (const float*)dcols, (__nv_bfloat16*)dx, N, H, W, C, R, S, stride, pad, P, Q, Kp);
   NSK_LAUNCH_CHECK("col2im");
   return NSK_OK;
@@ -371,7 +381,7 @@ int nsk_col2im(const void* dcols, void* dx, int N, int H, int W, int C, int R, i
 int nsk_augment_crop_flip(const uint8_t* img, const int32_t* offs, void* out, int N, int H, int W, int C, int pad,
                           const float* mean, const float* stdv, int Cp, void* stream) {
   long long n = (long long)N * H * W * Cp;
-  augment_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(img, offs, (__nv_bfloat16*)out, N, H, W, C,
+  nsk::launch_pdl(augment_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, img, offs, (__nv_bfloat16*)out, N, H, W, C,
                                                                           pad, mean, stdv, Cp);
   NSK_LAUNCH_CHECK("augment_crop_flip");
   return NSK_OK;

@@ -15,6 +15,7 @@ constexpr int TS = 16;
 __global__ void simt_gemm_kernel(int a_mn, int b_mn, int M, int N, int K, const float* __restrict__ A, long long lda,
                                  const float* __restrict__ B, long long ldb, float* C, long long ldc,
                                  const float* __restrict__ bias, float beta) {
+  pdl_wait();
   __shared__ float As[TS][TS + 1];
   __shared__ float Bs[TS][TS + 1];
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -46,6 +47,7 @@ __global__ void simt_gemm_kernel(int a_mn, int b_mn, int M, int N, int K, const 
 __global__ void simt_dot_kernel(int a_mn, int b_mn, int M, int N, int K, const float* __restrict__ A, long long lda,
                                 const float* __restrict__ B, long long ldb, float* C, long long ldc,
                                 const float* __restrict__ bias, float beta) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
   for (long long o = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); o < (long long)M * N;
@@ -71,6 +73,7 @@ __global__ void simt_dot_kernel(int a_mn, int b_mn, int M, int N, int K, const f
 __global__ void simt_short_k_kernel(int a_mn, int b_mn, int M, int N, int K, const float* __restrict__ A,
                                     long long lda, const float* __restrict__ B, long long ldb, float* C,
                                     long long ldc, const float* __restrict__ bias, float beta) {
+  pdl_wait();
   for (long long o = blockIdx.x * (long long)blockDim.x + threadIdx.x; o < (long long)M * N;
        o += (long long)gridDim.x * blockDim.x) {
     const int m = (int)(o / N), n = (int)(o - (long long)m * N);
@@ -94,19 +97,19 @@ extern "C" int nsk_gemm_simt(int a_mn, int b_mn, int M, int N, int K, const floa
   if (M < 1 || N < 1 || K < 1) return nsk::set_error(NSK_ERR_SHAPE, "gemm: empty problem");
   const long long outs = (long long)M * N;
   if (K <= 32) {
-    simt_short_k_kernel<<<nsk::grid_for(outs, 256), 256, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B,
+    nsk::launch_pdl(simt_short_k_kernel, nsk::grid_for(outs, 256), 256, 0, (cudaStream_t)stream, a_mn, b_mn, M, N, K, A, lda, B,
                                                                                    ldb, C, ldc, bias, beta);
     NSK_LAUNCH_CHECK("simt_short_k");
     return NSK_OK;
   }
   if (outs <= 65536) {
-    simt_dot_kernel<<<nsk::grid_for(outs * 32, 256), 256, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B,
+    nsk::launch_pdl(simt_dot_kernel, nsk::grid_for(outs * 32, 256), 256, 0, (cudaStream_t)stream, a_mn, b_mn, M, N, K, A, lda, B,
                                                                                     ldb, C, ldc, bias, beta);
     NSK_LAUNCH_CHECK("simt_dot");
     return NSK_OK;
   }
   dim3 grid((N + TS - 1) / TS, (M + TS - 1) / TS), block(TS, TS);
-  simt_gemm_kernel<<<grid, block, 0, (cudaStream_t)stream>>>(a_mn, b_mn, M, N, K, A, lda, B, ldb, C, ldc, bias, beta);
+  nsk::launch_pdl(simt_gemm_kernel, grid, block, 0, (cudaStream_t)stream, a_mn, b_mn, M, N, K, A, lda, B, ldb, C, ldc, bias, beta);
   NSK_LAUNCH_CHECK("simt_gemm");
   return NSK_OK;
 }

@@ -146,6 +146,7 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 template <int BN, int ESZ, int STAGES, bool RR>
 __global__ void __launch_bounds__(256, 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UmmaProb p) {
+  pdl_wait();
   using S = Smem<BN, ESZ, STAGES, RR>;
   using T = KT<ESZ>;
   extern __shared__ uint8_t smem_raw[];
@@ -505,6 +506,7 @@ __global__ void __launch_bounds__(256, 1)
 // Both sides are contiguous in the (tap, cin) index: fully coalesced, fixed summation order.
 __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M, int N, float* dw,
                                     float beta) {
+  pdl_wait();
   // 4 consecutive (tap, cin) entries per thread (M % 4 == 0 since Cin % 64 == 0), splits folded in order
   const long long total4 = (long long)M * N / 4;
   const long long plane = (long long)N * Mpad;
@@ -542,6 +544,7 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, in
 // split-K GEMM fold: C[m, n] = sum_z ws[z][m][n] (+ bias[n]) (+ beta * C[m, n]), fp32 or bf16 out
 __global__ void splitk_fold_kernel(const float* __restrict__ ws, int splits, int M, int N, void* C, long long ldc,
                                    int c_f32, const float* __restrict__ bias, float beta) {
+  pdl_wait();
   const long long total = (long long)M * N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -602,7 +605,7 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStre
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  kern<<<grid, 256, smem, st>>>(a, b, p);
+  nsk::launch_pdl(kern, grid, 256, smem, st, a, b, p);
   NSK_LAUNCH_CHECK("umma_kernel");
   return NSK_OK;
 }
@@ -819,7 +822,7 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
     rc = esz == 2 ? dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, st) : dispatch_bn<4>(BN, ma, mb, p, mt, nt, splits, st);
     if (rc) return rc;
     const long long total = (long long)M * N;
-    splitk_fold_kernel<<<nsk::grid_for(total, 256), 256, 0, st>>>(ws, splits, M, N, C, ldc, c_f32, bias, beta);
+    nsk::launch_pdl(splitk_fold_kernel, nsk::grid_for(total, 256), 256, 0, st, ws, splits, M, N, C, ldc, c_f32, bias, beta);
     NSK_LAUNCH_CHECK("splitk_fold_kernel");
     return NSK_OK;
   }
@@ -1050,7 +1053,7 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   long long total = (long long)M * d->K;
   if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: dw and workspace must be 16-byte aligned");
-  wgrad_reduce_kernel<<<nsk::grid_for(total / 4, 256), 256, 0, (cudaStream_t)stream>>>((const float*)ws, splits, Mpad,
+  nsk::launch_pdl(wgrad_reduce_kernel, nsk::grid_for(total / 4, 256), 256, 0, (cudaStream_t)stream, (const float*)ws, splits, Mpad,
                                                                                        M, d->K, dw, beta);
   NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
   return NSK_OK;

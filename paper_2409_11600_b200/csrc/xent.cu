@@ -27,6 +27,7 @@ struct XentScratch {
 __global__ void __launch_bounds__(XW * 32) xent_fwd_kernel(const float* __restrict__ z, const float* __restrict__ tgt,
                                                            int m, int c, float* __restrict__ probs, float* loss,
                                                            int* err, double* part, unsigned* ticket) {
+  pdl_wait();
   __shared__ double wpart[XW];
   __shared__ bool last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(XW * 32) xent_fwd_kernel(const float* __restri
 
 __global__ void xent_bwd_kernel(const float* __restrict__ probs, const float* __restrict__ tgt, const float* g, int m,
                                 int c, float* __restrict__ d) {
+  pdl_wait();
   const double scale = (double)g[0] / (double)m;
   const long long n = (long long)m * c;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -94,6 +96,7 @@ __device__ __forceinline__ float ldf<__nv_bfloat16>(const __nv_bfloat16* p) { re
 
 template <typename T>
 __global__ void __launch_bounds__(XT) sum_kernel(const T* __restrict__ x, uint64_t n, float* out) {
+  pdl_wait();
   __shared__ double part[XT / 32];
   double s = 0.0;
   for (uint64_t i = threadIdx.x; i < n; i += XT) s += (double)ldf<T>(x + i);
@@ -108,12 +111,14 @@ __global__ void __launch_bounds__(XT) sum_kernel(const T* __restrict__ x, uint64
 }
 
 __global__ void fill_scalar_kernel(const float* g, float* out, uint64_t n) {
+  pdl_wait();
   const float v = g[0];
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
     out[i] = v;
 }
 
 __global__ void argmax_kernel(const float* __restrict__ z, const float* __restrict__ labels, int m, int c, int* count) {
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
   int local = 0;
@@ -173,7 +178,7 @@ int nsk_xent_fwd(const float* logits, const float* targets, int m, int c, float*
     NSK_CUDA(cudaMemset(sc.ticket, 0, sizeof(unsigned)));
     sc.cap = cap;
   }
-  xent_fwd_kernel<<<blocks, XW * 32, 0, (cudaStream_t)stream>>>(logits, targets, m, c, probs, loss_out, err_flag,
+  nsk::launch_pdl(xent_fwd_kernel, blocks, XW * 32, 0, (cudaStream_t)stream, logits, targets, m, c, probs, loss_out, err_flag,
                                                                 sc.part, sc.ticket);
   NSK_LAUNCH_CHECK("xent_fwd");
   return NSK_OK;
@@ -182,22 +187,22 @@ int nsk_xent_fwd(const float* logits, const float* targets, int m, int c, float*
 int nsk_xent_bwd(const float* probs, const float* targets, const float* g, int m, int c, float* dlogits,
                  void* stream) {
   long long n = (long long)m * c;
-  xent_bwd_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(probs, targets, g, m, c, dlogits);
+  nsk::launch_pdl(xent_bwd_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, probs, targets, g, m, c, dlogits);
   NSK_LAUNCH_CHECK("xent_bwd");
   return NSK_OK;
 }
 
 int nsk_sum_f32(int dtype, const void* x, uint64_t n, float* out, void* stream) {
   if (dtype == NSK_DTYPE_F32)
-    sum_kernel<float><<<1, XT, 0, (cudaStream_t)stream>>>((const float*)x, n, out);
+    nsk::launch_pdl(sum_kernel<float>, 1, XT, 0, (cudaStream_t)stream, (const float*)x, n, out);
   else
-    sum_kernel<__nv_bfloat16><<<1, XT, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, n, out);
+    nsk::launch_pdl(sum_kernel<__nv_bfloat16>, 1, XT, 0, (cudaStream_t)stream, (const __nv_bfloat16*)x, n, out);
   NSK_LAUNCH_CHECK("sum");
   return NSK_OK;
 }
 
 int nsk_fill_like_scalar(const float* g, float* out, uint64_t n, void* stream) {
-  fill_scalar_kernel<<<nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(g, out, n);
+  nsk::launch_pdl(fill_scalar_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, g, out, n);
   NSK_LAUNCH_CHECK("fill_like_scalar");
   return NSK_OK;
 }
@@ -208,7 +213,7 @@ int nsk_argmax_correct(const float* logits, const float* labels, int m, int c, i
   int blocks = (m + 7) / 8;
   if (blocks > 4 * nsk::sm_count()) blocks = 4 * nsk::sm_count();
   if (blocks < 1) blocks = 1;
-  argmax_kernel<<<blocks, 256, 0, st>>>(logits, labels, m, c, count_out);
+  nsk::launch_pdl(argmax_kernel, blocks, 256, 0, st, logits, labels, m, c, count_out);
   NSK_LAUNCH_CHECK("argmax_correct");
   return NSK_OK;
 }
