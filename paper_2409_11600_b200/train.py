@@ -20,7 +20,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib, autodiff, nn
-from ._lib import F32, check
+from ._lib import BF16, F32, check
 from .autodiff import backward, data_from_device
 from .errors import NskRuntimeError
 from .tensor import SCALARS, Buffer, DeviceScalar, Tensor, check_index_values
@@ -88,10 +88,13 @@ class Trainer:
     """Classification training loop over a tape-recorded model.
 
     ``optimizer`` is ``("sgd", lr, momentum)`` or ``("adamw", Hyperparams, clip_norm|None)``.
+    ``augment=(pad, mean, std)``: the inputs are uint8 NHWC images [B, H, W, C]; each step crops (zero pad
+    ``pad``), flips and normalises them on the GPU (K18) with host-drawn (dy, dx, flip) per image, and the
+    model runs on the NHWC bf16 result (``model.forward(x_nhwc=...)``).
     """
 
     def __init__(self, session, model, x_shape, classes: int, optimizer=("sgd", 0.1, 0.9), graph: bool = True,
-                 warmup: int = 2, dp=None):
+                 warmup: int = 2, dp=None, augment=None, augment_seed: int = 0):
         self.s = session
         self.model = model
         self.classes = classes
@@ -101,11 +104,25 @@ class Trainer:
         self.dp = dp
         self.x_shape = tuple(x_shape)
         b = self.x_shape[0]
-        self.x_pin = PinnedArray(self.x_shape)
+        self.augment = augment
         self.y_pin = PinnedArray((b,))
-        pool = session.pool
-        self.x_dev = Tensor(self.x_shape, Buffer(int(np.prod(self.x_shape)), F32))
         self.y_dev = Tensor((b,), Buffer(b, F32))
+        if augment is None:
+            self.x_pin = PinnedArray(self.x_shape)
+            self.x_dev = Tensor(self.x_shape, Buffer(int(np.prod(self.x_shape)), F32))
+        else:
+            # raw uint8 images (held in a 4-byte-word buffer), per-image crop offsets / flip bits (int32)
+            nbytes = int(np.prod(self.x_shape))
+            self.x_pin = PinnedArray(self.x_shape, np.uint8)
+            self.x_dev = Tensor(((nbytes + 3) // 4,), Buffer((nbytes + 3) // 4, F32))
+            self.offs_pin = PinnedArray((b, 3), np.int32)
+            self.offs_dev = Tensor((b * 3,), Buffer(b * 3, F32))
+            pad, mean, std = augment
+            c = self.x_shape[3]
+            self.aug_stats = Tensor((2, c), Buffer(2 * c, F32))
+            self.aug_stats.buffer.upload(np.stack([np.broadcast_to(np.asarray(mean, np.float32), (c,)),
+                                                   np.broadcast_to(np.asarray(std, np.float32), (c,))]))
+            self.aug_rng = np.random.default_rng(augment_seed)
         for t in (self.x_dev, self.y_dev):
             t.refs = 1  # external hold: the traversal never returns these to the pool
         self.y_dev.host_src = self.y_pin.array
@@ -124,9 +141,18 @@ class Trainer:
         s = self.s
         if self.dp is not None:
             self.dp.begin_step()
-        x = data_from_device(self.x_dev)
         y = data_from_device(self.y_dev)
-        logits = self.model.forward(x)
+        if self.augment is None:
+            logits = self.model.forward(data_from_device(self.x_dev))
+        else:
+            from .tensor import empty_tensor
+
+            b, h, w, c = self.x_shape
+            xa = empty_tensor(s.pool, (b, h, w, c), BF16)
+            check(_lib.lib().nsk_augment_crop_flip(self.x_dev.ptr, self.offs_dev.ptr, xa.ptr, b, h, w, c,
+                                                   int(self.augment[0]), self.aug_stats.ptr,
+                                                   self.aug_stats.ptr + 4 * c, c, _lib.stream()))
+            logits = self.model.forward(x_nhwc=data_from_device(xa))
         loss = nn.cross_entropy(logits, y, s.pool)
         s.push_named("train.loss", loss)
         backward(s.tape(), s.grad_cache, s.pool)
@@ -149,8 +175,9 @@ class Trainer:
             raise NskRuntimeError("loss was not reclaimed by backward()")
         return loss._scalar
 
-    def stage(self, x_host, y_host) -> None:
-        """Host batch -> pinned -> device (async on the compute stream)."""
+    def stage(self, x_host, y_host, offsets=None) -> None:
+        """Host batch -> pinned -> device (async on the compute stream). With ``augment``, ``offsets`` [B, 3]
+        (dy, dx, flip) default to a draw from the trainer's Generator (oracle/restated.draw_crop_flip order)."""
         y = np.asarray(y_host, dtype=np.float32).reshape(-1)
         check_index_values(y, self.classes, "target")
         if self.input_classes is not None:
@@ -162,9 +189,16 @@ class Trainer:
             self._copied = ev.value
         else:
             check(lib.nsk_event_sync(self._copied))  # previous H2D finished reading the pinned buffers
-        np.copyto(self.x_pin.array, np.asarray(x_host, dtype=np.float32).reshape(self.x_shape))
+        np.copyto(self.x_pin.array, np.asarray(x_host, dtype=self.x_pin.dtype).reshape(self.x_shape))
         np.copyto(self.y_pin.array, y)
         check(lib.nsk_memcpy_h2d(self.x_dev.ptr, self.x_pin.ptr, self.x_pin.nbytes, st))
+        if self.augment is not None:
+            from .data import _draw_crop_flip
+
+            offs = _draw_crop_flip(self.aug_rng, self.x_shape[0], int(self.augment[0])) if offsets is None \
+                else np.asarray(offsets, np.int32)
+            np.copyto(self.offs_pin.array, offs.reshape(-1, 3))
+            check(lib.nsk_memcpy_h2d(self.offs_dev.ptr, self.offs_pin.ptr, self.offs_pin.nbytes, st))
         check(lib.nsk_memcpy_h2d(self.y_dev.ptr, self.y_pin.ptr, self.y_pin.nbytes, st))
         check(lib.nsk_event_record(self._copied, st))
 
@@ -187,9 +221,9 @@ class Trainer:
         self.steps_done += 1
         return sc
 
-    def step(self, x_host, y_host) -> DeviceScalar:
+    def step(self, x_host, y_host, offsets=None) -> DeviceScalar:
         """The public call: copy the host batch in, run one training step, return the loss (on device)."""
-        self.stage(x_host, y_host)
+        self.stage(x_host, y_host, offsets)
         # the pinned staging buffers may be overwritten by the next stage() only after this step's copies ran
         return self.run_staged()
 
