@@ -21,10 +21,11 @@ struct Job {
   int d1, d2, d3;  // tile grid extents (mode-specific)
   int halo;        // 4D: coordinate offset (-1 = OOB halo rows/cols)
   int boxes_per_stage;
+  int lane_issuers;
 };
 
 template <int STAGES>
-__global__ void __launch_bounds__(128, 1) tma_loop(const __grid_constant__ CUtensorMap map, Job j, int iters,
+__global__ void __launch_bounds__(256, 1) tma_loop(const __grid_constant__ CUtensorMap map, Job j, int iters,
                                                   long long* cyc) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
@@ -34,9 +35,15 @@ __global__ void __launch_bounds__(128, 1) tma_loop(const __grid_constant__ CUten
     fence_mbar_init();
   }
   __syncthreads();
-  const int issuers = blockDim.x / 32;
-  if (threadIdx.x % 32 != 0) return;
-  const int me = threadIdx.x / 32;
+  const int issuers = j.lane_issuers ? j.lane_issuers : blockDim.x / 32;
+  int me;
+  if (j.lane_issuers) {
+    if (threadIdx.x >= j.lane_issuers) return;
+    me = threadIdx.x;
+  } else {
+    if (threadIdx.x % 32 != 0) return;
+    me = threadIdx.x / 32;
+  }
   long long t0 = clock64();
   const int bps = j.boxes_per_stage;
   for (int i = 0; i < iters; ++i) {
@@ -87,10 +94,16 @@ int main() {
   struct Case {
     const char* name;
     int mode, C, H, W, N, rows_k, bw, bh, bn, halo, bps;
-    int rows = 128, ctas = 1, stages = 8, issuers = 1;
+    int rows = 128, ctas = 1, stages = 8, issuers = 1, lanes = 0;
   };
   // NHWC bf16 tensors; 2D cases view [N*H*W, C] with 64-element (128 B) boxes of 128 rows
   std::vector<Case> cases = {
+      {"2D  box 64x128 x8 stages, 4 issuer lanes/1 warp", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 1, 4},
+      {"2D  box 64x128 x8 stages, 8 issuer lanes/1 warp", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 1, 8},
+      {"2D  box 64x256 x4 stages, 4 issuer warps", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 256, 1, 4, 4},
+      {"2D  box 64x128 x8 stages, 8 issuer warps", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 8},
+      {"4D  box 64x32x4x1 x8, 8 issuer warps", 1, 64, 32, 32, 256, 0, 32, 4, 1, 0, 1, 128, 1, 8, 8},
+      {"I2C 32x32x64 x8, 8 issuer warps", 2, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 8},
       {"2D  box 64x128 x8 stages, 2 issuer warps", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 2},
       {"2D  box 64x128 x8 stages, 4 issuer warps", 0, 64, 32, 32, 256, 0, 0, 0, 0, 0, 1, 128, 1, 8, 4},
       {"4D  box 64x32x8x1 (32KB) x4", 1, 64, 32, 32, 256, 0, 32, 8, 1, 0, 1, 256, 1, 4},
@@ -121,6 +134,7 @@ int main() {
     j.mode = c.mode;
     j.halo = c.halo;
     j.boxes_per_stage = c.bps;
+    j.lane_issuers = c.lanes;
     CUresult r;
     const long long npix = (long long)c.N * c.H * c.W;
     if (c.mode == 0) {
