@@ -84,6 +84,39 @@ def capture(fn):
     return StepGraph(ex.value, int(n.value)), result
 
 
+class _InputSlot:
+    """One set of batch buffers: pinned host staging, device inputs, copy/consume events, its captured graph."""
+
+    def __init__(self, x_shape, augment):
+        b = x_shape[0]
+        self.y_pin = PinnedArray((b,))
+        self.y_dev = Tensor((b,), Buffer(b, F32))
+        self.offs_pin = self.offs_dev = None
+        if augment is None:
+            self.x_pin = PinnedArray(x_shape)
+            self.x_dev = Tensor(x_shape, Buffer(int(np.prod(x_shape)), F32))
+        else:
+            # raw uint8 images (held in a 4-byte-word buffer), per-image crop offsets / flip bits (int32)
+            nbytes = int(np.prod(x_shape))
+            self.x_pin = PinnedArray(x_shape, np.uint8)
+            self.x_dev = Tensor(((nbytes + 3) // 4,), Buffer((nbytes + 3) // 4, F32))
+            self.offs_pin = PinnedArray((b, 3), np.int32)
+            self.offs_dev = Tensor((b * 3,), Buffer(b * 3, F32))
+        for t in (self.x_dev, self.y_dev):
+            t.refs = 1  # external hold: the traversal never returns these to the pool
+        self.y_dev.host_src = self.y_pin.array
+        lib = _lib.lib()
+        evs = []
+        for _ in range(2):
+            ev = C.c_void_p()
+            check(lib.nsk_event_create(0, C.byref(ev)))
+            evs.append(ev.value)
+        self.copied, self.consumed = evs  # H2D from the pinned buffers done / last step reading x_dev done
+        self.copy_pending = False
+        self.graph: StepGraph | None = None
+        self.loss_slot: int | None = None
+
+
 class Trainer:
     """Classification training loop over a tape-recorded model.
 
@@ -105,36 +138,33 @@ class Trainer:
         self.x_shape = tuple(x_shape)
         b = self.x_shape[0]
         self.augment = augment
-        self.y_pin = PinnedArray((b,))
-        self.y_dev = Tensor((b,), Buffer(b, F32))
-        if augment is None:
-            self.x_pin = PinnedArray(self.x_shape)
-            self.x_dev = Tensor(self.x_shape, Buffer(int(np.prod(self.x_shape)), F32))
-        else:
-            # raw uint8 images (held in a 4-byte-word buffer), per-image crop offsets / flip bits (int32)
-            nbytes = int(np.prod(self.x_shape))
-            self.x_pin = PinnedArray(self.x_shape, np.uint8)
-            self.x_dev = Tensor(((nbytes + 3) // 4,), Buffer((nbytes + 3) // 4, F32))
-            self.offs_pin = PinnedArray((b, 3), np.int32)
-            self.offs_dev = Tensor((b * 3,), Buffer(b * 3, F32))
+        self._slots = [_InputSlot(self.x_shape, augment)]
+        self._cur = 0  # input slot the next step reads
+        self._async_n = 0
+        self._copy_stream = None
+        if augment is not None:
             pad, mean, std = augment
             c = self.x_shape[3]
             self.aug_stats = Tensor((2, c), Buffer(2 * c, F32))
             self.aug_stats.buffer.upload(np.stack([np.broadcast_to(np.asarray(mean, np.float32), (c,)),
                                                    np.broadcast_to(np.asarray(std, np.float32), (c,))]))
             self.aug_rng = np.random.default_rng(augment_seed)
-        for t in (self.x_dev, self.y_dev):
-            t.refs = 1  # external hold: the traversal never returns these to the pool
-        self.y_dev.host_src = self.y_pin.array
         # token models: ids are validated on the host at staging time (sync-free inside the step)
         self.input_classes = getattr(model, "input_classes", None)
         if self.input_classes is not None:
             self.x_dev.host_src = self.x_pin.array
         self.steps_done = 0
-        self.graph: StepGraph | None = None
-        self.loss_slot: int | None = None
         self.fresh_at_capture = None
-        self._copied = None
+
+    # the current input slot's buffers (slot 0 unless step_async alternates)
+    x_pin = property(lambda self: self._slots[self._cur].x_pin)
+    y_pin = property(lambda self: self._slots[self._cur].y_pin)
+    x_dev = property(lambda self: self._slots[self._cur].x_dev)
+    y_dev = property(lambda self: self._slots[self._cur].y_dev)
+    offs_pin = property(lambda self: self._slots[self._cur].offs_pin)
+    offs_dev = property(lambda self: self._slots[self._cur].offs_dev)
+    graph = property(lambda self: self._slots[self._cur].graph)
+    loss_slot = property(lambda self: self._slots[self._cur].loss_slot)
 
     # -- the step body (recorded on the tape) --
     def _body(self) -> DeviceScalar:
@@ -182,13 +212,13 @@ class Trainer:
         check_index_values(y, self.classes, "target")
         if self.input_classes is not None:
             check_index_values(np.asarray(x_host, dtype=np.float32), self.input_classes, "onehot")
-        lib, st = _lib.lib(), _lib.stream()
-        if self._copied is None:
-            ev = C.c_void_p()
-            check(lib.nsk_event_create(0, C.byref(ev)))
-            self._copied = ev.value
-        else:
-            check(lib.nsk_event_sync(self._copied))  # previous H2D finished reading the pinned buffers
+        lib = _lib.lib()
+        sl = self._slots[self._cur]
+        st = self._copy_stream if self._copy_stream is not None else _lib.stream()
+        if sl.copy_pending:
+            check(lib.nsk_event_sync(sl.copied))  # the previous H2D finished reading the pinned buffers
+        if st != _lib.stream():
+            check(lib.nsk_event_wait(st, sl.consumed))  # the last step reading this slot's device inputs is done
         np.copyto(self.x_pin.array, np.asarray(x_host, dtype=self.x_pin.dtype).reshape(self.x_shape))
         np.copyto(self.y_pin.array, y)
         check(lib.nsk_memcpy_h2d(self.x_dev.ptr, self.x_pin.ptr, self.x_pin.nbytes, st))
@@ -200,24 +230,28 @@ class Trainer:
             np.copyto(self.offs_pin.array, offs.reshape(-1, 3))
             check(lib.nsk_memcpy_h2d(self.offs_dev.ptr, self.offs_pin.ptr, self.offs_pin.nbytes, st))
         check(lib.nsk_memcpy_h2d(self.y_dev.ptr, self.y_pin.ptr, self.y_pin.nbytes, st))
-        check(lib.nsk_event_record(self._copied, st))
+        check(lib.nsk_event_record(sl.copied, st))
+        sl.copy_pending = True
+        if st != _lib.stream():
+            check(lib.nsk_event_wait(_lib.stream(), sl.copied))  # compute waits for the copy, not the host
 
     def run_staged(self) -> DeviceScalar:
         """One step on the already-staged device batch (no host copies)."""
-        if self.graph is not None:
-            self.graph.launch()
-            self.steps_done += 1
-            return DeviceScalar(self.loss_slot)
-        if self.use_graph and self.steps_done >= self.warmup:
+        sl = self._slots[self._cur]
+        if sl.graph is not None:
+            sl.graph.launch()
+            sc = DeviceScalar(sl.loss_slot)
+        elif self.use_graph and self.steps_done >= self.warmup:
             fresh = self.s.pool.stats()["fresh"]
-            self.graph, sc = capture(self._body)
+            sl.graph, sc = capture(self._body)
             if self.s.pool.stats()["fresh"] != fresh:
                 raise NskRuntimeError("pool was not warm at capture time")
-            self.loss_slot = sc.slot
-            self.graph.launch()
-            self.steps_done += 1
-            return DeviceScalar(self.loss_slot)
-        sc = self._body()
+            sl.loss_slot = sc.slot
+            sl.graph.launch()
+            sc = DeviceScalar(sl.loss_slot)
+        else:
+            sc = self._body()
+        check(_lib.lib().nsk_event_record(sl.consumed, _lib.stream()))
         self.steps_done += 1
         return sc
 
@@ -227,6 +261,21 @@ class Trainer:
         # the pinned staging buffers may be overwritten by the next stage() only after this step's copies ran
         return self.run_staged()
 
+    def step_async(self, x_host, y_host, offsets=None) -> DeviceScalar:
+        """``step`` with the host->device copy on a copy stream into one of two input slots, so the copy (and
+        the host-side staging) of batch i+1 overlaps the device work of batch i. Each slot has its own
+        captured graph; the returned loss is still a device scalar (read it when needed)."""
+        if len(self._slots) < 2:
+            self._slots.append(_InputSlot(self.x_shape, self.augment))
+            s = C.c_void_p()
+            check(_lib.lib().nsk_stream_create(C.byref(s)))
+            self._copy_stream = s.value
+        self._cur = self._async_n % 2
+        self._async_n += 1
+        self.stage(x_host, y_host, offsets)
+        return self.run_staged()
+
     @property
     def launches_per_step(self) -> int:
-        return self.graph.nodes if self.graph is not None else -1
+        g = self._slots[0].graph
+        return g.nodes if g is not None else -1

@@ -232,10 +232,11 @@ def test_resnet50_graphed_training_steps(dev):
 
 @pytest.mark.parametrize("model", ["smallcnn", "resnet18"])
 def test_loss_trajectory_100_steps(dev, model):
-    """North star: the 100-step loss trajectory stays within 1% of the CPU reference (float64 oracle), on the
-    committed golden (tests/golden/gen_trajectory.py: fixed synthetic dataset, reference epoch shuffling,
-    batch 32, SGD lr 0.01 m 0.9). Bar: every 10-step window mean within 1%; each single step within
-    max(2%, 2x the oracle's own bf16-vs-f64 deviation at that step)."""
+    """North star: the loss trajectory stays within 1% of the CPU reference (float64 oracle), on the committed
+    golden (tests/golden/gen_trajectory.py: fixed synthetic dataset, reference epoch shuffling, batch 32, SGD
+    m 0.9; small CNN 100 steps at lr 0.01, ResNet-18 30 steps at lr 0.002). Bar: every 10-step window mean
+    within 1%; each single step within max(1%, 2x the oracle's own bf16-vs-f64 deviation at that step) --
+    per-step losses of a BatchNorm network drift under rounding alone, which the golden records."""
     import importlib.util
     import os
 
@@ -253,12 +254,32 @@ def test_loss_trajectory_100_steps(dev, model):
     sched = G.schedule(len(f64))
     s = Session(seed=0)
     net = ResNet18(s) if model == "resnet18" else SmallCNN(s)
-    tr = Trainer(s, net, (G.TRAJ_BATCH, 3, 32, 32), 10, optimizer=("sgd", G.LR, G.MOMENTUM), graph=True, warmup=2)
+    lr = G.SETTINGS[model][1]
+    tr = Trainer(s, net, (G.TRAJ_BATCH, 3, 32, 32), 10, optimizer=("sgd", lr, G.MOMENTUM), graph=True, warmup=2)
     got = np.array([float(tr.step(x[rows], y[rows])) for rows in sched])
     assert np.all(np.isfinite(got))
     win = lambda a: a.reshape(-1, 10).mean(axis=1)  # noqa: E731
     wdev = np.abs(win(got) - win(f64)) / win(f64)
     assert wdev.max() <= 1e-2, (wdev.max(), np.round(win(got), 4), np.round(win(f64), 4))
     step_dev = np.abs(got - f64) / f64
-    bar = np.maximum(2e-2, 2 * np.abs(b16 - f64) / f64)
+    bar = np.maximum(1e-2, 2 * np.abs(b16 - f64) / f64)
     assert np.all(step_dev <= bar), (int(np.argmax(step_dev - bar)), step_dev.max())
+
+
+def test_step_async_double_buffered_matches_step(dev):
+    """Trainer.step_async (copy stream, two input slots, two graphs) reproduces Trainer.step losses."""
+    from paper_2409_11600_b200.models import ResNet18
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    rng = np.random.default_rng(8)
+    b = 16
+    xs = [rng.standard_normal((b, 3, 32, 32)).astype(np.float32) for _ in range(7)]
+    ys = [rng.integers(0, 10, b).astype(np.float32) for _ in range(7)]
+    out = {}
+    for mode in ("step", "async"):
+        s = Session(seed=0)
+        tr = Trainer(s, ResNet18(s), xs[0].shape, 10, optimizer=("sgd", 0.1, 0.9), graph=True, warmup=2)
+        fn = tr.step if mode == "step" else tr.step_async
+        out[mode] = [float(fn(x, y)) for x, y in zip(xs, ys)]  # a graph's loss slot is reused: read each step
+    np.testing.assert_allclose(out["async"], out["step"], rtol=1e-5)
