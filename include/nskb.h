@@ -172,10 +172,11 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
                float* ws, void* stream);
 int nsk_avgpool_fwd(int dtype_in, const void* x, float* y, int N, int HW, int C, void* stream);
 int nsk_avgpool_bwd(const float* dy, int dtype_out, void* dx, int N, int HW, int C, void* stream);
-int nsk_maxpool_fwd(const void* x, void* y, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
-                    void* stream);
-int nsk_maxpool_bwd(const void* x, const void* dy, void* dx, int N, int H, int W, int C, int k, int stride, int pad,
+/* argmax: one byte per output element (window position r*k+s of the first maximum), written by the forward */
+int nsk_maxpool_fwd(const void* x, void* y, void* argmax, int N, int H, int W, int C, int k, int stride, int pad,
                     int P, int Q, void* stream);
+int nsk_maxpool_bwd(const void* argmax, const void* dy, void* dx, int N, int H, int W, int C, int k, int stride,
+                    int pad, int P, int Q, void* stream);
 /* NCHW f32 (host image layout) -> NHWC bf16 with channel padding to Cp (zeros) */
 int nsk_nchw_to_nhwc(const float* x, void* y, int N, int C, int H, int W, int Cp, void* stream);
 int nsk_nhwc_to_nchw(int dtype_in, const void* x, float* y, int N, int C, int H, int W, int Cp, void* stream);

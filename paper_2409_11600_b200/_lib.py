@@ -93,7 +93,7 @@ SIGNATURES = {
     "nsk_bn_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, f32, u64, i32, vp, vp]),
     "nsk_avgpool_fwd": (i32, [i32, vp, vp, i32, i32, i32, vp]),
     "nsk_avgpool_bwd": (i32, [vp, i32, vp, i32, i32, i32, vp]),
-    "nsk_maxpool_fwd": (i32, [vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
+    "nsk_maxpool_fwd": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
     "nsk_maxpool_bwd": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),
     "nsk_nchw_to_nhwc": (i32, [vp, vp, i32, i32, i32, i32, i32, vp]),
     "nsk_nhwc_to_nchw": (i32, [i32, vp, vp, i32, i32, i32, i32, i32, vp]),

@@ -50,74 +50,110 @@ __global__ void avgpool_bwd_kernel(const float* __restrict__ dy, T* __restrict__
 }
 
 // max pool (NHWC bf16): window k x k, stride, pad (padding = -inf); first maximum wins (numpy argmax convention)
-__global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, int N, int H,
-                                   int W, int C, int k, int st, int pad, int P, int Q) {
+// 8 channels per thread (16-byte loads); the window position of the first maximum (row-major window order,
+// strictly greater wins: restated.maxpool_bwd) is saved per output element as one byte for the backward.
+__global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                   uint8_t* __restrict__ arg, int N, int H, int W, int C, int k, int st, int pad,
+                                   int P, int Q) {
   pdl_wait();
-  const long long n_out = (long long)N * P * Q * C;
+  const int CV = C / 8;
+  const long long n_out = (long long)N * P * Q * CV;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_out; i += (long long)gridDim.x * blockDim.x) {
-    int c = (int)(i % C);
-    long long t = i / C;
-    int q = (int)(t % Q);
+    const int cv = (int)(i % CV);
+    long long t = i / CV;
+    const int q = (int)(t % Q);
     t /= Q;
-    int p = (int)(t % P);
-    long long n = t / P;
-    float best = -INFINITY;
+    const int p = (int)(t % P);
+    const long long n = t / P;
+    float best[8];
+    uint32_t at[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      best[j] = -INFINITY;
+      at[j] = 0;
+    }
+    bool first = true;
     for (int r = 0; r < k; ++r) {
-      int h = p * st - pad + r;
+      const int h = p * st - pad + r;
       if (h < 0 || h >= H) continue;
       for (int s = 0; s < k; ++s) {
-        int w = q * st - pad + s;
+        const int w = q * st - pad + s;
         if (w < 0 || w >= W) continue;
-        float v = __bfloat162float(x[((n * H + h) * W + w) * C + c]);
-        if (v > best) best = v;
+        const uint4 u = __ldg((const uint4*)(x + ((n * H + h) * W + w) * C + cv * 8));
+        const __nv_bfloat162* h2 = (const __nv_bfloat162*)&u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(h2[j]);
+          if (first || f.x > best[2 * j]) {
+            best[2 * j] = f.x;
+            at[2 * j] = r * k + s;
+          }
+          if (first || f.y > best[2 * j + 1]) {
+            best[2 * j + 1] = f.y;
+            at[2 * j + 1] = r * k + s;
+          }
+        }
+        first = false;
       }
     }
-    y[i] = __float2bfloat16_rn(best);
+    uint4 o;
+    o.x = pack_bf16x2(best[0], best[1]);
+    o.y = pack_bf16x2(best[2], best[3]);
+    o.z = pack_bf16x2(best[4], best[5]);
+    o.w = pack_bf16x2(best[6], best[7]);
+    *(uint4*)(y + i * 8) = o;
+    uint2 a8;
+    a8.x = at[0] | (at[1] << 8) | (at[2] << 16) | (at[3] << 24);
+    a8.y = at[4] | (at[5] << 8) | (at[6] << 16) | (at[7] << 24);
+    *(uint2*)(arg + i * 8) = a8;
   }
 }
 
-// gather formulation: each input element sums dy over the windows whose (first) argmax it is. No atomics.
-__global__ void maxpool_bwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ dy,
+// gather formulation: each input element sums dy over the windows whose saved first-argmax it is. No atomics,
+// fixed summation order (window row-major), 8 channels per thread.
+__global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const __nv_bfloat16* __restrict__ dy,
                                    __nv_bfloat16* __restrict__ dx, int N, int H, int W, int C, int k, int st, int pad,
                                    int P, int Q) {
   pdl_wait();
-  const long long n_in = (long long)N * H * W * C;
+  const int CV = C / 8;
+  const long long n_in = (long long)N * H * W * CV;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_in; i += (long long)gridDim.x * blockDim.x) {
-    int c = (int)(i % C);
-    long long t = i / C;
-    int w = (int)(t % W);
+    const int cv = (int)(i % CV);
+    long long t = i / CV;
+    const int w = (int)(t % W);
     t /= W;
-    int h = (int)(t % H);
-    long long n = t / H;
-    float acc = 0.f;
+    const int h = (int)(t % H);
+    const long long n = t / H;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     // outputs p with p*st - pad <= h <= p*st - pad + k - 1
-    int p_lo = (h + pad - k + 1 + st - 1) / st;
-    if (h + pad - k + 1 < 0) p_lo = 0;
-    int p_hi = (h + pad) / st;
-    int q_lo = (w + pad - k + 1 + st - 1) / st;
-    if (w + pad - k + 1 < 0) q_lo = 0;
-    int q_hi = (w + pad) / st;
-    for (int p = p_lo; p <= p_hi && p < P; ++p)
+    int p_lo = h + pad - k + 1 <= 0 ? 0 : (h + pad - k + 1 + st - 1) / st;
+    const int p_hi = (h + pad) / st;
+    int q_lo = w + pad - k + 1 <= 0 ? 0 : (w + pad - k + 1 + st - 1) / st;
+    const int q_hi = (w + pad) / st;
+    for (int p = p_lo; p <= p_hi && p < P; ++p) {
+      const uint32_t r = h - (p * st - pad);
       for (int q = q_lo; q <= q_hi && q < Q; ++q) {
-        float best = -INFINITY;
-        int bh = -1, bw = -1;
-        for (int r = 0; r < k; ++r) {
-          int hh = p * st - pad + r;
-          if (hh < 0 || hh >= H) continue;
-          for (int s = 0; s < k; ++s) {
-            int ww = q * st - pad + s;
-            if (ww < 0 || ww >= W) continue;
-            float v = __bfloat162float(x[((n * H + hh) * W + ww) * C + c]);
-            if (bh < 0 || v > best) {
-              best = v;
-              bh = hh;
-              bw = ww;
-            }
-          }
+        const uint32_t tap = r * k + (w - (q * st - pad));
+        const long long o = ((n * P + p) * Q + q) * C + cv * 8;
+        const uint2 a8 = __ldg((const uint2*)(arg + o));
+        const uint4 g = __ldg((const uint4*)(dy + o));
+        const __nv_bfloat162* g2 = (const __nv_bfloat162*)&g;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(g2[j]);
+          const uint32_t word = j < 2 ? a8.x : a8.y;
+          const int sh = (j & 1) * 16;
+          if (((word >> sh) & 0xff) == tap) acc[2 * j] += f.x;
+          if (((word >> (sh + 8)) & 0xff) == tap) acc[2 * j + 1] += f.y;
         }
-        if (bh == h && bw == w) acc += __bfloat162float(dy[((n * P + p) * Q + q) * C + c]);
       }
-    dx[i] = __float2bfloat16_rn(acc);
+    }
+    uint4 u;
+    u.x = pack_bf16x2(acc[0], acc[1]);
+    u.y = pack_bf16x2(acc[2], acc[3]);
+    u.z = pack_bf16x2(acc[4], acc[5]);
+    u.w = pack_bf16x2(acc[6], acc[7]);
+    *(uint4*)(dx + i * 8) = u;
   }
 }
 
@@ -310,20 +346,24 @@ int nsk_avgpool_bwd(const float* dy, int dtype_out, void* dx, int N, int HW, int
   return NSK_OK;
 }
 
-int nsk_maxpool_fwd(const void* x, void* y, int N, int H, int W, int C, int k, int stride, int pad, int P, int Q,
-                    void* stream) {
+int nsk_maxpool_fwd(const void* x, void* y, void* argmax, int N, int H, int W, int C, int k, int stride, int pad,
+                    int P, int Q, void* stream) {
+  if (C % 8 || ((uintptr_t)x & 15) || ((uintptr_t)y & 15) || ((uintptr_t)argmax & 7) || k * k > 255)
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: C must be a multiple of 8, buffers aligned, k*k < 256");
   long long n = (long long)N * P * Q * C;
-  nsk::launch_pdl(maxpool_fwd_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
-      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, N, H, W, C, k, stride, pad, P, Q);
+  nsk::launch_pdl(maxpool_fwd_kernel, nsk::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream,
+      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)argmax, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_fwd");
   return NSK_OK;
 }
 
-int nsk_maxpool_bwd(const void* x, const void* dy, void* dx, int N, int H, int W, int C, int k, int stride, int pad,
-                    int P, int Q, void* stream) {
+int nsk_maxpool_bwd(const void* argmax, const void* dy, void* dx, int N, int H, int W, int C, int k, int stride,
+                    int pad, int P, int Q, void* stream) {
+  if (C % 8 || ((uintptr_t)dy & 15) || ((uintptr_t)dx & 15) || ((uintptr_t)argmax & 7))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: C must be a multiple of 8, buffers aligned");
   long long n = (long long)N * H * W * C;
-  nsk::launch_pdl(maxpool_bwd_kernel, nsk::grid_for(n, 256), 256, 0, (cudaStream_t)stream, 
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, N, H, W, C, k, stride, pad, P, Q);
+  nsk::launch_pdl(maxpool_bwd_kernel, nsk::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream,
+      (const uint8_t*)argmax, (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_bwd");
   return NSK_OK;
 }

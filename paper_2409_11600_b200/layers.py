@@ -281,24 +281,27 @@ def _r_avgpool(node, g, pool, sinks):
 
 
 def maxpool(x: Tensor, k: int, stride: int, pad: int, pool: Pool) -> Tensor:
+    """k x k max-pool (NHWC bf16); the first-maximum window position is kept as one byte per output for the
+    backward (restated.maxpool_bwd tie rule)."""
     if x.dtype != BF16:
         raise NskTypeError("maxpool expects a bf16 NHWC activation")
     n, h, w, c = x.shape
     p, q = conv_out(h, k, stride, pad), conv_out(w, k, stride, pad)
     y = empty_tensor(pool, (n, p, q, c), BF16)
-    check(_lib.lib().nsk_maxpool_fwd(x.ptr, y.ptr, n, h, w, c, k, stride, pad, p, q, _lib.stream()))
-    record("maxpool", y, x, saved=(x,), attrs={"k": k, "stride": stride, "pad": pad})
+    arg = _internal_tensor(empty_tensor(pool, ((n * p * q * c + 3) // 4,)))  # bytes in a float32 buffer
+    check(_lib.lib().nsk_maxpool_fwd(x.ptr, y.ptr, arg.ptr, n, h, w, c, k, stride, pad, p, q, _lib.stream()))
+    record("maxpool", y, x, saved=(arg,), attrs={"k": k, "stride": stride, "pad": pad, "shape": x.shape})
     return y
 
 
 @rule("maxpool")
 def _r_maxpool(node, g, pool, sinks):
-    (x,) = node.saved
+    (arg,) = node.saved
     a = node.attrs
-    n, h, w, c = x.shape
+    n, h, w, c = a["shape"]
     _, p, q, _ = g.shape
-    dx = empty_tensor(pool, x.shape, BF16)
-    check(_lib.lib().nsk_maxpool_bwd(x.ptr, g.ptr, dx.ptr, n, h, w, c, a["k"], a["stride"], a["pad"], p, q,
+    dx = empty_tensor(pool, a["shape"], BF16)
+    check(_lib.lib().nsk_maxpool_bwd(arg.ptr, g.ptr, dx.ptr, n, h, w, c, a["k"], a["stride"], a["pad"], p, q,
                                      _lib.stream()))
     return [dx]
 

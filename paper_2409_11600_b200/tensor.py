@@ -35,6 +35,21 @@ MATMUL_PRECISION = os.environ.get("NSK_MATMUL_PRECISION", "tf32")  # "tf32" (tcg
 _TC_MIN_WORK = 1 << 24  # below this M*N*K the exact SIMT kernel costs only microseconds
 
 
+class _GrowBuffer:
+    """Grow-only float32 scratch (stream-ordered reuse by consecutive kernels)."""
+
+    def __init__(self):
+        self.buf = None
+
+    def get(self, nbytes: int):
+        if self.buf is None or self.buf.nbytes < nbytes:
+            self.buf = Buffer((max(nbytes, 1 << 20) + 3) // 4, F32)
+        return self.buf
+
+
+_TRANSPOSE_WS = _GrowBuffer()
+
+
 def _np_dtype(dtype):
     return np.float32 if dtype == F32 else np.uint16
 
@@ -424,8 +439,27 @@ def _gemm(a_ptr, a_mn, lda, b_ptr, b_mn, ldb, M, N, K, out_ptr, ldc, dtype=F32, 
         check(lib.nsk_gemm(BF16, a_mn, b_mn, M, N, K, a_ptr, lda, b_ptr, ldb, out_ptr, ldc, int(out_f32),
                            bias_ptr, beta, st))
         return
-    use_tc = (MATMUL_PRECISION == "tf32" and aligned and M * N * K >= _TC_MIN_WORK and not a_mn and not b_mn)
-    if use_tc:
+    use_tc = MATMUL_PRECISION == "tf32" and aligned and M * N * K >= _TC_MIN_WORK
+    if use_tc and (a_mn or b_mn):
+        # MN-major float32 operands (weight / input gradients of a large classifier): transpose them to
+        # K-major once (a memory pass) and stay on the tf32 tensor cores instead of the SIMT kernel
+        ws = _TRANSPOSE_WS.get(4 * ((M * K if a_mn else 0) + (N * K if b_mn else 0)))
+        p = ws.ptr
+        if a_mn:  # A stored [K, M] with row pitch lda -> [M, K]
+            if lda != M:
+                use_tc = False
+            else:
+                check(lib.nsk_transpose_2d(F32, a_ptr, p, K, M, st))
+                a_ptr, lda, a_mn, p = p, K, 0, p + 4 * M * K
+        if b_mn and use_tc:
+            if ldb != N:
+                use_tc = False
+            else:
+                check(lib.nsk_transpose_2d(F32, b_ptr, p, K, N, st))
+                b_ptr, ldb, b_mn = p, K, 0
+        if use_tc and ((lda * 4) % 16 or (ldb * 4) % 16):
+            use_tc = False
+    if use_tc and not a_mn and not b_mn:
         check(lib.nsk_gemm(F32, 0, 0, M, N, K, a_ptr, lda, b_ptr, ldb, out_ptr, ldc, 1, bias_ptr, beta, st))
     else:
         check(lib.nsk_gemm_simt(a_mn, b_mn, M, N, K, a_ptr, lda, b_ptr, ldb, out_ptr, ldc, bias_ptr, beta, st))

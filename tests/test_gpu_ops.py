@@ -403,13 +403,17 @@ def test_clip_grad_norm(session):
 
 # --- pooling / layout / augmentation / embedding ----------------------------------------------------------
 
-def test_avgpool_and_maxpool(session):
+@pytest.mark.parametrize("relu_ties", [False, True])
+def test_avgpool_and_maxpool(session, relu_ties):
+    """relu_ties: post-ReLU input (many equal zeros) exercises the first-maximum tie rule, bit for bit."""
     from paper_2409_11600_b200 import autodiff, layers
     from paper_2409_11600_b200._lib import BF16
 
     rng = np.random.default_rng(5)
     pool = session.pool
     x = X.round_bf16(rng.standard_normal((4, 8, 8, 64)))
+    if relu_ties:
+        x = np.maximum(x, 0)
     xt = autodiff.make_param(pool, x, "x", dtype=BF16)
     y = layers.avgpool_global(autodiff.make_data(pool, x, dtype=BF16), pool)
     assert rel(y.data, X.avgpool_fwd(x)) < 1e-6
