@@ -60,13 +60,15 @@ struct UmmaProb {
   // im2col-mode A operand (any output width): the tile's first pixel sits at bounding-box position
   // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
   int i2c, lw, lh;
+  int tma_store;  // bf16 output rows contiguous in m (fprop, stride-1 dgrad, GEMM): epilogue writes via TMA
   // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
   // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
   float* stats;
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
-constexpr int kStgPitch = 80;
+constexpr int kStgPitch = 64;          // epilogue staging: dense 32 x 32 bf16 blocks (TMA-store source)
+constexpr int kStgBytes = 32 * kStgPitch;
 constexpr int kProducers = 3;          // TMA issuing threads (warps 0, 2, 3)          // epilogue staging row pitch (64 B of bf16 + 16 B pad)
 
 template <int ESZ>
@@ -76,15 +78,18 @@ struct KT {
   static constexpr int UK = 32 / ESZ;   // UMMA K per instruction (16 bf16 / 8 tf32)
 };
 
-template <int BN, int ESZ, int STAGES, bool RR = false>
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4>
 struct Smem {
   static constexpr int A_BYTES = RR ? kRRMaxA : 128 * 128;
   static constexpr int B1_BYTES = BN * 128;               // one tap's B tile
   static constexpr int B_BYTES = B1_BYTES * (RR ? 3 : 1);  // rr: up to 3 taps per column group
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int STG_OFF = BAR_OFF + 8 * (2 * STAGES + 4) + 16;
-  static constexpr int TOTAL = STG_OFF + 4 * 32 * 80 + 1024;  // + epilogue staging (4 warps x 32 rows x 80 B)
+  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 16 + 127) / 128 * 128;  // TMA-store source
+  // staging buffers per epilogue warp: double-buffered with 8 warps (one CTA per SM anyway); single with 4 so
+  // the 64/128-wide tiles keep two CTAs per SM
+  static constexpr int NSTG = EPI == 8 ? 2 : 1;
+  static constexpr int TOTAL = STG_OFF + EPI * NSTG * kStgBytes + 1024;  // + epilogue staging
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
@@ -102,8 +107,9 @@ __device__ __forceinline__ uint4 bf16x8_axpby(uint4 old, float beta, uint4 v) {
   return r;
 }
 
-// named barrier over the four epilogue warps (128 threads)
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barriers: one per epilogue warpgroup (ids 1, 2; 128 threads), one over all epilogue warps (id 3)
+__device__ __forceinline__ void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
+__device__ __forceinline__ void epi_bar_all(int threads) { asm volatile("bar.sync 3, %0;" ::"r"(threads) : "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
   asm volatile(
@@ -143,11 +149,14 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 // Persistent warp-specialised tcgen05 kernel: each CTA walks work units u = blockIdx.x, +gridDim.x, ...
 // The smem ring runs continuously across units; two TMEM accumulators let the epilogue of unit j
 // overlap the MMAs of unit j+1.
-template <int BN, int ESZ, int STAGES, bool RR>
-__global__ void __launch_bounds__(256, 1)
-    umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const UmmaProb p) {
+// EPI epilogue warps (4 or 8): with 8, two warpgroups take alternate 32-column chunks of each tile, doubling the
+// TMEM-drain / store parallelism for the wide (BN = 256) tiles whose epilogue is the bottleneck.
+template <int BN, int ESZ, int STAGES, bool RR, int EPI>
+__global__ void __launch_bounds__(128 + 32 * EPI, 1)
+    umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const UmmaProb p) {
   pdl_wait();
-  using S = Smem<BN, ESZ, STAGES, RR>;
+  using S = Smem<BN, ESZ, STAGES, RR, EPI>;
   using T = KT<ESZ>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -169,7 +178,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], EPI);  // one arrival per epilogue warp
     }
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
@@ -350,14 +359,16 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
-    const int q = warp & 3;
+    const int q = warp & 3;         // TMEM lane quarter (a warp may only access lanes 32*(warp%4) .. +31)
+    const int eg = (warp - 4) >> 2;  // epilogue warpgroup: chunks eg, eg + EPI/4, ...
     const int r = q * 32 + lane;  // tile row == TMEM lane
     const bool vec_ok = ((p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0);
-    float* st_acc = (float*)(stage_base + 4 * 32 * kStgPitch);  // [2][N] CTA channel sums (stats mode)
-    float* st_red = st_acc + 2 * p.N;                           // [4 warps][2][32]
+    float* st_acc = (float*)(stage_base + EPI * S::NSTG * kStgBytes);  // [2][N] CTA channel sums (stats mode)
+    int sbuf = 0;  // staging double buffer (TMA stores of the previous chunk may still be reading the other)
+    float* st_red = st_acc + 2 * p.N + eg * 256;                // per warpgroup: [4 warps][2][32]
     if (p.stats) {
-      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 128) st_acc[i] = 0.f;
-      epi_bar();
+      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) st_acc[i] = 0.f;
+      epi_bar_all(32 * EPI);
     }
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -386,7 +397,7 @@ __global__ void __launch_bounds__(256, 1)
       int nchunks = (p.N - w.n0 + 31) / 32;
       if (nchunks > BN / 32) nchunks = BN / 32;
 #pragma unroll 1
-      for (int c = 0; c < nchunks; ++c) {
+      for (int c = eg; c < nchunks; c += EPI / 4) {
         uint32_t v[32];
         if (w.nk > 0) {
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
@@ -432,16 +443,30 @@ __global__ void __launch_bounds__(256, 1)
         } else if (full_chunk) {
           // bf16: stage this warp's 32 rows x 32 columns in shared memory, then write 16-byte pieces so
           // one store instruction covers 8 rows x 64 contiguous bytes instead of 32 scattered rows.
-          uint8_t* stg = stage_base + q * (32 * kStgPitch);
-#pragma unroll
-          for (int t = 0; t < 32; t += 8) {
-            uint4 u4;
-            u4.x = pack_bf16x2(f[t], f[t + 1]);
-            u4.y = pack_bf16x2(f[t + 2], f[t + 3]);
-            u4.z = pack_bf16x2(f[t + 4], f[t + 5]);
-            u4.w = pack_bf16x2(f[t + 6], f[t + 7]);
-            *(uint4*)(stg + lane * kStgPitch + t * 2) = u4;
+          uint8_t* stg = stage_base + ((warp - 4) * S::NSTG + sbuf) * kStgBytes;
+          if (p.tma_store) {
+            if (lane == 0) {  // the TMA store that last read this buffer is done with it
+              if constexpr (S::NSTG == 2)
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              else
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncwarp();
           }
+          uint4 u4[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            u4[t].x = pack_bf16x2(f[8 * t], f[8 * t + 1]);
+            u4[t].y = pack_bf16x2(f[8 * t + 2], f[8 * t + 3]);
+            u4[t].z = pack_bf16x2(f[8 * t + 4], f[8 * t + 5]);
+            u4[t].w = pack_bf16x2(f[8 * t + 6], f[8 * t + 7]);
+          }
+#pragma unroll
+          for (int c4 = 0; c4 < 4; ++c4) {  // rotated 16-byte chunks: 4-way instead of 16-way bank conflicts
+            const int t = (c4 + lane) & 3;
+            *(uint4*)(stg + lane * kStgPitch + t * 16) = u4[t];
+          }
+          if (p.tma_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (p.stats) {
             // column sums of the staged (bf16-rounded) tile: lane = column, rows of this warp
@@ -457,13 +482,24 @@ __global__ void __launch_bounds__(256, 1)
             }
             st_red[q * 64 + lane] = s1;
             st_red[q * 64 + 32 + lane] = s2;
-            epi_bar();
+            epi_bar(eg);
             if (q == 0) {  // fixed warp order: deterministic
               st_acc[col0 + lane] += (st_red[lane] + st_red[64 + lane]) + (st_red[128 + lane] + st_red[192 + lane]);
               st_acc[p.N + col0 + lane] +=
                   (st_red[32 + lane] + st_red[96 + lane]) + (st_red[160 + lane] + st_red[224 + lane]);
             }
-            epi_bar();
+            epi_bar(eg);
+          }
+          if (p.tma_store) {
+            if (lane == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmC),
+                  "r"(smem_u32(stg)), "r"(col0), "r"(w.m0 + q * 32)
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            sbuf = (sbuf + 1) % S::NSTG;
+            continue;
           }
 #pragma unroll
           for (int it = 0; it < 4; ++it) {
@@ -489,10 +525,11 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (p.stats) {
-      epi_bar();
+      epi_bar_all(32 * EPI);
       float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
-      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 128) out[i] = st_acc[i];
+      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) out[i] = st_acc[i];
     }
   }
   __syncthreads();
@@ -588,11 +625,12 @@ int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
   return NSK_OK;
 }
 
-template <int BN, int ESZ, int STAGES, bool RR = false>
-int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStream_t st, int* grid_out) {
-  using S = Smem<BN, ESZ, STAGES, RR>;
-  auto kern = umma_kernel<BN, ESZ, STAGES, RR>;
-  const int smem = S::TOTAL + (p.stats ? (2 * p.N + 4 * 64) * (int)sizeof(float) : 0);
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4>
+int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, UmmaProb p, cudaStream_t st,
+                int* grid_out) {
+  using S = Smem<BN, ESZ, STAGES, RR, EPI>;
+  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI>;
+  const int smem = S::TOTAL + (p.stats ? (2 * p.N + EPI * 64) * (int)sizeof(float) : 0);
   if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
   static int configured = 0;
   if (smem > configured) {
@@ -605,14 +643,17 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, cudaStre
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  nsk::launch_pdl(kern, grid, 256, smem, st, a, b, p);
+  nsk::launch_pdl(kern, grid, 128 + 32 * EPI, smem, st, a, b, c, p);
   NSK_LAUNCH_CHECK("umma_kernel");
   return NSK_OK;
 }
 
 template <int ESZ>
 int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
-                cudaStream_t st, int* grid_out = nullptr) {
+                cudaStream_t st, int* grid_out = nullptr, const CUtensorMap* cmap = nullptr) {
+  static CUtensorMap dummy{};
+  const CUtensorMap& c = cmap ? *cmap : dummy;
+  if (!cmap) p.tma_store = 0;
   p.mt = mt;
   p.nt = nt;
   p.units = mt * nt * nz;
@@ -620,20 +661,26 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
     if constexpr (ESZ == 2) {
       switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
         case 64:
-          return launch_umma<64, 2, 2, true>(a, b, p, st, grid_out);
+          return launch_umma<64, 2, 2, true>(a, b, c, p, st, grid_out);
         case 128:
-          return launch_umma<128, 2, 2, true>(a, b, p, st, grid_out);
+          return launch_umma<128, 2, 2, true>(a, b, c, p, st, grid_out);
       }
     }
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "row-reuse conv needs bf16 and N <= 128");
   }
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 4>(a, b, p, st, grid_out);
+      return launch_umma<64, ESZ, 4>(a, b, c, p, st, grid_out);
     case 128:
-      return launch_umma<128, ESZ, 3>(a, b, p, st, grid_out);
-    case 256:
-      return launch_umma<256, ESZ, 4>(a, b, p, st, grid_out);
+      return launch_umma<128, ESZ, 3>(a, b, c, p, st, grid_out);
+    case 256: {
+      // 8 epilogue warps unless the statistics buffers would not fit beside them
+      using S8 = Smem<256, ESZ, 4, false, 8>;
+      const int need = S8::TOTAL + (p.stats ? (2 * p.N + 8 * 64) * (int)sizeof(float) : 0);
+      if (need <= 227 * 1024 && !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0'))
+        return launch_umma<256, ESZ, 4, false, 8>(a, b, c, p, st, grid_out);
+      return launch_umma<256, ESZ, 4>(a, b, c, p, st, grid_out);
+    }
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
 }
@@ -738,6 +785,18 @@ int i2c_map(UmmaProb& p, CUtensorMap* m, const void* act, int N, int Hin, int Wi
   return NSK_OK;
 }
 
+// TMA-store map of a bf16 [M, N] output with row pitch ldc: 32 x 32 boxes (one epilogue warp's chunk)
+bool out_map(CUtensorMap* m, void* out, long long M, int N, long long ldc) {
+  if (N % 32 || (ldc * 2) % 16 || ((uintptr_t)out & 15)) return false;
+  const char* env = getenv("NSK_TMA_STORE");
+  if (env && env[0] == '0') return false;
+  uint64_t dims[2] = {(uint64_t)N, (uint64_t)M};
+  uint64_t str[1] = {(uint64_t)ldc * 2};
+  uint32_t box[2] = {32, 32};
+  return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, str, box, nullptr,
+                          CU_TENSOR_MAP_SWIZZLE_NONE) == NSK_OK;
+}
+
 bool force_i2c() {
   const char* env = getenv("NSK_CONV_I2C");
   return env && env[0] == '1';
@@ -826,8 +885,11 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
     NSK_LAUNCH_CHECK("splitk_fold_kernel");
     return NSK_OK;
   }
-  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, st);
-  return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, st);
+  CUtensorMap mc;
+  const bool ts = !c_f32 && beta == 0.f && out_map(&mc, C, M, N, ldc);
+  p.tma_store = ts;
+  if (esz == 2) return dispatch_bn<2>(BN, ma, mb, p, mt, nt, 1, st, nullptr, ts ? &mc : nullptr);
+  return dispatch_bn<4>(BN, ma, mb, p, mt, nt, 1, st, nullptr, ts ? &mc : nullptr);
 }
 
 }  // extern "C"
@@ -886,7 +948,11 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
       return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
     p.stats = stats;
   }
-  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream, nparts);
+  CUtensorMap mc;
+  const bool ts = !y_f32 && out_map(&mc, y, p.M, d->K, d->K);
+  p.tma_store = ts;
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream, nparts,
+                        ts ? &mc : nullptr);
 }
 
 }  // namespace
@@ -972,7 +1038,11 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   } else if (ncls == 1) {
     try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN);
   }
-  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream);
+  CUtensorMap mc;
+  const bool ts = ncls == 1 && beta == 0.f && out_map(&mc, dx, p.M, d->C, d->C);
+  p.tma_store = ts;
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream, nullptr,
+                        ts ? &mc : nullptr);
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
