@@ -19,7 +19,10 @@
 namespace {
 
 enum { MODE_GEMM = 0, MODE_CONV = 1, MODE_WGRAD = 2 };
-enum { BMODE_2D = 0, BMODE_DGRAD3D = 1 };
+// BMODE_RR3: row-reuse fprop, the three taps of a column group (filter taps tw, tw+3, tw+6) fetched as ONE
+// 3-D box {64 channels, BN filters, 3 taps (element stride 3)} -- one TMA op instead of three
+// (BMODE_RR3T: the same box for dgrad, where the 64-channel box dimension is the output (N) side)
+enum { BMODE_2D = 0, BMODE_DGRAD3D = 1, BMODE_RR3 = 2, BMODE_RR3T = 3 };
 
 constexpr int kMaxTaps = 9;
 
@@ -228,6 +231,13 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           const int nt = p.gnt[w.z][g];
           mbar_expect_tx(&full[s], (uint32_t)(p.ext_rows * p.Wt * 128 + nt * S::B1_BYTES));
           tma_load_4d(&tmA, &full[s], sa, c0, w_img + p.gdw[w.z][g], h_img + p.gdhmin[w.z][g], n_img);
+          if (p.bmode == BMODE_RR3 || p.bmode == BMODE_RR3T) {
+            if (p.bmode == BMODE_RR3)
+              tma_load_3d(&tmB, &full[s], sb, c0, w.n0, p.gw[w.z][g][0]);
+            else
+              tma_load_3d(&tmB, &full[s], sb, w.n0, c0, p.gw[w.z][g][0]);
+            continue;
+          }
           for (int t = 0; t < nt; ++t) {
             if (p.bmode == BMODE_2D) {
               tma_load_2d(&tmB, &full[s], sb + t * S::B1_BYTES, p.gw[w.z][g][t] * (p.cchunks * 64) + c0, w.n0);
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer ----------------
     const int a_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? 0 : p.a_mn);
-    const int b_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? (p.bmode == BMODE_DGRAD3D) : p.b_mn);
+    const int b_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? (p.bmode == BMODE_DGRAD3D || p.bmode == BMODE_RR3T) : p.b_mn);
     const uint32_t idesc = make_idesc(ESZ == 2 ? 1u : 2u, (uint32_t)a_mn, (uint32_t)b_mn, 128u, (uint32_t)BN);
     const uint32_t a_lbo = a_mn ? (T::KS * 128) : 16;
     const uint32_t b_lbo = b_mn ? (T::KS * 128) : 16;
@@ -802,6 +812,28 @@ bool force_i2c() {
   return env && env[0] == '1';
 }
 
+// Row-reuse 3x3: every column group holds taps (dh -1, 0, +1) = filter taps tw, tw+3, tw+6, so the group's B
+// tiles are ONE strided 3-D box {64 channels, 64|BN rows, 3 taps (element stride 3)} over the KRSC filter
+// viewed as {C, K, R*S} -- one TMA op instead of three.
+void try_rr3(UmmaProb& p, CUtensorMap* mb, const NskConvDesc* d, const void* w, int BN, int mode) {
+  bool three = d->R == 3 && d->S == 3 && p.ngroups[0] == 3;
+  for (int g = 0; three && g < 3; ++g)
+    three = p.gnt[0][g] == 3 && p.gw[0][g][1] == p.gw[0][g][0] + 3 && p.gw[0][g][2] == p.gw[0][g][0] + 6;
+  const char* env = getenv("NSK_RR3");
+  if (!three || (env && env[0] == '0')) return;
+  const int RS = d->R * d->S;
+  uint64_t dims[3] = {(uint64_t)d->C, (uint64_t)d->K, (uint64_t)RS};
+  uint64_t str[2] = {(uint64_t)RS * d->C * 2, (uint64_t)d->C * 2};
+  uint32_t box[3] = {64, (uint32_t)(mode == BMODE_RR3 ? BN : 64), 9};  // span 9, stride 3 -> 3 taps loaded
+  uint32_t es[3] = {1, 1, 3};
+  CUtensorMap m;
+  if (nsk::encode_tmap(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, w, dims, str, box, es, CU_TENSOR_MAP_SWIZZLE_128B) ==
+      NSK_OK) {
+    *mb = m;
+    p.bmode = mode;
+  }
+}
+
 int check_desc(const NskConvDesc* d) {
   if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride < 1)
     return nsk::set_error(NSK_ERR_SHAPE, "conv2d: invalid descriptor");
@@ -938,8 +970,8 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   p.out_f32 = y_f32;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 128))) return rc;
-  } else {
-    try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN);
+  } else if (try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN)) {
+    try_rr3(p, &mb, d, w, BN, BMODE_RR3);
   }
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   if (stats) {
@@ -1035,8 +1067,8 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   p.beta = beta;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls, 128))) return rc;
-  } else if (ncls == 1) {
-    try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN);
+  } else if (ncls == 1 && try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN)) {
+    if (BN == 64) try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
   }
   CUtensorMap mc;
   const bool ts = ncls == 1 && beta == 0.f && out_map(&mc, dx, p.M, d->C, d->C);
