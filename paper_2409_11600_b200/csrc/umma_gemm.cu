@@ -64,6 +64,7 @@ struct UmmaProb {
   // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
   int i2c, lw, lh;
   int tma_store;  // bf16 output rows contiguous in m (fprop, stride-1 dgrad, GEMM): epilogue writes via TMA
+  int bslab;      // MN-major B (wgrad dy): all BN/64 slabs of a k-step as ONE 3-D box {64, K rows, slabs}
   // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
   // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
   float* stats;
@@ -295,6 +296,8 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         if (p.mode == MODE_GEMM || p.mode == MODE_WGRAD) {
           if (!p.b_mn) {
             tma_load_2d(&tmB, &full[s], sb, kk * T::KE, w.n0);
+          } else if (p.bslab) {
+            tma_load_3d(&tmB, &full[s], sb, 0, kk * T::KS, w.n0 / T::KE);
           } else {
 #pragma unroll
             for (int b = 0; b < BN / T::KE; ++b)
@@ -1126,7 +1129,22 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
                                CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
   }
+  // B (dy, MN-major) for a BN-wide tile = BN/64 slabs of 64 channels: one 3-D box {64, 64 pixels, BN/64 slabs}
+  // (slab stride 128 B) instead of BN/64 boxes
+  int bslab = 0;
+  if (BN > 64 && !(getenv("NSK_BSLAB") && getenv("NSK_BSLAB")[0] == '0')) {
+    uint64_t dims[3] = {64, (uint64_t)pix, (uint64_t)d->K / 64};
+    uint64_t str[2] = {(uint64_t)d->K * 2, 128};
+    uint32_t box[3] = {64, 64, (uint32_t)BN / 64};
+    CUtensorMap m3;
+    if (nsk::encode_tmap(&m3, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, dy, dims, str, box, nullptr,
+                         CU_TENSOR_MAP_SWIZZLE_128B) == NSK_OK) {
+      mb = m3;
+      bslab = 1;
+    }
+  }
   UmmaProb p{};
+  p.bslab = bslab;
   p.mode = MODE_WGRAD;
   p.a_mn = 1;
   p.b_mn = 1;
