@@ -64,6 +64,7 @@ struct UmmaProb {
   // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
   int i2c, lw, lh;
   int tma_store;  // bf16 output rows contiguous in m (fprop, stride-1 dgrad, GEMM): epilogue writes via TMA
+                  // (2: TMA reduce-add into the existing output, i.e. beta == 1 accumulation)
   int bslab;      // MN-major B (wgrad dy): all BN/64 slabs of a k-step as ONE 3-D box {64, K rows, slabs}
   // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
   // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
@@ -505,10 +506,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           }
           if (p.tma_store) {
             if (lane == 0) {
-              asm volatile(
-                  "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmC),
-                  "r"(smem_u32(stg)), "r"(col0), "r"(w.m0 + q * 32)
-                  : "memory");
+              if (p.tma_store == 2)
+                asm volatile(
+                    "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                        &tmC),
+                    "r"(smem_u32(stg)), "r"(col0), "r"(w.m0 + q * 32)
+                    : "memory");
+              else
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmC),
+                    "r"(smem_u32(stg)), "r"(col0), "r"(w.m0 + q * 32)
+                    : "memory");
               asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
             sbuf = (sbuf + 1) % S::NSTG;
@@ -1074,8 +1082,11 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
     if (BN == 64) try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
   }
   CUtensorMap mc;
-  const bool ts = ncls == 1 && beta == 0.f && out_map(&mc, dx, p.M, d->C, d->C);
-  p.tma_store = ts;
+  const char* red = getenv("NSK_TMA_REDUCE");
+  const bool ts = ncls == 1 && (beta == 0.f || (beta == 1.f && !(red && red[0] == '0'))) &&
+                  out_map(&mc, dx, p.M, d->C, d->C);
+  p.tma_store = ts ? (beta == 1.f ? 2 : 1) : 0;
+  if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream, nullptr,
                         ts ? &mc : nullptr);
 }

@@ -487,3 +487,33 @@ def test_conv_bn_fused_statistics(session, case):
     node_saved = y.node.saved
     np.testing.assert_allclose(node_saved[2].data, mean, rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(node_saved[3].data, invstd, rtol=1e-4)
+
+
+@pytest.mark.parametrize("case", [(4, 32, 32, 64, 64, 3, 1, 1), (2, 56, 56, 256, 64, 1, 1, 0),
+                                  (4, 32, 32, 64, 128, 3, 2, 1)])
+def test_conv2d_dgrad_accumulates_in_place(dev, case):
+    """nsk_conv2d_dgrad_acc: dx = dgrad + dx (TMA reduce-add for stride 1, staged read-modify-write for the
+    stride-2 parity classes) -- the in-place second gradient contribution the autodiff uses."""
+    import ctypes as C
+
+    from paper_2409_11600_b200 import _lib
+    from paper_2409_11600_b200._lib import BF16, ConvDesc
+    from paper_2409_11600_b200.tensor import Buffer
+
+    n, h, w, c, k, r, st, pad = case
+    p = (h + 2 * pad - r) // st + 1
+    rng = np.random.default_rng(sum(case))
+    dy = X.round_bf16(rng.standard_normal((n, p, p, k)))
+    wt = X.round_bf16(rng.standard_normal((k, r, r, c)) / np.sqrt(k * r * r))
+    dx0 = X.round_bf16(rng.standard_normal((n, h, w, c)))
+    bufs = {}
+    for name, a in (("dy", dy), ("w", wt), ("dx", dx0)):
+        bufs[name] = Buffer(a.size, BF16)
+        bufs[name].upload(a)
+    d = ConvDesc(n, h, w, c, k, r, r, st, pad, p, p)
+    lib = _lib.lib()
+    _lib.check(lib.nsk_conv2d_dgrad_acc(C.byref(d), bufs["dy"].ptr, bufs["w"].ptr, bufs["dx"].ptr, 1.0,
+                                        _lib.stream()))
+    got = bufs["dx"].host().reshape(dx0.shape)
+    ref = dx0.astype(np.float64) + X.round_bf16(X.conv2d_dgrad(dy, wt, dx0.shape, st, pad))
+    assert rel(got, X.round_bf16(ref)) < 1e-3
