@@ -1,0 +1,66 @@
+"""§8(f) 3: the reference's own language runtime (its lexer, parser, interpreter and CLI, unmodified) driving
+this backend. The same .nsk programs run once on the reference CPU path and once with
+paper_2409_11600_b200.nsk_backend installed; the printed training curves must agree.
+"""
+
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_CANDIDATES = (os.path.join(ROOT, "baseline", "_ref"), "/root/reference/pkg/src")
+
+
+def _ref_path():
+    for c in REF_CANDIDATES:
+        if os.path.isdir(os.path.join(c, "nsk")):
+            return c
+    pytest.skip("the reference package is not installed (baseline/_ref)")
+
+
+def _dataset(d):
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((192, 4))
+    y = (x[:, 0] + 0.5 * x[:, 1] > 0).astype(int) + (x[:, 2] > 1).astype(int)
+    with open(os.path.join(d, "data.csv"), "w") as f:
+        f.write("a,b,c,d,label\n")
+        for r, lab in zip(x, y):
+            f.write(",".join(f"{v:.6f}" for v in r) + f",{lab}\n")
+
+
+def _run(cmd_prefix, script, ref):
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([ROOT, ref]))
+    r = subprocess.run(cmd_prefix + ["run", script, "--seed", "0", "--workers", "1"], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return [ln.split() for ln in r.stdout.strip().splitlines()]
+
+
+@pytest.mark.parametrize("program,tol", [("mlp_train.nsk", 1e-4), ("minibatch_adamw.nsk", 1e-3)])
+def test_reference_interpreter_runs_on_device(tmp_path, program, tol):
+    ref = _ref_path()
+    _dataset(tmp_path)
+    script = str(tmp_path / program)
+    shutil.copy(os.path.join(ROOT, "tests", "nsk", program), script)
+    cpu = _run([sys.executable, "-c", "import sys; from nsk.cli import main; sys.exit(main(sys.argv[1:]))"], script, ref)
+    dev = _run([sys.executable, "-m", "paper_2409_11600_b200.nsk_backend"], script, ref)
+    assert len(cpu) == len(dev) and len(cpu) > 0
+    for a, b in zip(cpu, dev):
+        assert [t for t in a if not _is_num(t)] == [t for t in b if not _is_num(t)]
+        for x, y in zip(a, b):
+            if _is_num(x):
+                assert abs(float(x) - float(y)) <= tol * max(1.0, abs(float(x))), (a, b)
+
+
+def _is_num(t):
+    try:
+        float(t)
+        return True
+    except ValueError:
+        return False
