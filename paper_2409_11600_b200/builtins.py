@@ -206,6 +206,16 @@ def _flatten(session, frame, args, line):
     return session.note_tensor(layers.reshape(x, (x.shape[0], x.numel // x.shape[0]), session.pool), x)
 
 
+def _images(session, frame, args, line):
+    """images(x, h, w, c): rows of a [N, h*w*c] feature matrix (e.g. CSV pixels) as an NHWC image batch."""
+    _need(args, 4, "images", line)
+    x = _tensor(args[0], "images", line)
+    h, w, c = (_int(a, "images", line) for a in args[1:])
+    if x.rank != 2 or x.shape[1] != h * w * c:
+        raise NskTypeError(f"images: cannot view {list(x.shape)} as [N, {h}, {w}, {c}]", line)
+    return session.note_tensor(layers.reshape(x, (x.shape[0], h, w, c), session.pool), x)
+
+
 def _add(session, frame, args, line):
     _need(args, 2, "add", line)
     a, b = _tensor(args[0], "add", line), _tensor(args[1], "add", line)
@@ -285,5 +295,6 @@ BUILTINS = {
     "avgpool": _avgpool,
     "maxpool": _maxpool,
     "flatten": _flatten,
+    "images": _images,
     "add": _add,
 }

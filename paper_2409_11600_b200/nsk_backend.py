@@ -4,8 +4,9 @@
 
 The reference reaches its hot path only through module-level names: the ``Tensor`` type the
 interpreter's arithmetic dispatch checks (interpreter.py:29, :395-446), the ``rec_*`` functions it calls
-(interpreter.py:18), the tape and assignment push of ``Session`` (runtime.py:23, :140-170), the pool / grad
-cache / parameter group a ``Session`` constructs (runtime.py:26-27, :140-145), ``make_data`` in the dataset
+(interpreter.py:18), the tape and assignment push of ``Session`` (runtime.py:23, :140-170), the pool the CLI
+builds (cli.py:20, :81) and the grad cache / parameter group a ``Session`` constructs (runtime.py:26-27,
+:140-145), ``make_data`` in the dataset
 loader and builtins (dataset.py:16, builtins.py:275-281) and the ``BUILTINS`` registry (builtins.py:284),
 looked up at call time (interpreter.py:495-508). ``install`` rebinds exactly those names to the device
 implementations of this package -- nothing in the reference is edited -- so a ``.nsk`` program runs its
@@ -66,6 +67,7 @@ def install() -> None:
     _import_reference()
     import nsk.autodiff as r_autodiff
     import nsk.builtins as r_builtins
+    import nsk.cli as r_cli
     import nsk.dataset as r_dataset
     import nsk.errors as r_errors
     import nsk.interpreter as r_interp
@@ -85,6 +87,7 @@ def install() -> None:
     r_runtime.Tape = A.Tape
     r_runtime.push_assignment = A.push_assignment
     r_runtime.Pool = T.Pool
+    r_cli.Pool = T.Pool  # cli.py:81 builds the session's pool (--no-pool / --pool-stats keep working)
     r_runtime.GradCache = T.GradCache
     r_runtime.ParamGroup = N.ParamGroup
     r_dataset.make_data = A.make_data

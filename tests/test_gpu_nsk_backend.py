@@ -64,3 +64,22 @@ def _is_num(t):
         return True
     except ValueError:
         return False
+
+
+def test_reference_interpreter_trains_a_cnn_on_device(tmp_path):
+    """The new CNN builtins (conv2d, batchnorm, avgpool, images) through the reference interpreter: the
+    program runs on the device and its loss falls (the reference itself has no conv ops to compare with)."""
+    ref = _ref_path()
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((256, 8 * 8 * 3))
+    y = (x[:, :64].mean(axis=1) > 0).astype(int) * 3 + (x[:, 64:128].mean(axis=1) > 0).astype(int)
+    with open(tmp_path / "images.csv", "w") as f:
+        f.write(",".join(f"p{i}" for i in range(192)) + ",label\n")
+        for r, lab in zip(x, y):
+            f.write(",".join(f"{v:.5f}" for v in r) + f",{lab}\n")
+    script = str(tmp_path / "cnn_train.nsk")
+    shutil.copy(os.path.join(ROOT, "tests", "nsk", "cnn_train.nsk"), script)
+    out = _run([sys.executable, "-m", "paper_2409_11600_b200.nsk_backend"], script, ref)
+    losses = [float(ln[3]) for ln in out]
+    assert len(losses) == 30 and all(np.isfinite(losses))
+    assert np.mean(losses[-5:]) < 0.8 * np.mean(losses[:5]), losses
