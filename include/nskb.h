@@ -158,15 +158,23 @@ int nsk_scale_multi(int n_tensors, float* const* g, const uint64_t* numel, const
 /* x [rows, C] (NHWC flattened), bf16; training-mode batch stats (biased var), eps.
  * y = relu?((x-mean)*invstd*gamma + beta + residual?);  ws: nsk_bn_workspace(rows, C) bytes */
 uint64_t nsk_bn_workspace(uint64_t rows, int C);
+/* running (optional, [2, C]): running mean / unbiased variance updated with `momentum` from this batch */
 int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
-               float eps, int relu, const void* residual, void* relu_mask, float* ws, void* stream);
+               float eps, int relu, const void* residual, void* relu_mask, float* running, float momentum, float* ws,
+               void* stream);
 /* nsk_bn_fwd with the statistics taken from conv partials (nsk_conv2d_fprop_stats) instead of a pass over x */
 int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
                         float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
-                        void* relu_mask, float* ws, void* stream);
+                        void* relu_mask, float* running, float momentum, float* ws, void* stream);
 /* relu_mask (fwd output, bwd input; NULL without ReLU): one byte per 8 channels, bit j = [y > 0] of channel
  * 8k+j, rows*C/8 bytes. dres (optional) receives the masked gradient flowing to the residual input.
  * dgamma_beta [2, C] (= dgamma_beta*beta_acc + new). */
+/* running statistics [2, C] (mean row, unbiased variance row) updated from a training forward's mean/invstd */
+int nsk_bn_running_update(const float* mean, const float* invstd, float* running, uint64_t rows, int C,
+                          float momentum, float eps, void* stream);
+/* inference-mode forward from the running statistics (no batch statistics, nothing saved) */
+int nsk_bn_fwd_eval(const void* x, const float* gamma_beta, const float* running, void* y, uint64_t rows, int C,
+                    float eps, int relu, const void* residual, float* ws, void* stream);
 int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float* gamma_beta, const float* mean,
                const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
                float* ws, void* stream);

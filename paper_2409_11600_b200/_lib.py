@@ -88,9 +88,11 @@ SIGNATURES = {
     "nsk_clip_scale": (i32, [vp, f32, vp, vp]),
     "nsk_scale_multi": (i32, [i32, vp, vp, vp, vp]),
     "nsk_bn_workspace": (u64, [u64, i32]),
-    "nsk_bn_fwd": (i32, [vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, vp]),
-    "nsk_bn_fwd_partials": (i32, [vp, i32, vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, vp]),
+    "nsk_bn_fwd": (i32, [vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, f32, vp, vp]),
+    "nsk_bn_fwd_partials": (i32, [vp, i32, vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, f32, vp, vp]),
     "nsk_bn_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, f32, u64, i32, vp, vp]),
+    "nsk_bn_running_update": (i32, [vp, vp, vp, u64, i32, f32, f32, vp]),
+    "nsk_bn_fwd_eval": (i32, [vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp]),
     "nsk_avgpool_fwd": (i32, [i32, vp, vp, i32, i32, i32, vp]),
     "nsk_avgpool_bwd": (i32, [vp, i32, vp, i32, i32, i32, vp]),
     "nsk_maxpool_fwd": (i32, [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, i32, i32, vp]),

@@ -117,7 +117,7 @@ __device__ void fold_partials(const float* part, int nblk, int C, int c, double*
 // fold partials (float64) -> mean, invstd and the fused affine (scale, shift); grid = C blocks
 __global__ void __launch_bounds__(FT) bn_fwd_finalize(const float* part, int nblk, uint64_t rows, int C, float eps,
                                                       const float* gb, float* mean, float* invstd, float* scale,
-                                                      float* shift) {
+                                                      float* shift, float* running, float momentum) {
   pdl_wait();
   const int c = blockIdx.x;
   double a, b;
@@ -132,6 +132,12 @@ __global__ void __launch_bounds__(FT) bn_fwd_finalize(const float* part, int nbl
     double g = gb[c], be = gb[C + c];
     scale[c] = (float)(g * is);
     shift[c] = (float)(be - mu * g * is);
+    if (running) {  // running statistics, unbiased variance (torch.nn.BatchNorm2d convention)
+      const double n = (double)rows;
+      const double unb = n > 1.0 ? var * n / (n - 1.0) : var;
+      running[c] = (float)((1.0 - momentum) * running[c] + momentum * mu);
+      running[C + c] = (float)((1.0 - momentum) * running[C + c] + momentum * unb);
+    }
   }
 }
 
@@ -163,6 +169,31 @@ __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __res
       mask[i] = (uint8_t)bits;
     }
   }
+}
+
+// running statistics (eval mode): rm = (1-m) rm + m mean, rv = (1-m) rv + m var_unbiased, var from invstd
+__global__ void bn_running_kernel(const float* __restrict__ mean, const float* __restrict__ invstd, float* running,
+                                  int C, double rows, float momentum, float eps) {
+  pdl_wait();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double is = invstd[c];
+  double var = 1.0 / (is * is) - (double)eps;
+  if (var < 0.0) var = 0.0;
+  const double unb = rows > 1.0 ? var * rows / (rows - 1.0) : var;
+  running[c] = (float)((1.0 - momentum) * running[c] + momentum * (double)mean[c]);
+  running[C + c] = (float)((1.0 - momentum) * running[C + c] + momentum * unb);
+}
+
+// eval-mode affine from running statistics: scale = g / sqrt(rv + eps), shift = b - rm * scale
+__global__ void bn_eval_affine_kernel(const float* __restrict__ gb, const float* __restrict__ running, int C,
+                                      float eps, float* scale, float* shift) {
+  pdl_wait();
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double sc = (double)gb[c] / sqrt((double)running[C + c] + (double)eps);
+  scale[c] = (float)sc;
+  shift[c] = (float)((double)gb[C + c] - (double)running[c] * sc);
 }
 
 // bwd pass 1: sum dz and sum dz*x per channel, dz = dy * [y > 0] (relu) or dy
@@ -273,7 +304,8 @@ uint64_t nsk_bn_workspace(uint64_t rows, int C) {
 }
 
 int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, float* invstd, uint64_t rows, int C,
-               float eps, int relu, const void* residual, void* relu_mask, float* ws, void* stream) {
+               float eps, int relu, const void* residual, void* relu_mask, float* running, float momentum, float* ws,
+               void* stream) {
   int rc = check(rows, C, x, residual);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -284,7 +316,7 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
   nsk::launch_pdl(bn_stats_kernel, nb, BT, smem, st, (const __nv_bfloat16*)x, rows, C, part);
-  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift, running, momentum);
   const uint64_t nv = rows * (uint64_t)C / 8;
   nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
                                                         shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
@@ -296,18 +328,44 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
 // no statistics pass over x
 int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const float* gamma_beta, void* y,
                         float* mean, float* invstd, uint64_t rows, int C, float eps, int relu, const void* residual,
-                        void* relu_mask, float* ws, void* stream) {
+                        void* relu_mask, float* running, float momentum, float* ws, void* stream) {
   int rc = check(rows, C, x, residual);
   if (rc) return rc;
   if (nparts < 1) return nsk::set_error(NSK_ERR_SHAPE, "batchnorm: no statistics partials");
   cudaStream_t st = (cudaStream_t)stream;
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
-  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift);
+  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift, running, momentum);
   const uint64_t nv = rows * (uint64_t)C / 8;
   nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
                                                         shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd_partials");
+  return NSK_OK;
+}
+
+// running-statistics update from a training-mode forward's mean / invstd (momentum convention of
+// torch.nn.BatchNorm2d: new = (1 - m) * old + m * batch, unbiased batch variance)
+int nsk_bn_running_update(const float* mean, const float* invstd, float* running, uint64_t rows, int C,
+                          float momentum, float eps, void* stream) {
+  nsk::launch_pdl(bn_running_kernel, (C + 127) / 128, 128, 0, (cudaStream_t)stream, mean, invstd, running, C,
+                  (double)rows, momentum, eps);
+  NSK_LAUNCH_CHECK("bn_running_update");
+  return NSK_OK;
+}
+
+// inference forward: y = relu(x * g / sqrt(rv + eps) + b - rm * g / sqrt(rv + eps) [+ residual])
+int nsk_bn_fwd_eval(const void* x, const float* gamma_beta, const float* running, void* y, uint64_t rows, int C,
+                    float eps, int relu, const void* residual, float* ws, void* stream) {
+  int rc = check(rows, C, x, residual);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  float* scale = ws + (size_t)MAXBLK * 2 * C;
+  float* shift = scale + C;
+  nsk::launch_pdl(bn_eval_affine_kernel, (C + 127) / 128, 128, 0, st, gamma_beta, running, C, eps, scale, shift);
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+                  (const __nv_bfloat16*)residual, scale, shift, (__nv_bfloat16*)y, (uint8_t*)nullptr, rows, C, relu);
+  NSK_LAUNCH_CHECK("bn_fwd_eval");
   return NSK_OK;
 }
 

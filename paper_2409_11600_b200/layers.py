@@ -13,6 +13,7 @@ optimizer). Gradients always take the dtype of the tensor they belong to.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 
 import numpy as np
 
@@ -185,16 +186,34 @@ def _r_conv2d(node, g, pool, sinks):
 # --- batchnorm (+ residual, + relu) ---------------------------------------------------------------
 
 def conv_bn(x: Tensor, w: Tensor, gb: Tensor, stride: int, pad: int, pool: Pool, relu: bool = False,
-            residual: Tensor | None = None, layout: str = "nhwc") -> Tensor:
-    """conv2d followed by batchnorm (two recorded ops, same gradients); the conv kernel emits the BN
-    channel statistics so the normalisation reads its input once."""
-    return batchnorm(conv2d(x, w, stride, pad, pool, layout=layout, bn_stats=True), gb, pool, relu=relu,
-                     residual=residual)
+            residual: Tensor | None = None, layout: str = "nhwc", training: bool = True) -> Tensor:
+    """conv2d followed by batchnorm (two recorded ops, same gradients); in training the conv kernel emits the
+    BN channel statistics so the normalisation reads its input once."""
+    return batchnorm(conv2d(x, w, stride, pad, pool, layout=layout, bn_stats=training), gb, pool, relu=relu,
+                     residual=residual, training=training)
+
+
+_RUNNING: "weakref.WeakKeyDictionary[Tensor, Buffer]" = weakref.WeakKeyDictionary()
+BN_MOMENTUM = 0.1
+
+
+def bn_running(gb: Tensor) -> Buffer:
+    """The running statistics [2, C] (mean row, unbiased variance row) of a BatchNorm parameter, created on
+    first use as (0, 1); training forwards update them with momentum BN_MOMENTUM, eval forwards read them."""
+    buf = _RUNNING.get(gb)
+    if buf is None:
+        c = gb.shape[1]
+        buf = Buffer(2 * c, F32)
+        buf.upload(np.concatenate([np.zeros(c, np.float32), np.ones(c, np.float32)]))
+        _RUNNING[gb] = buf
+    return buf
 
 
 def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: Tensor | None = None,
-              eps: float = 1e-5) -> Tensor:
-    """Training-mode batch norm over N*H*W per channel, gamma_beta = [2, C]; optional residual add and ReLU."""
+              eps: float = 1e-5, training: bool = True) -> Tensor:
+    """Batch norm over N*H*W per channel, gamma_beta = [2, C]; optional residual add and ReLU. Training mode
+    normalises with the batch statistics (and updates the running ones); eval mode (``training=False``)
+    with the running statistics and records nothing for backward."""
     if x.dtype != BF16:
         raise NskTypeError("batchnorm expects a bf16 NHWC activation")
     c = x.shape[-1]
@@ -206,6 +225,15 @@ def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: T
     lib = _lib.lib()
     st = _lib.stream()
     y = empty_tensor(pool, x.shape, BF16)
+    running = bn_running(gb)
+    if not training:
+        ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
+        check(lib.nsk_bn_fwd_eval(x.ptr, gb.ptr, running.ptr, y.ptr, rows, c, float(eps), int(relu),
+                                  None if residual is None else residual.ptr, ws.ptr, st))
+        if x.bn_partials is not None:
+            release_tensor(pool, x.bn_partials[0])
+            x.bn_partials = None
+        return y
     mean = _internal_tensor(empty_tensor(pool, (c,)))
     invstd = _internal_tensor(empty_tensor(pool, (c,)))
     ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
@@ -216,12 +244,12 @@ def batchnorm(x: Tensor, gb: Tensor, pool: Pool, relu: bool = False, residual: T
     parts = x.bn_partials
     if parts is not None:
         check(lib.nsk_bn_fwd_partials(parts[0].ptr, parts[1], x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c,
-                                      float(eps), int(relu), rp, mp, ws.ptr, st))
+                                      float(eps), int(relu), rp, mp, running.ptr, float(BN_MOMENTUM), ws.ptr, st))
         release_tensor(pool, parts[0])
         x.bn_partials = None
     else:
         check(lib.nsk_bn_fwd(x.ptr, gb.ptr, y.ptr, mean.ptr, invstd.ptr, rows, c, float(eps), int(relu), rp, mp,
-                             ws.ptr, st))
+                             running.ptr, float(BN_MOMENTUM), ws.ptr, st))
     saved = (x, gb, mean, invstd) + ((mask,) if relu else ())
     record("batchnorm", y, x, gb, residual, saved=saved, attrs={"relu": relu, "rows": rows, "c": c})
     return y

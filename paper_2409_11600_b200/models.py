@@ -98,22 +98,22 @@ class ResNet18:
     def num_params(self) -> int:
         return sum(t.numel for _n, t in self.s.param_group.params)
 
-    def forward(self, x_nchw: Tensor | None = None, x_nhwc: Tensor | None = None) -> Tensor:
+    def forward(self, x_nchw: Tensor | None = None, x_nhwc: Tensor | None = None, train: bool = True) -> Tensor:
         pool, push = self.s.pool, self.s.push_named
         if x_nhwc is not None:
             stem = layers.conv2d(x_nhwc, self.stem_w, 1, 1, pool)
         else:  # host-layout batch: the NCHW->NHWC change is fused into the stem's im2col gather
             stem = layers.conv2d(x_nchw, self.stem_w, 1, 1, pool, layout="nchw")
-        h = layers.batchnorm(stem, self.stem_bn, pool, relu=True)
+        h = layers.batchnorm(stem, self.stem_bn, pool, relu=True, training=train)
         push("rn.stem", h)
         for i, blk in enumerate(self.blocks):
             st = blk["stride"]
-            o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True)
+            o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True, training=train)
             if "wsc" in blk:
-                sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False)
+                sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
             else:
                 sc = h
-            h = layers.conv_bn(o, blk["w2"], blk["bn2"], 1, 1, pool, relu=True, residual=sc)
+            h = layers.conv_bn(o, blk["w2"], blk["bn2"], 1, 1, pool, relu=True, residual=sc, training=train)
             push(f"rn.block{i}", h)
         feat = layers.avgpool_global(h, pool)
         logits = nn.linear(feat, self.fc_w, self.fc_b, pool)
@@ -170,26 +170,26 @@ class ResNet50:
     def num_params(self) -> int:
         return sum(t.numel for _n, t in self.s.param_group.params)
 
-    def block(self, i: int, h: Tensor) -> Tensor:
+    def block(self, i: int, h: Tensor, train: bool = True) -> Tensor:
         """Bottleneck block i: 1x1 reduce -> BN/ReLU -> 3x3 (stride) -> BN/ReLU -> 1x1 expand -> BN (+ shortcut) -> ReLU."""
         pool = self.s.pool
         blk = self.blocks[i]
         st = blk["stride"]
-        o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True)
-        o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True)
+        o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True, training=train)
+        o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True, training=train)
         if "wsc" in blk:
-            sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False)
+            sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
         else:
             sc = h
-        return layers.conv_bn(o, blk["w3"], blk["bn3"], 1, 0, pool, relu=True, residual=sc)
+        return layers.conv_bn(o, blk["w3"], blk["bn3"], 1, 0, pool, relu=True, residual=sc, training=train)
 
-    def forward(self, x_nchw: Tensor) -> Tensor:
+    def forward(self, x_nchw: Tensor, train: bool = True) -> Tensor:
         pool, push = self.s.pool, self.s.push_named
         stem = layers.conv2d(x_nchw, self.stem_w, 2, 3, pool, layout="nchw")
-        h = layers.maxpool(layers.batchnorm(stem, self.stem_bn, pool, relu=True), 3, 2, 1, pool)
+        h = layers.maxpool(layers.batchnorm(stem, self.stem_bn, pool, relu=True, training=train), 3, 2, 1, pool)
         push("rn.stem", h)
         for i in range(len(self.blocks)):
-            h = self.block(i, h)
+            h = self.block(i, h, train)
             push(f"rn.block{i}", h)
         feat = layers.avgpool_global(h, pool)
         logits = nn.linear(feat, self.fc_w, self.fc_b, pool)

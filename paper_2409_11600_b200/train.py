@@ -261,6 +261,36 @@ class Trainer:
         # the pinned staging buffers may be overwritten by the next stage() only after this step's copies ran
         return self.run_staged()
 
+    def evaluate(self, x_host, y_host) -> tuple[float, int]:
+        """Inference pass (§8(f) 4): forward with BatchNorm in eval mode (running statistics), the loss and the
+        argmax-correct count; nothing is kept for backward (tape_clear, autodiff.py:83-95). uint8 augment
+        inputs are normalised without crop or flip (centre offsets)."""
+        from .builtins import accuracy_count
+        from .tensor import empty_tensor
+
+        s, lib, st = self.s, _lib.lib(), _lib.stream()
+        y = autodiff.make_data(s.pool, np.asarray(y_host, np.float32).reshape(-1))
+        if self.augment is None:
+            logits = self.model.forward(autodiff.make_data(s.pool, np.asarray(x_host, np.float32)), train=False)
+        else:
+            imgs = np.ascontiguousarray(x_host, dtype=np.uint8)
+            b, h, w, c = imgs.shape
+            raw = Buffer((imgs.size + 3) // 4, F32)
+            raw.upload(np.frombuffer(imgs.tobytes() + b"\0" * (-imgs.size % 4), np.float32))
+            pad = int(self.augment[0])
+            offs = Buffer(b * 3, F32)
+            offs.upload(np.tile(np.array([pad, pad, 0], np.int32), b).view(np.float32))
+            xa = empty_tensor(s.pool, (b, h, w, c), BF16)
+            check(lib.nsk_augment_crop_flip(raw.ptr, offs.ptr, xa.ptr, b, h, w, c, pad, self.aug_stats.ptr,
+                                            self.aug_stats.ptr + 4 * c, c, st))
+            logits = self.model.forward(x_nhwc=data_from_device(xa), train=False)
+        loss = nn.cross_entropy(logits, y, s.pool)
+        correct = accuracy_count(logits, y)
+        value = float(loss.item())
+        s.push_named("eval.loss", loss)
+        s.tape().clear(s.pool)
+        return value, int(correct)
+
     def step_async(self, x_host, y_host, offsets=None) -> DeviceScalar:
         """``step`` with the host->device copy on a copy stream into one of two input slots, so the copy (and
         the host-side staging) of batch i+1 overlaps the device work of batch i. Each slot has its own
