@@ -14,7 +14,7 @@ import threading
 from .errors import NskRuntimeError, NskTypeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnskb.so")
+LIB_PATH = os.environ.get("NSK_LIB") or os.path.join(_HERE, "libnskb.so")  # NSK_LIB: A/B builds (tools/)
 
 F32, BF16 = 0, 1
 DTYPE_SIZE = {F32: 4, BF16: 2}

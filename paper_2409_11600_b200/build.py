@@ -15,15 +15,17 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(HERE, "libnskb.so")
+# NSK_BUILD_TAG / NSK_CFLAGS_EXTRA: side builds of compile-time variants for A/B timing (abl/libnskb_<tag>.so)
+_TAG = os.environ.get("NSK_BUILD_TAG", "")
+OBJ = os.path.join(ROOT, "build", "obj" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(ROOT, "abl", f"libnskb_{_TAG}.so") if _TAG else os.path.join(HERE, "libnskb.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
-]
+] + os.environ.get("NSK_CFLAGS_EXTRA", "").split()
 LDFLAGS = ["-shared", "-lcudart", "-l:libnccl.so.2"]
 
 
@@ -55,6 +57,7 @@ def _compile(src: str, hdr_mtime: float, verbose: bool) -> str:
 
 def build(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdr = _headers_mtime()
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:

@@ -59,7 +59,8 @@ struct UmmaProb {
   signed char gdw[4][kMaxTaps], gdhmin[4][kMaxTaps], gnt[4][kMaxTaps];
   signed char gdh[4][kMaxTaps][3], gw[4][kMaxTaps][3];
   int ext_rows;  // rows of the A box in rr mode (Ht + dh range)
-  int probe;     // diagnostics (env NSK_PROBE): bit0 skip MMAs, bit1 skip stores, bit2 skip B loads
+  int probe;     // diagnostics (env NSK_PROBE): bit0 skip MMAs, bit1 skip stores, bit2 skip B loads,
+                 // bit4 no A loads in weight-resident mode, bit5 accumulator never read
   // im2col-mode A operand (any output width): the tile's first pixel sits at bounding-box position
   // (lw + j*cs, lh + i*cs, n) and every tap is an unsigned im2col offset (tdw - lw, tdh - lh)
   int i2c, lw, lh;
@@ -69,12 +70,15 @@ struct UmmaProb {
   // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
   // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
   float* stats;
+  int wres;    // weight-resident row-reuse (see Smem WRES)
+  int rr_fast;  // row-reuse 3x3 on 32-wide rows, taps t = 0..2 at row offsets t (1: fprop, 2: dgrad) or 2 - t
+                // (4: fprop, 3: dgrad): the MMA issuer uses immediate descriptor offsets
+  int asplit;  // WRES: each stage's A box is asplit row bands, one per producer warp (more boxes in flight)
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
 constexpr int kStgPitch = 64;          // epilogue staging: dense 32 x 32 bf16 blocks (TMA-store source)
 constexpr int kStgBytes = 32 * kStgPitch;
-constexpr int kProducers = 3;          // TMA issuing threads (warps 0, 2, 3)          // epilogue staging row pitch (64 B of bf16 + 16 B pad)
 
 template <int ESZ>
 struct KT {
@@ -83,14 +87,17 @@ struct KT {
   static constexpr int UK = 32 / ESZ;   // UMMA K per instruction (16 bf16 / 8 tf32)
 };
 
-template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4>
+// WRES: weight-resident row-reuse conv (one 64-channel chunk, 3x3, N = BN): all 9 filter taps are loaded once
+// per CTA into a resident region and the ring stages carry only the row-extended A boxes.
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false>
 struct Smem {
   static constexpr int A_BYTES = RR ? kRRMaxA : 128 * 128;
-  static constexpr int B1_BYTES = BN * 128;               // one tap's B tile
-  static constexpr int B_BYTES = B1_BYTES * (RR ? 3 : 1);  // rr: up to 3 taps per column group
+  static constexpr int B1_BYTES = BN * 128;                                // one tap's B tile
+  static constexpr int B_BYTES = WRES ? 0 : B1_BYTES * (RR ? 3 : 1);      // rr: up to 3 taps per column group
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 4) + 16 + 127) / 128 * 128;  // TMA-store source
+  static constexpr int W_OFF = STAGES * STAGE_BYTES;                      // resident filter taps (WRES)
+  static constexpr int BAR_OFF = W_OFF + (WRES ? 9 * B1_BYTES : 0);
+  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 5) + 16 + 127) / 128 * 128;  // TMA-store source
   // staging buffers per epilogue warp: double-buffered with 8 warps (one CTA per SM anyway); single with 4 so
   // the 64/128-wide tiles keep two CTAs per SM
   static constexpr int NSTG = EPI == 8 ? 2 : 1;
@@ -115,6 +122,25 @@ __device__ __forceinline__ uint4 bf16x8_axpby(uint4 old, float beta, uint4 v) {
 // named barriers: one per epilogue warpgroup (ids 1, 2; 128 threads), one over all epilogue warps (id 3)
 __device__ __forceinline__ void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
 __device__ __forceinline__ void epi_bar_all(int threads) { asm volatile("bar.sync 3, %0;" ::"r"(threads) : "memory"); }
+// MMA gate: the gate warp waits on the mbarriers and releases the MMA warp through named barriers 4..4+STAGES-1
+// (stage s full) and 8, 9 (accumulator a drained), 64 threads each (gate warp arrives, MMA warp syncs)
+constexpr int kBarFull = 4, kBarAcc = 8;
+#ifdef NSK_NO_GATE
+constexpr bool kNoGate = true;
+#else
+constexpr bool kNoGate = false;
+#endif
+// Two co-resident CTAs per SM hide each other's MMA-issue gaps; the gate warp only pays off for one CTA per SM
+// (measured: -3 us on the weight-resident 64-channel conv, +1-2% on the two-per-SM configurations).
+template <class S>
+struct Launch {
+  static constexpr bool kTwoPerSM = 2 * S::TOTAL + 8192 <= 227 * 1024;
+  static constexpr bool kGate = !kTwoPerSM && !kNoGate;
+  template <int EPI>
+  static constexpr int threads() { return 128 + 32 * EPI + (kGate ? 32 : 0); }
+};
+__device__ __forceinline__ void gate_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void gate_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1, int c2) {
   asm volatile(
@@ -122,6 +148,31 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
           "r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// One 64-element K slab (4 UMMA k-steps) with compile-time descriptor steps: the offsets fold into immediates
+// of the uniform-register descriptor adds, so the issuing warp runs ~2 instructions per MMA.
+template <int AOFF0, int BOFF0, int AST, int BST, bool TF32>
+__device__ __forceinline__ void mma_slab_at(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, bool acc) {
+  umma_off<((AOFF0 + 0 * AST) >> 4), ((BOFF0 + 0 * BST) >> 4), TF32>(d, ad, bd, idesc, acc ? 1u : 0u);
+  umma_off<((AOFF0 + 1 * AST) >> 4), ((BOFF0 + 1 * BST) >> 4), TF32>(d, ad, bd, idesc, 1u);
+  umma_off<((AOFF0 + 2 * AST) >> 4), ((BOFF0 + 2 * BST) >> 4), TF32>(d, ad, bd, idesc, 1u);
+  umma_off<((AOFF0 + 3 * AST) >> 4), ((BOFF0 + 3 * BST) >> 4), TF32>(d, ad, bd, idesc, 1u);
+}
+
+// One 64-element K slab (4 UMMA k-steps) with compile-time descriptor steps (offsets are PTX immediates).
+template <int AST, int BST, bool TF32>
+__device__ __forceinline__ void mma_slab(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, bool acc) {
+  mma_slab_at<0, 0, AST, BST, TF32>(d, ad, bd, idesc, acc);
+}
+
+// Row-reuse column group of a 32-wide image: taps t = 0..2 read A shifted by whole rows (4 KB) in ascending
+// (DESC = false) or descending order, B at tap t of the strided box; BST = B k-step (32: K-major, 2048: MN-major).
+template <int B1, int BST, bool DESC>
+__device__ __forceinline__ void mma_rr32(uint32_t d, uint64_t ad, uint64_t bd, uint32_t idesc, bool acc) {
+  mma_slab_at<(DESC ? 2 : 0) * 4096, 0 * B1, 32, BST, false>(d, ad, bd, idesc, acc);
+  mma_slab_at<1 * 4096, 1 * B1, 32, BST, false>(d, ad, bd, idesc, true);
+  mma_slab_at<(DESC ? 0 : 2) * 4096, 2 * B1, 32, BST, false>(d, ad, bd, idesc, true);
 }
 
 struct Unit {
@@ -156,35 +207,39 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 // overlap the MMAs of unit j+1.
 // EPI epilogue warps (4 or 8): with 8, two warpgroups take alternate 32-column chunks of each tile, doubling the
 // TMEM-drain / store parallelism for the wide (BN = 256) tiles whose epilogue is the bottleneck.
-template <int BN, int ESZ, int STAGES, bool RR, int EPI>
-__global__ void __launch_bounds__(128 + 32 * EPI, 1)
+template <int BN, int ESZ, int STAGES, bool RR, int EPI, bool WRES>
+__global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::template threads<EPI>(),
+                                  Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::kTwoPerSM ? 2 : 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const UmmaProb p) {
   pdl_wait();
-  using S = Smem<BN, ESZ, STAGES, RR, EPI>;
+  using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
   using T = KT<ESZ>;
+  constexpr bool kGate = Launch<S>::kGate;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* wfull = tempty + 2;      // resident filter taps landed (WRES)
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 3);
   uint8_t* stage_base = smem + S::STG_OFF;
 
-  const int warp = threadIdx.x >> 5;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform role index
   const int lane = threadIdx.x & 31;
   const int units = p.units;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], WRES ? p.asplit : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI);  // one arrival per epilogue warp
     }
+    if (WRES) mbar_init(wfull, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -207,6 +262,12 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
   if (lane == 0 && (warp == 0 || warp == 2 || warp == 3) && prod < kProducers) {
     // ---------------- TMA producers ----------------
     int i = 0;  // global k-step counter (smem ring position)
+    if (WRES && prod == 0) {
+      mbar_expect_tx(wfull, (uint32_t)(p.ngroups[0] * 3 * S::B1_BYTES));
+      for (int g = 0; g < p.ngroups[0]; ++g) {
+        tma_load_3d(&tmB, wfull, smem + S::W_OFF + g * 3 * S::B1_BYTES, 0, 0, p.gw[0][g][0]);  // N = C = 64
+      }
+    }
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit w = decode_unit(p, u, BN);
       int n_img = 0, h_img = 0, w_img = 0;
@@ -219,9 +280,9 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
       }
       const bool half_a = (p.mode == MODE_WGRAD) && (w.m0 / 64 + 1 >= p.atoms_total);
       for (int kk = w.kb; kk < w.kb + w.nk; ++kk, ++i) {
-        if (i % kProducers != prod) continue;
+        if (!(WRES && p.asplit > 1) && i % kProducers != prod) continue;  // banded A: every warp, every stage
         const int s = i % STAGES;
-        if (i >= STAGES) mbar_wait(&empty[s], ((i / STAGES) - 1) & 1);
+        if (i >= STAGES) mbar_wait_backoff(&empty[s], ((i / STAGES) - 1) & 1);
         uint8_t* sa = smem + s * S::STAGE_BYTES;
         uint8_t* sb = sa + S::A_BYTES;
         if constexpr (RR) {
@@ -231,6 +292,17 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
           const int g = kk - chunk * ng;
           const int c0 = chunk * 64;
           const int nt = p.gnt[w.z][g];
+          if (WRES) {
+            const int rows = p.ext_rows / p.asplit, band = p.asplit > 1 ? prod : 0;
+            if (p.probe & 16) {  // diagnostics: no A traffic (MMAs on stale stages)
+              mbar_arrive(&full[s]);
+              continue;
+            }
+            mbar_expect_tx(&full[s], (uint32_t)(rows * p.Wt * 128));
+            tma_load_4d(&tmA, &full[s], sa + band * rows * p.Wt * 128, c0, w_img + p.gdw[w.z][g],
+                        h_img + p.gdhmin[w.z][g] + band * rows, n_img);
+            continue;
+          }
           mbar_expect_tx(&full[s], (uint32_t)(p.ext_rows * p.Wt * 128 + nt * S::B1_BYTES));
           tma_load_4d(&tmA, &full[s], sa, c0, w_img + p.gdw[w.z][g], h_img + p.gdhmin[w.z][g], n_img);
           if (p.bmode == BMODE_RR3 || p.bmode == BMODE_RR3T) {
@@ -317,61 +389,121 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0) {
+  } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
+    // The whole warp walks the pipeline (converged, so descriptors and ring state stay in uniform registers)
+    // and one elected lane issues: issuing from a divergent `lane == 0` branch made ptxas wrap every
+    // tcgen05.mma in a waterfall loop with vector->uniform moves, ~130 cycles per MMA instead of ~48.
     const int a_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? 0 : p.a_mn);
     const int b_mn = (p.mode == MODE_WGRAD) ? 1 : (p.mode == MODE_CONV ? (p.bmode == BMODE_DGRAD3D || p.bmode == BMODE_RR3T) : p.b_mn);
     const uint32_t idesc = make_idesc(ESZ == 2 ? 1u : 2u, (uint32_t)a_mn, (uint32_t)b_mn, 128u, (uint32_t)BN);
     const uint32_t a_lbo = a_mn ? (T::KS * 128) : 16;
     const uint32_t b_lbo = b_mn ? (T::KS * 128) : 16;
-    const uint32_t a_step = a_mn ? (T::UK * 128) : 32;
-    const uint32_t b_step = b_mn ? (T::UK * 128) : 32;
-    int i = 0, j = 0;
+    constexpr int MNS = T::UK * 128;  // MN-major k-step (bytes)
+    const int combo = a_mn * 2 + b_mn;
+    const bool skip_mma = p.probe & 1;
+    const int rr_fast = p.rr_fast;  // 1..4: 32-wide row-reuse groups with a fixed tap order (host-checked)
+    // ring position and phase are carried incrementally; the shared-memory descriptors are built once per stage
+    // and advanced by adding (byte offset >> 4) to their 14-bit address field
+    const uint32_t smem0 = smem_u32(smem);
+    int s = 0;
+    uint32_t ph = 0;
+    int j = 0;
+    if (WRES) mbar_wait(wfull, 0);
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = decode_unit(p, u, BN);
       const int acc = j & 1;
-      if (j >= 2) mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+      if (j >= 2) {
+        if constexpr (kGate)
+          gate_sync(kBarAcc + acc);
+        else
+          mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+      }
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int k = 0; k < w.nk; ++k, ++i) {
-        const int s = i % STAGES;
-        mbar_wait(&full[s], (i / STAGES) & 1);
+      int g = 0;  // RR column group of k-step k
+      for (int k = 0; k < w.nk; ++k) {
+        if constexpr (kGate)
+          gate_sync(kBarFull + s);
+        else
+          mbar_wait(&full[s], ph);
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * S::STAGE_BYTES);
-        const uint32_t sb = sa + S::A_BYTES;
-        if constexpr (RR) {
-          const int ng = p.ngroups[w.z];
-          const int g = k % ng;
-          const int nt = p.gnt[w.z][g];
-          for (int t = 0; t < nt; ++t) {
-            // tap view: rows shifted by (dh - dh_min) whole image rows of Wt pixels
-            const uint32_t at = sa + (uint32_t)((p.gdh[w.z][g][t] - p.gdhmin[w.z][g]) * p.Wt * 128);
-            const uint32_t bt = sb + t * S::B1_BYTES;
+        const uint32_t sa = smem0 + s * S::STAGE_BYTES;
+        const uint64_t ad0 = sdesc_sw128(sa, a_lbo, 1024);
+        const uint64_t bd0 =
+            sdesc_sw128(WRES ? smem0 + S::W_OFF + g * 3 * S::B1_BYTES : sa + S::A_BYTES, b_lbo, 1024);
+        if (elect_one()) {
+          if constexpr (RR) {
+            constexpr int B1 = S::B1_BYTES;
+            if (rr_fast == 1) {
+              mma_rr32<B1, 32, false>(d_tmem, ad0, bd0, idesc, k > 0);
+            } else if (rr_fast == 2) {
+              mma_rr32<B1, 2048, false>(d_tmem, ad0, bd0, idesc, k > 0);
+            } else if (rr_fast == 3) {
+              mma_rr32<B1, 2048, true>(d_tmem, ad0, bd0, idesc, k > 0);
+            } else if (rr_fast == 4) {
+              mma_rr32<B1, 32, true>(d_tmem, ad0, bd0, idesc, k > 0);
+            } else {
+              const uint32_t b_step = b_mn ? MNS : 32;
+              const int nt = p.gnt[w.z][g];
+              for (int t = 0; t < nt; ++t) {
+                // tap view: rows shifted by (dh - dh_min) whole image rows of Wt pixels
+                const uint32_t aoff = (uint32_t)((p.gdh[w.z][g][t] - p.gdhmin[w.z][g]) * p.Wt * 128);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint64_t ad = sdesc_sw128(at + q * a_step, a_lbo, 1024);
-              const uint64_t bd = sdesc_sw128(bt + q * b_step, b_lbo, 1024);
-              umma_bf16(d_tmem, ad, bd, idesc, (k > 0 || t > 0 || q > 0) ? 1u : 0u);
+                for (int q = 0; q < 4; ++q)
+                  umma_bf16(d_tmem, ad0 + ((aoff + q * 32) >> 4), bd0 + ((uint32_t)(t * B1 + q * b_step) >> 4),
+                            idesc, (k > 0 || t > 0 || q > 0) ? 1u : 0u);
+              }
             }
+          } else if (!skip_mma) {
+            constexpr bool TF = ESZ == 4;
+            if (combo == 0)
+              mma_slab<32, 32, TF>(d_tmem, ad0, bd0, idesc, k > 0);
+            else if (combo == 1)
+              mma_slab<32, MNS, TF>(d_tmem, ad0, bd0, idesc, k > 0);
+            else if (combo == 2)
+              mma_slab<MNS, 32, TF>(d_tmem, ad0, bd0, idesc, k > 0);
+            else
+              mma_slab<MNS, MNS, TF>(d_tmem, ad0, bd0, idesc, k > 0);
           }
-          umma_commit(&empty[s]);
-          continue;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint64_t ad = sdesc_sw128(sa + q * a_step, a_lbo, 1024);
-          const uint64_t bd = sdesc_sw128(sb + q * b_step, b_lbo, 1024);
-          if (p.probe & 1) continue;
-          if (ESZ == 2)
-            umma_bf16(d_tmem, ad, bd, idesc, (k > 0 || q > 0) ? 1u : 0u);
-          else
-            umma_tf32(d_tmem, ad, bd, idesc, (k > 0 || q > 0) ? 1u : 0u);
-        }
         umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (RR && ++g == p.ngroups[w.z]) g = 0;
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
-      umma_commit(&tfull[acc]);
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
     }
-  } else if (warp >= 4) {
+  } else if (kGate && warp == 4 + EPI) {
+    // ---------------- MMA gate ----------------
+    // Any shared-memory read by the MMA warp (an mbarrier try_wait, even on a completed phase) waits for the
+    // tensor pipe's queued operand reads and leaves it idle for ~130 cycles per stage -- a third of the time
+    // with 64-wide MMAs (tools/mma_gap.cu). This warp does the mbarrier waits in the MMA warp's order and
+    // releases it through named barriers, which cost the MMA warp nothing.
+    int s = 0;
+    uint32_t phase = 0;
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = decode_unit(p, u, BN);
+      const int acc = j & 1;
+      if (j >= 2) {
+        mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+        gate_arrive(kBarAcc + acc);
+      }
+      for (int k = 0; k < w.nk; ++k) {
+        mbar_wait(&full[s], phase);
+        gate_arrive(kBarFull + s);
+        if (++s == STAGES) {
+          s = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + EPI) {
     // ---------------- epilogue ----------------
     const int q = warp & 3;         // TMEM lane quarter (a warp may only access lanes 32*(warp%4) .. +31)
     const int eg = (warp - 4) >> 2;  // epilogue warpgroup: chunks eg, eg + EPI/4, ...
@@ -388,7 +520,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = decode_unit(p, u, BN);
       const int acc = j & 1;
-      mbar_wait(&tfull[acc], (j >> 1) & 1);
+      mbar_wait_backoff(&tfull[acc], (j >> 1) & 1);
       tc_fence_after();
       const int m = w.m0 + r;
       const bool row_ok = m < p.M;
@@ -413,6 +545,7 @@ __global__ void __launch_bounds__(128 + 32 * EPI, 1)
 #pragma unroll 1
       for (int c = eg; c < nchunks; c += EPI / 4) {
         uint32_t v[32];
+        if (p.probe & 32) continue;  // diagnostics: accumulator never read
         if (w.nk > 0) {
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
           tmem_ld_wait();
@@ -646,11 +779,11 @@ int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
   return NSK_OK;
 }
 
-template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4>
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false>
 int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, UmmaProb p, cudaStream_t st,
                 int* grid_out) {
-  using S = Smem<BN, ESZ, STAGES, RR, EPI>;
-  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI>;
+  using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
+  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES>;
   const int smem = S::TOTAL + (p.stats ? (2 * p.N + EPI * 64) * (int)sizeof(float) : 0);
   if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
   static int configured = 0;
@@ -664,7 +797,7 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  nsk::launch_pdl(kern, grid, 128 + 32 * EPI, smem, st, a, b, c, p);
+  nsk::launch_pdl(kern, grid, Launch<S>::template threads<EPI>(), smem, st, a, b, c, p);
   NSK_LAUNCH_CHECK("umma_kernel");
   return NSK_OK;
 }
@@ -681,8 +814,13 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
   if (p.rr) {
     if constexpr (ESZ == 2) {
       switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
-        case 64:
+        case 64: {
+          // one 64-channel chunk, N = 64, 3x3 in strided tap boxes: keep all 9 taps resident (the ring then
+          // moves only A; re-fetching the 72 KB filter per tile was half the L2->smem traffic)
+          if (p.wres && nt == 1 && nz == 1) return launch_umma<64, 2, 4, true, 8, true>(a, b, c, p, st, grid_out);
+          if (p.wres) return nsk::set_error(NSK_ERR_UNSUPPORTED, "weight-resident conv needs a single 64-wide tile");
           return launch_umma<64, 2, 2, true>(a, b, c, p, st, grid_out);
+        }
         case 128:
           return launch_umma<128, 2, 2, true>(a, b, c, p, st, grid_out);
       }
@@ -842,7 +980,33 @@ void try_rr3(UmmaProb& p, CUtensorMap* mb, const NskConvDesc* d, const void* w, 
       NSK_OK) {
     *mb = m;
     p.bmode = mode;
+    if (p.Wt == 32) {
+      bool asc = true, desc = true;
+      for (int g = 0; g < 3; ++g)
+        for (int t = 0; t < 3; ++t) {
+          asc = asc && p.gdh[0][g][t] - p.gdhmin[0][g] == t;
+          desc = desc && p.gdh[0][g][t] - p.gdhmin[0][g] == 2 - t;
+        }
+      const char* ef = getenv("NSK_RR_FAST");
+      if (!(ef && ef[0] == '0'))
+        p.rr_fast = asc ? (mode == BMODE_RR3 ? 1 : 2) : (desc ? (mode == BMODE_RR3 ? 4 : 3) : 0);
+    }
   }
+}
+
+// Weight-resident row-reuse (Smem WRES): a 3x3 over one 64-channel chunk with 64 outputs whose taps come in
+// strided boxes. The A map is re-encoded as row bands so the three producer warps each keep a box in flight
+// per stage (one 4-D box per issuing thread is latency-bound at ~15 B/clk/SM, tools/tma_rate.cu).
+void try_wres(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int Win, int Cin, int Nout) {
+  const char* env = getenv("NSK_WRES");
+  if (env && env[0] == '0') return;
+  if (!(p.bmode == BMODE_RR3 || p.bmode == BMODE_RR3T) || p.cchunks != 1 || Nout != 64 || p.ngroups[0] != 3) return;
+  const char* es = getenv("NSK_ASPLIT");
+  int split = es ? atoi(es) : 3;
+  if (split != 3 || p.ext_rows % 3) split = 1;  // one band per producer warp (three with a 4-stage ring)
+  if (split > 1 && nhwc_map(ma, act, N, Hin, Win, Cin, 64, p.Wt, p.ext_rows / split, 1, 1)) split = 1;
+  p.asplit = split;
+  p.wres = 1;
 }
 
 int check_desc(const NskConvDesc* d) {
@@ -983,6 +1147,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
     if ((rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 128))) return rc;
   } else if (try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN)) {
     try_rr3(p, &mb, d, w, BN, BMODE_RR3);
+    try_wres(p, &ma, x, d->N, d->H, d->W, d->C, d->K);
   }
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   if (stats) {
@@ -1079,7 +1244,10 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   if (i2c) {
     if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls, 128))) return rc;
   } else if (ncls == 1 && try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN)) {
-    if (BN == 64) try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
+    if (BN == 64) {
+      try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
+      try_wres(p, &ma, dy, d->N, P, Q, d->K, d->C);
+    }
   }
   CUtensorMap mc;
   const char* red = getenv("NSK_TMA_REDUCE");
