@@ -694,42 +694,59 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
 }
 
 // wgrad split-K reduction: ws[split][N][Mpad] (rows = cout, cols = (tap, cin)) -> dw[cout][tap][cin] (+= if beta).
-// Both sides are contiguous in the (tap, cin) index: fully coalesced, fixed summation order.
-__global__ void wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M, int N, float* dw,
-                                    float beta) {
+// Both sides are contiguous in the (tap, cin) index. Block (32, SL): 32 float4 columns x SL split slices (slice s
+// takes splits s, s+SL, ...), slices combined in slice order: deterministic. Small outputs with many splits (576 x 64
+// is only 9216 float4 columns) use 8 slices for 8x the loads in flight; large outputs one.
+template <int kWgSlices>
+__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float* __restrict__ ws, int splits, int Mpad, int M,
+                                                           int N, float* dw, float beta) {
   pdl_wait();
-  // 4 consecutive (tap, cin) entries per thread (M % 4 == 0 since Cin % 64 == 0), splits folded in order
+  constexpr int XT = 256 / kWgSlices;
+  __shared__ float4 red[kWgSlices][XT];
   const long long total4 = (long long)M * N / 4;
+  const long long i4 = (long long)blockIdx.x * XT + threadIdx.x;
+  const int sl = threadIdx.y;
   const long long plane = (long long)N * Mpad;
-  for (long long i4 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i4 < total4;
-       i4 += (long long)gridDim.x * blockDim.x) {
-    const long long idx = i4 * 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  long long idx = 0;
+  if (i4 < total4) {
+    idx = i4 * 4;
     const int n = (int)(idx / M);
     const int m = (int)(idx - (long long)n * M);
     const float* src = ws + (long long)n * Mpad + m;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int s = 0;
-    for (; s + 4 <= splits; s += 4) {
-      float4 v0 = __ldg((const float4*)(src + (s + 0) * plane));
-      float4 v1 = __ldg((const float4*)(src + (s + 1) * plane));
-      float4 v2 = __ldg((const float4*)(src + (s + 2) * plane));
-      float4 v3 = __ldg((const float4*)(src + (s + 3) * plane));
+    int s = sl;
+    for (; s + 3 * kWgSlices < splits; s += 4 * kWgSlices) {
+      const float4 v0 = __ldg((const float4*)(src + (s + 0 * kWgSlices) * plane));
+      const float4 v1 = __ldg((const float4*)(src + (s + 1 * kWgSlices) * plane));
+      const float4 v2 = __ldg((const float4*)(src + (s + 2 * kWgSlices) * plane));
+      const float4 v3 = __ldg((const float4*)(src + (s + 3 * kWgSlices) * plane));
       acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
       acc.x += v1.x; acc.y += v1.y; acc.z += v1.z; acc.w += v1.w;
       acc.x += v2.x; acc.y += v2.y; acc.z += v2.z; acc.w += v2.w;
       acc.x += v3.x; acc.y += v3.y; acc.z += v3.z; acc.w += v3.w;
     }
-    for (; s < splits; ++s) {
-      float4 v = __ldg((const float4*)(src + s * plane));
+    for (; s < splits; s += kWgSlices) {
+      const float4 v = __ldg((const float4*)(src + s * plane));
       acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
     }
-    float4* d = (float4*)(dw + idx);
-    if (beta != 0.f) {
-      float4 o = *d;
-      acc.x += beta * o.x; acc.y += beta * o.y; acc.z += beta * o.z; acc.w += beta * o.w;
-    }
-    *d = acc;
   }
+  if (kWgSlices > 1) {
+    red[sl][threadIdx.x] = acc;
+    __syncthreads();
+  }
+  if (sl != 0 || i4 >= total4) return;
+  float4 t = acc;
+#pragma unroll
+  for (int k = 1; k < kWgSlices; ++k) {
+    const float4 v = red[k][threadIdx.x];
+    t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+  }
+  float4* d = (float4*)(dw + idx);
+  if (beta != 0.f) {
+    const float4 o = *d;
+    t.x += beta * o.x; t.y += beta * o.y; t.z += beta * o.z; t.w += beta * o.w;
+  }
+  *d = t;
 }
 
 // split-K GEMM fold: C[m, n] = sum_z ws[z][m][n] (+ bias[n]) (+ beta * C[m, n]), fp32 or bf16 out
@@ -1352,8 +1369,12 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   long long total = (long long)M * d->K;
   if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: dw and workspace must be 16-byte aligned");
-  nsk::launch_pdl(wgrad_reduce_kernel, nsk::grid_for(total / 4, 256), 256, 0, (cudaStream_t)stream, (const float*)ws, splits, Mpad,
-                                                                                       M, d->K, dw, beta);
+  if (total / 4 < (long long)nsk::sm_count() * 512 && splits >= 16)
+    nsk::launch_pdl(wgrad_reduce_kernel<8>, (unsigned)((total / 4 + 31) / 32), dim3(32, 8), 0, (cudaStream_t)stream,
+                    (const float*)ws, splits, Mpad, M, d->K, dw, beta);
+  else
+    nsk::launch_pdl(wgrad_reduce_kernel<1>, (unsigned)((total / 4 + 255) / 256), dim3(256, 1), 0, (cudaStream_t)stream,
+                    (const float*)ws, splits, Mpad, M, d->K, dw, beta);
   NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
   return NSK_OK;
 }
