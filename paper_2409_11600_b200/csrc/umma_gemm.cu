@@ -40,6 +40,7 @@ struct UmmaProb {
   int ntaps[4];
   signed char tdh[4][kMaxTaps], tdw[4][kMaxTaps], tw[4][kMaxTaps];
   int os, Hd, Wd;   // output pixel mapping: (n, i*os+ph, j*os+pw) in an [Hd x Wd] grid
+  signed char cph[4], cpw[4];  // (ph, pw) of class z (dgrad parity classes; classes without taps may be dropped)
   int atoms_total;  // wgrad: M / 64
   int cin_atoms;    // wgrad: Cin / 64
   // epilogue
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         const int rem = m - nn * hw;
         const int ii = rem / p.Wo;
         const int jj = rem - ii * p.Wo;
-        const int ph = w.z >> 1, pw = w.z & 1;
+        const int ph = p.cph[w.z], pw = p.cpw[w.z];
         const long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
         row_off = pix * p.ldc;
       } else {
@@ -1213,7 +1214,15 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   const int Hg = d->H / st, Wg = d->W / st;
   int Wt = 0, Ht = 0, Nt = 0;
   const bool i2c = !pixel_tile(Wg, Hg, 128, &Wt, &Ht, &Nt) || force_i2c();
-  const int BN = pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, st * st);
+  int active = 0;  // parity classes with at least one tap
+  for (int c = 0; c < st * st; ++c) {
+    bool any = false;
+    for (int r = 0; r < d->R; ++r)
+      for (int q = 0; q < d->S; ++q)
+        any = any || (((st == 2 ? (c >> 1) : 0) + d->pad - r) % st == 0 && ((st == 2 ? (c & 1) : 0) + d->pad - q) % st == 0);
+    active += any;
+  }
+  const int BN = pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, beta == 1.f ? active : st * st);
   CUtensorMap ma, mb;
   if (!i2c && (rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
   {
@@ -1251,15 +1260,37 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
         ++t;
       }
     p.ntaps[c] = t;
+    p.cph[c] = (signed char)ph;
+    p.cpw[c] = (signed char)pw;
   }
-  // map classes to (ph, pw) = (c>>1, c&1) even when stride == 1 (single class 0)
+  // accumulating into an existing gradient: a parity class without taps (1x1 stride 2: three of four) adds
+  // nothing, so its work units are dropped instead of re-writing dx unchanged
+  int ncls_run = ncls;
+  if (beta == 1.f && ncls > 1) {
+    ncls_run = 0;
+    for (int c = 0; c < ncls; ++c) {
+      if (p.ntaps[c] == 0) continue;
+      if (ncls_run != c) {
+        p.ntaps[ncls_run] = p.ntaps[c];
+        for (int t = 0; t < p.ntaps[c]; ++t) {
+          p.tdh[ncls_run][t] = p.tdh[c][t];
+          p.tdw[ncls_run][t] = p.tdw[c][t];
+          p.tw[ncls_run][t] = p.tw[c][t];
+        }
+        p.cph[ncls_run] = p.cph[c];
+        p.cpw[ncls_run] = p.cpw[c];
+      }
+      ++ncls_run;
+    }
+    if (ncls_run == 0) return NSK_OK;  // nothing to add
+  }
   p.os = st; p.Hd = d->H; p.Wd = d->W;
   p.out = dx;
   p.ldc = d->C;
   p.out_f32 = 0;
   p.beta = beta;
   if (i2c) {
-    if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls, 128))) return rc;
+    if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls_run, 128))) return rc;
   } else if (ncls == 1 && try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN)) {
     if (BN == 64) {
       try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
@@ -1272,8 +1303,8 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
                   out_map(&mc, dx, p.M, d->C, d->C);
   p.tma_store = ts ? (beta == 1.f ? 2 : 1) : 0;
   if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
-  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls, (cudaStream_t)stream, nullptr,
-                        ts ? &mc : nullptr);
+  return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run, (cudaStream_t)stream,
+                        nullptr, ts ? &mc : nullptr);
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {

@@ -108,11 +108,13 @@ class ResNet18:
         push("rn.stem", h)
         for i, blk in enumerate(self.blocks):
             st = blk["stride"]
-            o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True, training=train)
+            # projection shortcut recorded first: its backward then runs after conv1's and accumulates into dx,
+            # which lets the 1x1 stride-2 dgrad skip the three parity classes it has no taps for
             if "wsc" in blk:
                 sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
             else:
                 sc = h
+            o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True, training=train)
             h = layers.conv_bn(o, blk["w2"], blk["bn2"], 1, 1, pool, relu=True, residual=sc, training=train)
             push(f"rn.block{i}", h)
         feat = layers.avgpool_global(h, pool)
@@ -175,12 +177,13 @@ class ResNet50:
         pool = self.s.pool
         blk = self.blocks[i]
         st = blk["stride"]
-        o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True, training=train)
-        o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True, training=train)
+        # projection shortcut first: its (stride-2) dgrad then accumulates into dx last and skips tapless classes
         if "wsc" in blk:
             sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
         else:
             sc = h
+        o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True, training=train)
+        o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True, training=train)
         return layers.conv_bn(o, blk["w3"], blk["bn3"], 1, 0, pool, relu=True, residual=sc, training=train)
 
     def forward(self, x_nchw: Tensor, train: bool = True) -> Tensor:

@@ -490,10 +490,12 @@ def test_conv_bn_fused_statistics(session, case):
 
 
 @pytest.mark.parametrize("case", [(4, 32, 32, 64, 64, 3, 1, 1), (2, 56, 56, 256, 64, 1, 1, 0),
-                                  (4, 32, 32, 64, 128, 3, 2, 1)])
+                                  (4, 32, 32, 64, 128, 3, 2, 1), (4, 32, 32, 64, 128, 1, 2, 0),
+                                  (2, 14, 14, 128, 256, 1, 2, 0)])
 def test_conv2d_dgrad_accumulates_in_place(dev, case):
     """nsk_conv2d_dgrad_acc: dx = dgrad + dx (TMA reduce-add for stride 1, staged read-modify-write for the
-    stride-2 parity classes) -- the in-place second gradient contribution the autodiff uses."""
+    stride-2 parity classes) -- the in-place second gradient contribution the autodiff uses. 1x1 stride 2:
+    only parity class (0, 0) has a tap; the other three are dropped and must leave dx untouched."""
     import ctypes as C
 
     from paper_2409_11600_b200 import _lib
