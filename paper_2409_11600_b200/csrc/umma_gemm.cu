@@ -13,6 +13,8 @@
 // Every smem stage holds 128 bytes of K per operand row: 4 UMMA k-substeps.
 // Operands can be K-major (TMA box {128B of K, rows}) or MN-major
 // (boxes of 64 bf16 / 32 fp32 MN-elements x KS K-rows), all 128B-swizzled.
+#include <type_traits>
+
 #include "common.cuh"
 #include "../../include/nskb.h"
 
@@ -401,50 +403,52 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     const uint32_t a_lbo = a_mn ? (T::KS * 128) : 16;
     const uint32_t b_lbo = b_mn ? (T::KS * 128) : 16;
     constexpr int MNS = T::UK * 128;  // MN-major k-step (bytes)
-    const int combo = a_mn * 2 + b_mn;
-    const bool skip_mma = p.probe & 1;
-    const int rr_fast = p.rr_fast;  // 1..4: 32-wide row-reuse groups with a fixed tap order (host-checked)
-    // ring position and phase are carried incrementally; the shared-memory descriptors are built once per stage
-    // and advanced by adding (byte offset >> 4) to their 14-bit address field
+    const int rr_groups = RR ? p.ngroups[0] : 1;  // row reuse runs single-class launches only
     const uint32_t smem0 = smem_u32(smem);
-    int s = 0;
-    uint32_t ph = 0;
-    int j = 0;
     if (WRES) mbar_wait(wfull, 0);
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const Unit w = decode_unit(p, u, BN);
-      const int acc = j & 1;
-      if (j >= 2) {
-        if constexpr (kGate)
-          gate_sync(kBarAcc + acc);
-        else
-          mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
-      }
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      int g = 0;  // RR column group of k-step k
-      for (int k = 0; k < w.nk; ++k) {
-        if constexpr (kGate)
-          gate_sync(kBarFull + s);
-        else
-          mbar_wait(&full[s], ph);
+    // The loop is instantiated per MMA kind (KIND: 1..4 fixed-order 32-wide row reuse, 0 general row reuse,
+    // 10..13 one K slab with operand majors a_mn*2+b_mn, -1 no MMAs) so nothing between two MMA bursts reads
+    // parameter space or branches through a jump table. Ring position and phase are carried incrementally;
+    // the shared-memory descriptors are built once per stage and advanced by immediates.
+    auto mma_loop = [&](auto kind_c) {
+      constexpr int KIND = decltype(kind_c)::value;
+      int s = 0;
+      uint32_t ph = 0;
+      int j = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+        const Unit w = decode_unit(p, u, BN);
+        const int acc = j & 1;
+        if (j >= 2) {
+          if constexpr (kGate)
+            gate_sync(kBarAcc + acc);
+          else
+            mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+        }
         tc_fence_after();
-        const uint32_t sa = smem0 + s * S::STAGE_BYTES;
-        const uint64_t ad0 = sdesc_sw128(sa, a_lbo, 1024);
-        const uint64_t bd0 =
-            sdesc_sw128(WRES ? smem0 + S::W_OFF + g * 3 * S::B1_BYTES : sa + S::A_BYTES, b_lbo, 1024);
-        if (elect_one()) {
-          if constexpr (RR) {
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        int g = 0;  // RR column group of k-step k
+        for (int k = 0; k < w.nk; ++k) {
+          if constexpr (kGate)
+            gate_sync(kBarFull + s);
+          else
+            mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t sa = smem0 + s * S::STAGE_BYTES;
+          const uint64_t ad0 = sdesc_sw128(sa, a_lbo, 1024);
+          const uint64_t bd0 =
+              sdesc_sw128(WRES ? smem0 + S::W_OFF + g * 3 * S::B1_BYTES : sa + S::A_BYTES, b_lbo, 1024);
+          if (elect_one()) {
             constexpr int B1 = S::B1_BYTES;
-            if (rr_fast == 1) {
+            constexpr bool TF = ESZ == 4;
+            if constexpr (KIND == 1) {
               mma_rr32<B1, 32, false>(d_tmem, ad0, bd0, idesc, k > 0);
-            } else if (rr_fast == 2) {
+            } else if constexpr (KIND == 2) {
               mma_rr32<B1, 2048, false>(d_tmem, ad0, bd0, idesc, k > 0);
-            } else if (rr_fast == 3) {
+            } else if constexpr (KIND == 3) {
               mma_rr32<B1, 2048, true>(d_tmem, ad0, bd0, idesc, k > 0);
-            } else if (rr_fast == 4) {
+            } else if constexpr (KIND == 4) {
               mma_rr32<B1, 32, true>(d_tmem, ad0, bd0, idesc, k > 0);
-            } else {
+            } else if constexpr (KIND == 0) {
               const uint32_t b_step = b_mn ? MNS : 32;
               const int nt = p.gnt[w.z][g];
               for (int t = 0; t < nt; ++t) {
@@ -455,29 +459,46 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
                   umma_bf16(d_tmem, ad0 + ((aoff + q * 32) >> 4), bd0 + ((uint32_t)(t * B1 + q * b_step) >> 4),
                             idesc, (k > 0 || t > 0 || q > 0) ? 1u : 0u);
               }
-            }
-          } else if (!skip_mma) {
-            constexpr bool TF = ESZ == 4;
-            if (combo == 0)
+            } else if constexpr (KIND == 10) {
               mma_slab<32, 32, TF>(d_tmem, ad0, bd0, idesc, k > 0);
-            else if (combo == 1)
+            } else if constexpr (KIND == 11) {
               mma_slab<32, MNS, TF>(d_tmem, ad0, bd0, idesc, k > 0);
-            else if (combo == 2)
+            } else if constexpr (KIND == 12) {
               mma_slab<MNS, 32, TF>(d_tmem, ad0, bd0, idesc, k > 0);
-            else
+            } else if constexpr (KIND == 13) {
               mma_slab<MNS, MNS, TF>(d_tmem, ad0, bd0, idesc, k > 0);
+            }
+            umma_commit(&empty[s]);
           }
-        umma_commit(&empty[s]);
+          __syncwarp();
+          if (RR && ++g == rr_groups) g = 0;
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1u;
+          }
         }
+        if (elect_one()) umma_commit(&tfull[acc]);
         __syncwarp();
-        if (RR && ++g == p.ngroups[w.z]) g = 0;
-        if (++s == STAGES) {
-          s = 0;
-          ph ^= 1u;
-        }
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
-      __syncwarp();
+    };
+    using std::integral_constant;
+    if constexpr (RR) {
+      switch (p.rr_fast) {
+        case 1: mma_loop(integral_constant<int, 1>{}); break;
+        case 2: mma_loop(integral_constant<int, 2>{}); break;
+        case 3: mma_loop(integral_constant<int, 3>{}); break;
+        case 4: mma_loop(integral_constant<int, 4>{}); break;
+        default: mma_loop(integral_constant<int, 0>{}); break;
+      }
+    } else if (p.probe & 1) {
+      mma_loop(integral_constant<int, -1>{});
+    } else {
+      switch (a_mn * 2 + b_mn) {
+        case 0: mma_loop(integral_constant<int, 10>{}); break;
+        case 1: mma_loop(integral_constant<int, 11>{}); break;
+        case 2: mma_loop(integral_constant<int, 12>{}); break;
+        default: mma_loop(integral_constant<int, 13>{}); break;
+      }
     }
   } else if (kGate && warp == 4 + EPI) {
     // ---------------- MMA gate ----------------
@@ -1396,6 +1417,7 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
   p.ldc = d->K;
   p.out_f32 = 1;
   p.Mpad = Mpad;
+  if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   if ((rc = dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, (cudaStream_t)stream))) return rc;
   long long total = (long long)M * d->K;
   if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
