@@ -138,7 +138,11 @@ constexpr bool kNoGate = false;
 template <class S>
 struct Launch {
   static constexpr bool kTwoPerSM = 2 * S::TOTAL + 8192 <= 227 * 1024;
+#ifdef NSK_GATE_ALL
+  static constexpr bool kGate = !kNoGate;
+#else
   static constexpr bool kGate = !kTwoPerSM && !kNoGate;
+#endif
   template <int EPI>
   static constexpr int threads() { return 128 + 32 * EPI + (kGate ? 32 : 0); }
 };
