@@ -135,6 +135,51 @@ def _param_bn(session, frame, args, line):
     return t
 
 
+def _param_embedding(session, frame, args, line):
+    """param_embedding(vocab, dim): the [vocab, dim] gather table of onehot(tok) @ xavier_uniform(dim, vocab)
+    (one seed draw, stored transposed -- embedding(tokens, table) equals the reference composition)."""
+    _need(args, 2, "param_embedding", line)
+    vocab = _int(args[0], "param_embedding", line)
+    dim = _int(args[1], "param_embedding", line)
+    name = session.new_param_name()
+    vals = np.ascontiguousarray(nn.xavier_values(dim, vocab, session.new_seed()).T)
+    t = autodiff.make_param(session.pool, vals, name)
+    session.param_group.add(name, t)
+    return t
+
+
+def _param_gru(session, frame, args, line):
+    """param_gru(hidden, cols): the (r, z, n) gate weights xavier_uniform(hidden, cols) x 3 (three seed draws
+    in that order) stacked to [3*hidden, cols] -- the input (cols = embedding) or recurrent (cols = hidden)
+    weight of gru()."""
+    _need(args, 2, "param_gru", line)
+    hidden = _int(args[0], "param_gru", line)
+    cols = _int(args[1], "param_gru", line)
+    name = session.new_param_name()
+    vals = np.concatenate([nn.xavier_values(hidden, cols, session.new_seed()) for _ in range(3)])
+    t = autodiff.make_param(session.pool, vals, name)
+    session.param_group.add(name, t)
+    return t
+
+
+def _embedding(session, frame, args, line):
+    """embedding(tokens [B, T], table [V, E]) -> time-major rows [T*B, E]."""
+    _need(args, 2, "embedding", line)
+    tokens = _tensor(args[0], "embedding", line)
+    table = _tensor(args[1], "embedding", line)
+    return session.note_tensor(layers.embedding(tokens, table, session.pool), tokens, table)
+
+
+def _gru(session, frame, args, line):
+    """gru(x [T*B, E], w [3H, E], b [3H], u [3H, H], c [3H], steps) -> h_T [B, H] (h_0 = 0), the fused
+    recurrence of the reference composition r = sigmoid(x@Wr + br + h@Ur + cr), z likewise,
+    n = tanh(x@Wn + bn + r * (h@Un + cn)), h = n - z*n + z*h."""
+    _need(args, 6, "gru", line)
+    x, w, b, u, c = (_tensor(a, "gru", line) for a in args[:5])
+    steps = _int(args[5], "gru", line)
+    return session.note_tensor(layers.gru(x, w, b, u, c, steps, session.pool), x, w, b, u, c)
+
+
 def _linear(session, frame, args, line):
     _need(args, 3, "linear", line)
     x, w, b = (_tensor(a, "linear", line) for a in args)
@@ -297,4 +342,8 @@ BUILTINS = {
     "flatten": _flatten,
     "images": _images,
     "add": _add,
+    "param_embedding": _param_embedding,
+    "param_gru": _param_gru,
+    "embedding": _embedding,
+    "gru": _gru,
 }
