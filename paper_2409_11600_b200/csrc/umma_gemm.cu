@@ -419,8 +419,16 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       int s = 0;
       uint32_t ph = 0;
       int j = 0;
+      // fixed-order row reuse: every unit has the same k-steps (single class, no split) -- no per-tile decode
+      const int nk_fixed = (KIND >= 1 && KIND <= 4) ? rr_groups * p.cchunks : 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-        const Unit w = decode_unit(p, u, BN);
+        Unit w;
+        if constexpr (KIND >= 1 && KIND <= 4) {
+          w.z = 0;
+          w.nk = nk_fixed;
+        } else {
+          w = decode_unit(p, u, BN);
+        }
         const int acc = j & 1;
         if (j >= 2) {
           if constexpr (kGate)
