@@ -343,11 +343,12 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         } else if (p.mode == MODE_CONV) {
           const int tap = kk / p.cchunks;
           const int c0 = (kk - tap * p.cchunks) * 64;
+          const int cls = p.k_per_split > 0 ? 0 : w.z;  // split-K convs: z is the split, the class is 0
           if (p.i2c)
             tma_load_4d_im2col(&tmA, &full[s], sa, c0, p.lw + w_img * p.cs, p.lh + h_img * p.cs, n_img,
-                               (uint16_t)(p.tdw[w.z][tap] - p.lw), (uint16_t)(p.tdh[w.z][tap] - p.lh));
+                               (uint16_t)(p.tdw[cls][tap] - p.lw), (uint16_t)(p.tdh[cls][tap] - p.lh));
           else
-            tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[w.z][tap], h_img * p.cs + p.tdh[w.z][tap],
+            tma_load_4d(&tmA, &full[s], sa, c0, w_img * p.cs + p.tdw[cls][tap], h_img * p.cs + p.tdh[cls][tap],
                         n_img);
         } else {  // WGRAD: A = x, MN-major atoms of 64 channels at tap offsets; K = 64 dy pixels
           const int pix0 = kk * 64;
@@ -386,12 +387,13 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         } else {
           const int tap = kk / p.cchunks;
           const int c0 = (kk - tap * p.cchunks) * 64;
+          const int cls = p.k_per_split > 0 ? 0 : w.z;
           if (p.bmode == BMODE_2D) {
-            tma_load_2d(&tmB, &full[s], sb, p.tw[w.z][tap] * (p.cchunks * 64) + c0, w.n0);
+            tma_load_2d(&tmB, &full[s], sb, p.tw[cls][tap] * (p.cchunks * 64) + c0, w.n0);
           } else {
 #pragma unroll
             for (int b = 0; b < BN / 64; ++b)
-              tma_load_3d(&tmB, &full[s], sb + b * 8192, w.n0 + b * 64, p.tw[w.z][tap], c0);
+              tma_load_3d(&tmB, &full[s], sb + b * 8192, w.n0 + b * 64, p.tw[cls][tap], c0);
           }
         }
       }
@@ -561,6 +563,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       long long row_off;
       if (p.mode == MODE_WGRAD) {
         row_off = (long long)w.z * p.N * p.Mpad + m;  // transposed partials: ws[split][n][m]
+      } else if (p.mode == MODE_CONV && p.k_per_split > 0) {
+        row_off = ((long long)w.z * p.M + m) * p.ldc;  // split-K conv: fp32 partials ws[z][M][N]
       } else if (p.mode == MODE_CONV) {
         const int hw = p.Ho * p.Wo;
         const int nn = m / hw;
@@ -783,6 +787,63 @@ __global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float* __restri
   *d = t;
 }
 
+// split-K conv fold: y[m, :] = bf16(sum_z ws[z][m][:] (+ beta * y[m, :])) in split order, 8 channels per thread;
+// with `stats`, also per-block channel partials [gridDim.x][2][N] (sum, sum of squares of the stored bf16 values)
+// for the BatchNorm consuming y (nsk_bn_fwd_partials), as the conv epilogue would have written them.
+constexpr int kFoldThreads = 256;
+__global__ void __launch_bounds__(kFoldThreads) conv_split_fold_kernel(const float* __restrict__ ws, int splits, int M,
+                                                                       int N, __nv_bfloat16* y, float beta, float* stats) {
+  pdl_wait();
+  extern __shared__ float fold_red[];  // [RPB][N] (stats)
+  const int CV = N / 8;
+  const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = kFoldThreads / CV;
+  const long long plane = (long long)M * N;
+  float s1[8] = {0}, s2[8] = {0};
+  if (ro < RPB) {
+    for (long long r = (long long)blockIdx.x * RPB + ro; r < M; r += (long long)gridDim.x * RPB) {
+      const float* src = ws + r * N + cv * 8;
+      float a[8];
+      {
+        const float4 u0 = __ldg((const float4*)src), u1 = __ldg((const float4*)(src + 4));
+        a[0] = u0.x; a[1] = u0.y; a[2] = u0.z; a[3] = u0.w; a[4] = u1.x; a[5] = u1.y; a[6] = u1.z; a[7] = u1.w;
+      }
+      for (int z = 1; z < splits; ++z) {
+        const float4 u0 = __ldg((const float4*)(src + z * plane)), u1 = __ldg((const float4*)(src + z * plane + 4));
+        a[0] += u0.x; a[1] += u0.y; a[2] += u0.z; a[3] += u0.w; a[4] += u1.x; a[5] += u1.y; a[6] += u1.z; a[7] += u1.w;
+      }
+      uint4* dst = (uint4*)(y + r * N + cv * 8);
+      uint4 v;
+      v.x = pack_bf16x2(a[0], a[1]); v.y = pack_bf16x2(a[2], a[3]);
+      v.z = pack_bf16x2(a[4], a[5]); v.w = pack_bf16x2(a[6], a[7]);
+      if (beta != 0.f) v = bf16x8_axpby(*dst, beta, v);
+      *dst = v;
+      if (stats) {
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&v;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          s1[2 * i] += f.x; s2[2 * i] += f.x * f.x;
+          s1[2 * i + 1] += f.y; s2[2 * i + 1] += f.y * f.y;
+        }
+      }
+    }
+  }
+  if (!stats) return;
+  for (int pass = 0; pass < 2; ++pass) {
+    const float* sv = pass ? s2 : s1;
+    if (ro < RPB)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fold_red[ro * N + cv * 8 + j] = sv[j];
+    __syncthreads();
+    for (int c = threadIdx.x; c < N; c += kFoldThreads) {
+      float t = 0.f;
+      for (int r = 0; r < RPB; ++r) t += fold_red[r * N + c];
+      stats[(size_t)blockIdx.x * 2 * N + pass * N + c] = t;
+    }
+    __syncthreads();
+  }
+}
+
 // split-K GEMM fold: C[m, n] = sum_z ws[z][m][n] (+ bias[n]) (+ beta * C[m, n]), fp32 or bf16 out
 __global__ void splitk_fold_kernel(const float* __restrict__ ws, int splits, int M, int N, void* C, long long ldc,
                                    int c_f32, const float* __restrict__ bias, float beta) {
@@ -904,6 +965,10 @@ int pick_bn(int N) {
 // conv tiles: the widest N tile that still gives every SM a work unit (small late-stage grids
 // otherwise leave most of the 148 SMs idle: 4x4x512 at B=256 is only 32 M tiles)
 int pick_bn_units(int N, int m_tiles, int classes) {
+  if (const char* e = getenv("NSK_CONV_BN")) {  // experiment: force the conv N tile
+    const int f = atoi(e);
+    if ((f == 64 || f == 128 || f == 256) && f <= pick_bn(N)) return f;
+  }
   int bn = pick_bn(N);
   while (bn > 64 && 2 * m_tiles * classes * ((N + bn - 1) / bn) < nsk::sm_count()) bn /= 2;
   return bn;
@@ -1060,6 +1125,53 @@ void try_wres(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int
   p.wres = 1;
 }
 
+// Few output tiles over a long reduction (the 4x4 and 7x7 layers: 32 m-tiles x 512 channels): 256-wide tiles,
+// whose 128x256 MMAs read 25 % less shared memory per flop than 64-wide ones, with the K range split across work
+// units so every SM still has one -- fp32 partials in the library scratch, folded in split order
+// (conv_split_fold_kernel). Returns the split count (1: no split). NSK_CONV_SPLIT=0 disables.
+int conv_splits(int m_tiles, int N, int k_steps) {
+  const char* e = getenv("NSK_CONV_SPLIT");
+  if (e && e[0] == '0') return 1;
+  if (N < 256 || N % 256 || N > 2048) return 1;
+  const int units = m_tiles * (N / 256);
+  if (units >= nsk::sm_count() || k_steps < 64) return 1;  // 8x8 256->512 s2 (36 k-steps): 17.3 -> 19.7 us split
+  int splits = nsk::sm_count() / units;
+  if (e && atoi(e) > 1) splits = atoi(e);  // experiment: forced split count
+  if (splits > k_steps / 16) splits = k_steps / 16;
+  return splits < 2 ? 1 : splits;
+}
+
+// launch the split-K conv and its fold into the bf16 output (beta: accumulate; stats: BN partials, nparts out)
+int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int splits, int k_steps, void* out,
+                   float beta, float* stats, int* nparts, cudaStream_t st) {
+  const int M = p.M, N = p.N;
+  const int per = (k_steps + splits - 1) / splits;
+  splits = (k_steps + per - 1) / per;
+  float* ws = nullptr;
+  int rc = gemm_scratch((size_t)splits * M * N, st, &ws);
+  if (rc) return rc;
+  p.k_steps = k_steps;
+  p.k_per_split = per;
+  p.out = ws;
+  p.ldc = N;
+  p.out_f32 = 1;
+  p.beta = 0.f;
+  p.tma_store = 0;
+  p.stats = nullptr;
+  p.rr = 0;
+  if ((rc = dispatch_bn<2>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st))) return rc;
+  const int CV = N / 8, RPB = kFoldThreads / CV;
+  unsigned grid = (unsigned)((M + RPB - 1) / RPB);
+  if (stats && grid > (unsigned)(2 * nsk::sm_count())) grid = 2 * nsk::sm_count();
+  if (!stats && grid > (unsigned)(16 * nsk::sm_count())) grid = 16 * nsk::sm_count();
+  const size_t smem = stats ? (size_t)RPB * N * sizeof(float) : 0;
+  nsk::launch_pdl(conv_split_fold_kernel, grid, kFoldThreads, smem, st, (const float*)ws, splits, M, N,
+                  (__nv_bfloat16*)out, beta, stats);
+  NSK_LAUNCH_CHECK("conv_split_fold_kernel");
+  if (nparts) *nparts = (int)grid;
+  return NSK_OK;
+}
+
 int check_desc(const NskConvDesc* d) {
   if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride < 1)
     return nsk::set_error(NSK_ERR_SHAPE, "conv2d: invalid descriptor");
@@ -1161,7 +1273,9 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   const int P = d->P, Q = d->Q;
   int Wt = 0, Ht = 0, Nt = 0;
   const bool i2c = !pixel_tile(Q, P, 128, &Wt, &Ht, &Nt) || force_i2c();
-  const int BN = pick_bn_units(d->K, (d->N * P * Q + 127) / 128, 1);
+  const int fsteps = d->R * d->S * (d->C / 64);
+  const int splits = y_f32 ? 1 : conv_splits((d->N * P * Q + 127) / 128, d->K, fsteps);
+  const int BN = splits > 1 ? 256 : pick_bn_units(d->K, (d->N * P * Q + 127) / 128, 1);
   CUtensorMap ma, mb;
   if (!i2c && (rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
   {
@@ -1196,7 +1310,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   p.out_f32 = y_f32;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 128))) return rc;
-  } else if (try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN)) {
+  } else if (splits == 1 && try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN)) {
     try_rr3(p, &mb, d, w, BN, BMODE_RR3);
     try_wres(p, &ma, x, d->N, d->H, d->W, d->C, d->K);
   }
@@ -1207,6 +1321,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
       return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
     p.stats = stats;
   }
+  if (splits > 1) return conv_split_run(p, ma, mb, splits, fsteps, y, 0.f, stats, nparts, (cudaStream_t)stream);
   CUtensorMap mc;
   const bool ts = !y_f32 && out_map(&mc, y, p.M, d->K, d->K);
   p.tma_store = ts;
@@ -1255,7 +1370,9 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
         any = any || (((st == 2 ? (c >> 1) : 0) + d->pad - r) % st == 0 && ((st == 2 ? (c & 1) : 0) + d->pad - q) % st == 0);
     active += any;
   }
-  const int BN = pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, beta == 1.f ? active : st * st);
+  const int dsteps = d->R * d->S * (d->K / 64);
+  const int splits = st == 1 ? conv_splits((d->N * Hg * Wg + 127) / 128, d->C, dsteps) : 1;
+  const int BN = splits > 1 ? 256 : pick_bn_units(d->C, (d->N * Hg * Wg + 127) / 128, beta == 1.f ? active : st * st);
   CUtensorMap ma, mb;
   if (!i2c && (rc = nhwc_map(&ma, dy, d->N, P, Q, d->K, 64, Wt, Ht, Nt, 1))) return rc;
   {
@@ -1324,12 +1441,13 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   p.beta = beta;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, dy, d->N, P, Q, d->K, Hg, Wg, ncls_run, 128))) return rc;
-  } else if (ncls == 1 && try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN)) {
+  } else if (ncls == 1 && splits == 1 && try_rowreuse(p, &ma, dy, d->N, P, Q, d->K, BN)) {
     if (BN == 64) {
       try_rr3(p, &mb, d, w, BN, BMODE_RR3T);
       try_wres(p, &ma, dy, d->N, P, Q, d->K, d->C);
     }
   }
+  if (splits > 1) return conv_split_run(p, ma, mb, splits, dsteps, dx, beta, nullptr, nullptr, (cudaStream_t)stream);
   CUtensorMap mc;
   const char* red = getenv("NSK_TMA_REDUCE");
   const bool ts = ncls == 1 && (beta == 0.f || (beta == 1.f && !(red && red[0] == '0'))) &&
