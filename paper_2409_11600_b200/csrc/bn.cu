@@ -279,6 +279,215 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
   }
 }
 
+// ---- finalize folded into the apply pass ----
+// A separate finalize launch per BatchNorm cost ~4 us of step time each (39 per ResNet-18 step: 163 us measured by
+// skipping them). Instead the first C/2 blocks of the apply grid fold one channel per 128 threads (float64, fixed
+// order: threads stride the partial rows, butterfly, warp sums in order), publish scale/shift (or the backward coefficients) and
+// count themselves done; every block waits for the count, stages the per-channel values in shared memory and
+// applies. The folding blocks have the lowest indices, so they are resident before any block spins on them. The
+// last block to leave re-arms the counters for the next launch (launches of these kernels are stream-ordered).
+__device__ unsigned g_fold_sync[2][2];  // [fwd | bwd][folded channels, blocks done]
+
+__device__ __forceinline__ void fold_wait(unsigned* sync, unsigned target) {
+  if (threadIdx.x == 0) {
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sync) : "memory");
+      if (v >= target) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void fold_leave(unsigned* sync) {
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&sync[1], 1u) == gridDim.x - 1) {
+    sync[0] = 0u;
+    sync[1] = 0u;
+  }
+}
+
+// float64 fold of channel c's two partial columns over nblk rows of [nblk][2][C] by the 128 threads of one half
+// block (4 warps; fixed order: thread strides, butterfly, then the 4 warp sums in order). All BT threads call it.
+constexpr int FOLD_T = 128;  // threads per folded channel
+constexpr int AT = BT;       // threads per block of the fused fold+apply passes
+__device__ __forceinline__ void group_fold(const float* part, int nblk, int C, int c, double* a, double* b) {
+  __shared__ double red[AT / 32][2];
+  const int t = threadIdx.x % FOLD_T;
+  double x = 0.0, y = 0.0, x2 = 0.0, y2 = 0.0;
+  if (c < C) {
+    int k = t;
+    for (; k + FOLD_T < nblk; k += 2 * FOLD_T) {  // two rows in flight per thread
+      const float p0 = __ldcg(part + (size_t)k * 2 * C + c), q0 = __ldcg(part + (size_t)k * 2 * C + C + c);
+      const float p1 = __ldcg(part + (size_t)(k + FOLD_T) * 2 * C + c);
+      const float q1 = __ldcg(part + (size_t)(k + FOLD_T) * 2 * C + C + c);
+      x += p0; y += q0; x2 += p1; y2 += q1;
+    }
+    if (k < nblk) {
+      x += (double)__ldcg(part + (size_t)k * 2 * C + c);
+      y += (double)__ldcg(part + (size_t)k * 2 * C + C + c);
+    }
+  }
+  x = warp_sum_d(x + x2);
+  y = warp_sum_d(y + y2);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[w][0] = x;
+    red[w][1] = y;
+  }
+  __syncthreads();
+  const int g0 = (threadIdx.x / FOLD_T) * (FOLD_T / 32);
+  *a = (red[g0][0] + red[g0 + 1][0]) + (red[g0 + 2][0] + red[g0 + 3][0]);
+  *b = (red[g0][1] + red[g0 + 1][1]) + (red[g0 + 2][1] + red[g0 + 3][1]);
+  __syncthreads();  // red is reused by the next channel pair
+}
+
+__global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, int nblk, uint64_t rows, int C, float eps,
+                                                           const float* __restrict__ gb, float* mean, float* invstd,
+                                                           float* running, float momentum, float* affine,
+                                                           const __nv_bfloat16* __restrict__ x,
+                                                           const __nv_bfloat16* __restrict__ res,
+                                                           __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
+                                                           int relu, int nfold) {
+  pdl_wait();
+  unsigned* sync = g_fold_sync[0];
+  // folding blocks: the first nfold (<= SMs, so they are resident before anyone spins), 2 channels per pass
+  for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
+    const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
+    double a, b;
+    group_fold(part, nblk, C, c, &a, &b);
+    if (c < C && threadIdx.x % FOLD_T == 0) {
+      const double mu = a / (double)rows;
+      double var = b / (double)rows - mu * mu;
+      if (var < 0.0) var = 0.0;
+      const double is = 1.0 / sqrt(var + (double)eps);
+      mean[c] = (float)mu;
+      invstd[c] = (float)is;
+      const double g = gb[c], be = gb[C + c];
+      affine[c] = (float)(g * is);
+      affine[C + c] = (float)(be - mu * g * is);
+      if (running) {  // running statistics, unbiased variance (torch.nn.BatchNorm2d convention)
+        const double n = (double)rows;
+        const double unb = n > 1.0 ? var * n / (n - 1.0) : var;
+        running[c] = (float)((1.0 - momentum) * running[c] + momentum * mu);
+        running[C + c] = (float)((1.0 - momentum) * running[C + c] + momentum * unb);
+      }
+      __threadfence();
+      atomicAdd(&sync[0], 1u);
+    }
+  }
+  fold_wait(sync, (unsigned)C);
+  extern __shared__ float aff[];  // [2][C]
+  for (int i = threadIdx.x; i < 2 * C; i += AT) aff[i] = __ldcg(affine + i);
+  __syncthreads();
+  const float* scale = aff;
+  const float* shift = aff + C;
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  const int CV = C / 8;
+  for (uint64_t i = (uint64_t)blockIdx.x * AT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * AT) {
+    const int c0 = (int)(i % CV) * 8;
+    float f[8], r[8];
+    ld8(x + i * 8, f);
+    if (res) ld8(res + i * 8, r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float v = f[j] * scale[c0 + j] + shift[c0 + j];
+      if (res) v += r[j];
+      if (relu) v = v > 0.f ? v : 0.f;
+      f[j] = v;
+    }
+    st8(y + i * 8, f);
+    if (mask) {
+      unsigned bits = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) bits |= (f[j] > 0.f ? 1u : 0u) << j;
+      mask[i] = (uint8_t)bits;
+    }
+  }
+  fold_leave(sync);
+}
+
+__global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part, int nblk, uint64_t rows, int C,
+                                                               const float* __restrict__ gb,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ invstd, float* dgb,
+                                                               float beta_acc, float* coefg,
+                                                               const __nv_bfloat16* __restrict__ dy,
+                                                               const __nv_bfloat16* __restrict__ x,
+                                                               const uint8_t* __restrict__ mask,
+                                                               __nv_bfloat16* __restrict__ dx,
+                                                               __nv_bfloat16* __restrict__ dres, int nfold) {
+  pdl_wait();
+  unsigned* sync = g_fold_sync[1];
+  for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
+    const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
+    double sdz, sdzx;
+    group_fold(part, nblk, C, c, &sdz, &sdzx);
+    if (c < C && threadIdx.x % FOLD_T == 0) {
+      const double mu = mean[c], is = invstd[c], g = gb[c], M = (double)rows;
+      const double dbeta = sdz;
+      const double dgamma = is * (sdzx - mu * sdz);
+      if (beta_acc != 0.f) {
+        dgb[c] = (float)(dgamma + beta_acc * dgb[c]);
+        dgb[C + c] = (float)(dbeta + beta_acc * dgb[C + c]);
+      } else {
+        dgb[c] = (float)dgamma;
+        dgb[C + c] = (float)dbeta;
+      }
+      coefg[c] = (float)(g * is);
+      coefg[C + c] = (float)(-g * is * is * dgamma / M);
+      coefg[2 * C + c] = (float)(-g * is * dbeta / M + g * is * is * mu * dgamma / M);
+      __threadfence();
+      atomicAdd(&sync[0], 1u);
+    }
+  }
+  fold_wait(sync, (unsigned)C);
+  extern __shared__ float coef[];  // [3][C]
+  for (int i = threadIdx.x; i < 3 * C; i += AT) coef[i] = __ldcg(coefg + i);
+  __syncthreads();
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  const int CV = C / 8;
+  for (uint64_t i = (uint64_t)blockIdx.x * AT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * AT) {
+    const int c0 = (int)(i % CV) * 8;
+    float g[8], xv[8];
+    ld8(dy + i * 8, g);
+    ld8(x + i * 8, xv);
+    if (mask) {
+      const unsigned m = __ldg(mask + i);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = ((m >> j) & 1u) ? g[j] : 0.f;
+    }
+    if (dres) st8(dres + i * 8, g);
+    float o[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = coef[c0 + j] * g[j] + coef[C + c0 + j] * xv[j] + coef[2 * C + c0 + j];
+    st8(dx + i * 8, o);
+  }
+  fold_leave(sync);
+}
+
+// folding blocks: one per channel pair, at most one per SM (every folding block must be resident before any
+// block spins on the count: 1024 pairs for C = 2048 deadlocked with 4 resident blocks per SM)
+int fold_blocks(int C) {
+  const int groups = (C + AT / FOLD_T - 1) / (AT / FOLD_T);
+  return groups < nsk::sm_count() ? groups : nsk::sm_count();
+}
+unsigned fold_grid(uint64_t nv, int C) {
+  unsigned g = nsk::grid_for(nv, AT);
+  const unsigned need = (unsigned)fold_blocks(C);
+  return g < need ? need : g;
+}
+
+// The fused fold+apply stalls every block until the fold is done (a few us); that only beats a separate
+// finalize launch (~4 us of step time each) when the apply itself is long: ResNet-50's 56x56x256 layers
+// (8.3k vs 7.6k img/s) yes, ResNet-18's (2.61 vs 2.71 ms/step) no.
+bool fold_in_apply(uint64_t rows, int C) {
+  const char* e = getenv("NSK_BN_FOLD_APPLY");
+  if (e) return e[0] == '1';
+  return rows * (uint64_t)C >= (1ull << 25);
+}
+
 int nblocks(uint64_t rows, int C) {
   const int RPB = BT / (C / 8);
   uint64_t want = (rows + RPB * 8 - 1) / (RPB * 8);  // >= 8 rows per thread
@@ -316,10 +525,19 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
   nsk::launch_pdl(bn_stats_kernel, nb, BT, smem, st, (const __nv_bfloat16*)x, rows, C, part);
-  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, part, nb, rows, C, eps, gamma_beta, mean, invstd, scale, shift, running, momentum);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
-                                                        shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
+  if (!fold_in_apply(rows, C)) {
+    nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, eps, gamma_beta, mean, invstd, scale,
+                    shift, running, momentum);
+    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+                    (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
+                    (uint8_t*)relu_mask, rows, C, relu);
+    NSK_LAUNCH_CHECK("bn_fwd");
+    return NSK_OK;
+  }
+  nsk::launch_pdl(bn_apply_fold_kernel, fold_grid(nv, C), AT, 2 * C * sizeof(float), st, (const float*)part, nb, rows,
+                  C, eps, gamma_beta, mean, invstd, running, momentum, scale, (const __nv_bfloat16*)x,
+                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C));
   NSK_LAUNCH_CHECK("bn_fwd");
   return NSK_OK;
 }
@@ -335,10 +553,19 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   cudaStream_t st = (cudaStream_t)stream;
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
-  nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale, shift, running, momentum);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x, (const __nv_bfloat16*)residual, scale,
-                                                        shift, (__nv_bfloat16*)y, (uint8_t*)relu_mask, rows, C, relu);
+  if (!fold_in_apply(rows, C)) {
+    nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale,
+                    shift, running, momentum);
+    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+                    (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
+                    (uint8_t*)relu_mask, rows, C, relu);
+    NSK_LAUNCH_CHECK("bn_fwd_partials");
+    return NSK_OK;
+  }
+  nsk::launch_pdl(bn_apply_fold_kernel, fold_grid(nv, C), AT, 2 * C * sizeof(float), st, partials, nparts, rows, C, eps,
+                  gamma_beta, mean, invstd, running, momentum, scale, (const __nv_bfloat16*)x,
+                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C));
   NSK_LAUNCH_CHECK("bn_fwd_partials");
   return NSK_OK;
 }
@@ -382,12 +609,20 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   float* coef = ws + (size_t)MAXBLK * 2 * C;  // 3*C floats (workspace reserves 4*C)
   nsk::launch_pdl(bn_bwd_reduce_kernel, nb, BT, smem, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
                                              (const uint8_t*)relu_mask, rows, C, part);
-  nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, part, nb, rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc,
-                                                   coef);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, 
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, coef, (__nv_bfloat16*)dx,
-      (__nv_bfloat16*)dres, rows, C);
+  if (!fold_in_apply(rows, C)) {
+    nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, gamma_beta, mean, invstd,
+                    dgamma_beta, beta_acc, coef);
+    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)dy,
+                    (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (const float*)coef, (__nv_bfloat16*)dx,
+                    (__nv_bfloat16*)dres, rows, C);
+    NSK_LAUNCH_CHECK("bn_bwd");
+    return NSK_OK;
+  }
+  nsk::launch_pdl(bn_bwd_apply_fold_kernel, fold_grid(nv, C), AT, 3 * C * sizeof(float), st, (const float*)part, nb,
+                  rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc, coef, (const __nv_bfloat16*)dy,
+                  (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres,
+                  fold_blocks(C));
   NSK_LAUNCH_CHECK("bn_bwd");
   return NSK_OK;
 }

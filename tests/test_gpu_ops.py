@@ -199,9 +199,13 @@ def test_conv2d_shape_errors(session):
 
 # --- batchnorm -------------------------------------------------------------------------------------
 
+@pytest.mark.parametrize("fold_apply", ["0", "1"])
 @pytest.mark.parametrize("relu,res", [(False, False), (True, False), (True, True)])
-@pytest.mark.parametrize("shape", [(8, 32, 32, 64), (16, 4, 4, 512), (64, 8, 8, 256)])
-def test_batchnorm_fwd_bwd(session, shape, relu, res):
+@pytest.mark.parametrize("shape", [(8, 32, 32, 64), (16, 4, 4, 512), (64, 8, 8, 256), (2, 7, 7, 2048)])
+def test_batchnorm_fwd_bwd(session, shape, relu, res, fold_apply, monkeypatch):
+    """Both finalize strategies: a separate fold kernel, and the fold done by the first blocks of the apply
+    pass (NSK_BN_FOLD_APPLY=1; the default for large layers) -- 2048 channels exercise the capped fold grid."""
+    monkeypatch.setenv("NSK_BN_FOLD_APPLY", fold_apply)
     from paper_2409_11600_b200 import autodiff, layers
     from paper_2409_11600_b200._lib import BF16
 
