@@ -68,9 +68,12 @@ __device__ void block_reduce_store(float* s1, float* s2, int C, float* part) {
 }
 
 // pass 1 of fwd: sum x and sum x^2 per channel
+__device__ unsigned g_fold_sync[2][2];
+
 __global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __restrict__ x, uint64_t rows, int C,
                                                       float* part) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_fold_sync[0][0] = 0u;  // re-arm the apply pass's fold count
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -202,6 +205,7 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
                                                            const uint8_t* __restrict__ mask, uint64_t rows, int C,
                                                            float* part) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_fold_sync[1][0] = 0u;  // re-arm the apply pass's fold count
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -285,27 +289,22 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
 // order: threads stride the partial rows, butterfly, warp sums in order), publish scale/shift (or the backward coefficients) and
 // count themselves done; every block waits for the count, stages the per-channel values in shared memory and
 // applies. The folding blocks have the lowest indices, so they are resident before any block spins on them. The
-// last block to leave re-arms the counters for the next launch (launches of these kernels are stream-ordered).
-__device__ unsigned g_fold_sync[2][2];  // [fwd | bwd][folded channels, blocks done]
+// count is re-armed by the kernel that produced the partials (bn_stats / bn_bwd_reduce / the conv statistics
+// epilogue zero it at their start, nsk_bn_fold_counter), so the apply needs no exit accounting (2.4k
+// same-address atomics per launch were measurable).
+// g_fold_sync[fwd | bwd][0]: folded channels (declared with bn_stats_kernel)
 
 __device__ __forceinline__ void fold_wait(unsigned* sync, unsigned target) {
   if (threadIdx.x == 0) {
-    unsigned v;
+    unsigned v, ns = 64;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sync) : "memory");
       if (v >= target) break;
-      __nanosleep(64);
+      __nanosleep(ns);  // back off: a thousand pollers on one L2 line slow the folding blocks' atomics
+      if (ns < 512) ns *= 2;
     }
   }
   __syncthreads();
-}
-
-__device__ __forceinline__ void fold_leave(unsigned* sync) {
-  __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(&sync[1], 1u) == gridDim.x - 1) {
-    sync[0] = 0u;
-    sync[1] = 0u;
-  }
 }
 
 // float64 fold of channel c's two partial columns over nblk rows of [nblk][2][C] by the 128 threads of one half
@@ -405,7 +404,6 @@ __global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, in
       mask[i] = (uint8_t)bits;
     }
   }
-  fold_leave(sync);
 }
 
 __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part, int nblk, uint64_t rows, int C,
@@ -464,7 +462,6 @@ __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part
     for (int j = 0; j < 8; ++j) o[j] = coef[c0 + j] * g[j] + coef[C + c0 + j] * xv[j] + coef[2 * C + c0 + j];
     st8(dx + i * 8, o);
   }
-  fold_leave(sync);
 }
 
 // folding blocks: one per channel pair, at most one per SM (every folding block must be resident before any
@@ -505,6 +502,17 @@ int check(uint64_t rows, int C, const void* a, const void* b) {
 }
 
 }  // namespace
+
+// device address of the forward fold count, zeroed by the conv statistics epilogue (umma_gemm.cu) that feeds
+// nsk_bn_fwd_partials
+unsigned* nsk::bn_fold_counter_fwd() {
+  static unsigned* p = nullptr;
+  if (!p) {
+    void* a = nullptr;
+    if (cudaGetSymbolAddress(&a, g_fold_sync) == cudaSuccess) p = (unsigned*)a;
+  }
+  return p;
+}
 
 extern "C" {
 

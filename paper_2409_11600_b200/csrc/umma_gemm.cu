@@ -73,6 +73,7 @@ struct UmmaProb {
   // conv fprop feeding a BatchNorm: per-CTA channel partials [gridDim.x][2][N] (sum, sum of squares of
   // the bf16-rounded outputs) so the BN statistics need no extra pass over the activation
   float* stats;
+  unsigned* fold_reset;  // statistics feeding a fused BatchNorm apply: zero its fold count (bn.cu) at start
   int wres;    // weight-resident row-reuse (see Smem WRES)
   int rr_fast;  // row-reuse 3x3 on 32-wide rows, taps t = 0..2 at row offsets t (1: fprop, 2: dgrad) or 2 - t
                 // (4: fprop, 3: dgrad): the MMA issuer uses immediate descriptor offsets
@@ -220,6 +221,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const UmmaProb p) {
   pdl_wait();
+  if (p.fold_reset && blockIdx.x == 0 && threadIdx.x == 0) *p.fold_reset = 0u;
   using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
   using T = KT<ESZ>;
   constexpr bool kGate = Launch<S>::kGate;
@@ -1320,6 +1322,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
     if (stats_floats < (uint64_t)2 * nsk::sm_count() * 2 * d->K)
       return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
     p.stats = stats;
+    p.fold_reset = nsk::bn_fold_counter_fwd();
   }
   if (splits > 1) return conv_split_run(p, ma, mb, splits, fsteps, y, 0.f, stats, nparts, (cudaStream_t)stream);
   CUtensorMap mc;
