@@ -24,6 +24,7 @@ import os
 import numpy as np
 
 from . import _lib
+from .side import SIDE
 from ._lib import F32, check
 from .errors import NskRuntimeError
 
@@ -120,6 +121,7 @@ class DataParallel:
         ptr = self.s.grad_cache.arena.ptr + 4 * start
         check(lib.nsk_event_record(self.ev_compute[i], _lib.stream()))
         check(lib.nsk_event_wait(self.comm_stream, self.ev_compute[i]))
+        SIDE.order_after(self.comm_stream)  # weight gradients forked onto the side stream (side.py)
         check(lib.nsk_allreduce(self.comm, ptr, count, F32, self.comm_stream))
         self.launched[i] = True
 

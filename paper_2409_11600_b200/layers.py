@@ -18,6 +18,7 @@ import weakref
 import numpy as np
 
 from . import _lib
+from .side import SIDE
 from ._lib import BF16, F32, ConvDesc, check
 from .autodiff import SUNK, _internal_tensor, record, rule
 from .errors import NskRuntimeError, NskTypeError
@@ -29,9 +30,12 @@ class Workspace:
 
     def __init__(self):
         self.buf: Buffer | None = None
+        self.retired: list[Buffer] = []  # outgrown buffers a side-stream kernel may still read (side.py)
 
     def get(self, nbytes: int) -> Buffer:
         if self.buf is None or self.buf.nbytes < nbytes:
+            if self.buf is not None:
+                self.retired.append(self.buf)
             self.buf = Buffer((max(nbytes, 1 << 20) + 3) // 4, F32)
         return self.buf
 
@@ -175,7 +179,12 @@ def _r_conv2d(node, g, pool, sinks):
             xp, xtmp = _temp_bf16(xin, pool)
             need = lib.nsk_conv2d_wgrad_workspace(C.byref(desc))
             ws = WGRAD_WS.get(need)
-            check(lib.nsk_conv2d_wgrad(C.byref(desc), xp, gp, out_ptr, beta, ws.ptr, ws.nbytes, st))
+            wst = st
+            if sinks[1] is not None and SIDE.enabled():
+                # overlap the weight gradient with the rest of backward (side.py); its inputs stay alive to the join
+                wst = SIDE.fork(xin.buffer, g.buffer, None if xtmp is None else xtmp.buffer,
+                                None if gtmp is None else gtmp.buffer)
+            check(lib.nsk_conv2d_wgrad(C.byref(desc), xp, gp, out_ptr, beta, ws.ptr, ws.nbytes, wst))
             if xtmp is not None:
                 release_tensor(pool, xtmp)
     if gtmp is not None:

@@ -184,6 +184,10 @@ class Pool:
         return Buffer(numel, dtype)
 
     def release(self, buffer: Buffer) -> None:
+        from .side import SIDE
+
+        if SIDE.defer(self, buffer):  # read by an in-flight side-stream kernel: released at the join
+            return
         with self._lock:
             if buffer.in_pool:
                 raise NskRuntimeError("double release of a pooled buffer")
