@@ -95,6 +95,30 @@ def test_resnet18_graph_replay_matches_eager(dev):
     np.testing.assert_allclose(losses[True], losses[False], rtol=1e-5)
 
 
+def test_side_stream_weight_gradients_are_bit_identical(dev, monkeypatch):
+    """Conv weight gradients forked onto the side stream (side.py) vs all on the compute stream: captured
+    ResNet-18 steps give bit-identical losses and parameters (same kernels, same order within each stream;
+    the deferred releases keep every input alive until the join)."""
+    from paper_2409_11600_b200.models import ResNet18
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    rng = np.random.default_rng(5)
+    b = 32
+    xs = [rng.standard_normal((b, 3, 32, 32)).astype(np.float32) for _ in range(4)]
+    ys = [rng.integers(0, 10, b).astype(np.float32) for _ in range(4)]
+    out = {}
+    for side in ("1", "0"):
+        monkeypatch.setenv("NSK_SIDE_WGRAD", side)
+        s = Session(seed=0)
+        tr = Trainer(s, ResNet18(s), xs[0].shape, 10, optimizer=("sgd", 0.1, 0.9), graph=True, warmup=1)
+        losses = [float(tr.step(x, y)) for x, y in zip(xs, ys)]
+        out[side] = (losses, [t.data.copy() for _n, t in s.param_group.params])
+    assert out["1"][0] == out["0"][0]
+    for a, b2 in zip(out["1"][1], out["0"][1]):
+        np.testing.assert_array_equal(a, b2)
+
+
 def test_resnet50_whole_step_matches_oracle(session):
     """C4 architecture at a reduced 64x64 input (grids 32/16/8/4/2 exercise the im2col-mode convs, the 7x7/2
     stem and the 3x3/2 max-pool), one forward/backward vs the bf16-emulating oracle.
