@@ -41,7 +41,17 @@ class Workspace:
 
 
 WGRAD_WS = Workspace()
-BN_WS = Workspace()
+class _PerStream:
+    """One Workspace per stream (a forward branch on the side stream runs BatchNorms concurrently)."""
+
+    def __init__(self):
+        self.ws: dict[int, Workspace] = {}
+
+    def get(self, nbytes: int) -> Buffer:
+        return self.ws.setdefault(_lib.stream(), Workspace()).get(nbytes)
+
+
+BN_WS = _PerStream()
 
 
 def _temp_bf16(t: Tensor, pool: Pool) -> tuple[int, Tensor | None]:

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from .side import SIDE
 from . import autodiff, layers, nn
 from .runtime import Session
 from .tensor import Tensor
@@ -109,12 +110,19 @@ class ResNet18:
         for i, blk in enumerate(self.blocks):
             st = blk["stride"]
             # projection shortcut recorded first: its backward then runs after conv1's and accumulates into dx,
-            # which lets the 1x1 stride-2 dgrad skip the three parity classes it has no taps for
+            # which lets the 1x1 stride-2 dgrad skip the three parity classes it has no taps for. Its forward is
+            # an independent branch: issued on the side stream, overlapping conv1 (side.py)
             if "wsc" in blk:
+                fork = SIDE.enabled()
+                if fork:
+                    SIDE.branch_begin()
                 sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
+                if fork:
+                    SIDE.branch_end()
             else:
                 sc = h
             o = layers.conv_bn(h, blk["w1"], blk["bn1"], st, 1, pool, relu=True, training=train)
+            SIDE.branch_join()
             h = layers.conv_bn(o, blk["w2"], blk["bn2"], 1, 1, pool, relu=True, residual=sc, training=train)
             push(f"rn.block{i}", h)
         feat = layers.avgpool_global(h, pool)

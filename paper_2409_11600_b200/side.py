@@ -30,6 +30,8 @@ class SideStream:
         self.active = False
         self.reads: dict[int, object] = {}  # id(buffer) -> buffer read by in-flight side work
         self.deferred: list = []            # (pool, buffer) releases held until join
+        self._main = None                   # compute stream while a forward branch runs here (branch())
+        self._ev_branch = None
 
     @staticmethod
     def enabled() -> bool:
@@ -58,8 +60,9 @@ class SideStream:
         return self._stream
 
     def defer(self, pool, buffer) -> bool:
-        """Pool.release hook: hold the release of a buffer an in-flight side kernel reads."""
-        if self.active and id(buffer) in self.reads:
+        """Pool.release hook: hold the release of a buffer an in-flight side kernel reads (every release while a
+        forward branch is being issued here)."""
+        if self._main is not None or (self.active and id(buffer) in self.reads):
             self.deferred.append((pool, buffer))
             return True
         return False
@@ -82,6 +85,39 @@ class SideStream:
         held, self.deferred = self.deferred, []
         for pool, buf in held:
             pool.release(buf)
+
+
+    # ---- forward branches (independent sub-graphs, e.g. a projection shortcut next to conv1) ----
+    def branch_begin(self) -> None:
+        """Issue the following ops on this stream (ordered after the compute stream so far) until branch_end."""
+        self._init()
+        if self._ev_branch is None:
+            e = C.c_void_p()
+            check(_lib.lib().nsk_event_create(0, C.byref(e)))
+            self._ev_branch = e.value
+        lib = _lib.lib()
+        check(lib.nsk_event_record(self._ev_fork, _lib.stream()))
+        check(lib.nsk_event_wait(self._stream, self._ev_fork))
+        self._main = _lib.ctx.stream
+        _lib.ctx.stream = self._stream
+
+    def branch_end(self) -> None:
+        """Back to the compute stream; the branch is joined lazily by branch_join."""
+        _lib.ctx.stream = self._main
+        self._main = None
+        check(_lib.lib().nsk_event_record(self._ev_branch, self._stream))
+        self._branch_pending = True
+
+    def branch_join(self) -> None:
+        """Compute stream waits for the branch; its deferred releases go back to the pool."""
+        if not getattr(self, "_branch_pending", False):
+            return
+        check(_lib.lib().nsk_event_wait(_lib.stream(), self._ev_branch))
+        self._branch_pending = False
+        if not self.active:  # no weight-gradient work in flight holds these
+            held, self.deferred = self.deferred, []
+            for pool, buf in held:
+                pool.release(buf)
 
 
 SIDE = SideStream()
