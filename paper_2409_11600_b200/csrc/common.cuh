@@ -73,9 +73,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+int grid_cap_per_sm();  // blocks per SM for grid-stride elementwise kernels (runtime.cu; NSK_GRID_CAP)
 inline unsigned grid_for(int64_t n, int block, int per_thread = 1) {
   int64_t g = (n + (int64_t)block * per_thread - 1) / ((int64_t)block * per_thread);
-  int64_t cap = (int64_t)sm_count() * 16;
+  int64_t cap = (int64_t)sm_count() * grid_cap_per_sm();
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (unsigned)g;

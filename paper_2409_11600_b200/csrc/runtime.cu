@@ -45,6 +45,16 @@ int sm_count() {
   return g_sm_count;
 }
 
+int grid_cap_per_sm() {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("NSK_GRID_CAP");
+    cap = e ? atoi(e) : 16;
+    if (cap < 1) cap = 16;
+  }
+  return cap;
+}
+
 bool pdl_enabled() {
   static int on = -1;
   if (on < 0) {
