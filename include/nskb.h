@@ -95,6 +95,8 @@ int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, v
 int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream);
 /* dx = dgrad + beta * dx (bf16, in place): accumulates a second gradient contribution in the epilogue */
 int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, void* stream);
+/* CTAs per weight-gradient launch (0 = default two per SM); see side.py */
+int nsk_wgrad_grid_cap(int ctas);
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d);
 int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float* dw, float beta, void* ws,
                      uint64_t ws_bytes, void* stream);

@@ -61,6 +61,7 @@ SIGNATURES = {
     "nsk_gemm": (i32, [i32, i32, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, i32, vp, f32, vp]),
     "nsk_conv2d_fprop": (i32, [C.POINTER(ConvDesc), vp, vp, vp, i32, vp]),
     "nsk_conv2d_fprop_stats": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp, u64, C.POINTER(C.c_int), vp]),
+    "nsk_wgrad_grid_cap": (i32, [i32]),
     "nsk_conv2d_dgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp]),
     "nsk_conv2d_dgrad_acc": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp]),
     "nsk_conv2d_wgrad_workspace": (u64, [C.POINTER(ConvDesc)]),

@@ -893,6 +893,8 @@ int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
   return NSK_OK;
 }
 
+int g_wgrad_grid_cap = 0;  // CTAs per wgrad launch (0: two per SM as usual)
+
 template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false>
 int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, UmmaProb p, cudaStream_t st,
                 int* grid_out) {
@@ -908,6 +910,11 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   }
   const int per_sm = (2 * smem <= 227 * 1024) ? 2 : 1;  // small-N tiles: two co-resident CTAs per SM
   int grid = per_sm * nsk::sm_count();
+  if (p.mode == MODE_WGRAD) {  // weight gradients beside the compute stream: leave it SMs (nsk_wgrad_grid_cap)
+    int cap = g_wgrad_grid_cap;
+    if (const char* e = getenv("NSK_WGRAD_GRID")) cap = atoi(e);
+    if (cap > 0 && cap < grid) grid = cap;
+  }
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
@@ -1459,6 +1466,13 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run, (cudaStream_t)stream,
                         nullptr, ts ? &mc : nullptr);
+}
+
+// Grid cap for the weight-gradient kernels. side.py sets it to one CTA per SM while wgrads run on a side stream
+// next to the rest of backward: two persistent CTAs per SM starve the compute stream (2.41 -> 2.35 ms/step).
+int nsk_wgrad_grid_cap(int ctas) {
+  g_wgrad_grid_cap = ctas < 0 ? 0 : ctas;
+  return NSK_OK;
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {

@@ -40,6 +40,8 @@ class SideStream:
     def _init(self):
         if self._stream is None:
             lib = _lib.lib()
+            # weight gradients share the GPU with the compute stream: one persistent CTA per SM (umma_gemm.cu)
+            check(lib.nsk_wgrad_grid_cap(_lib.ctx.sm_count))
             s, e0, e1 = C.c_void_p(), C.c_void_p(), C.c_void_p()
             check(lib.nsk_stream_create(C.byref(s)))
             check(lib.nsk_event_create(0, C.byref(e0)))
