@@ -68,12 +68,13 @@ __device__ void block_reduce_store(float* s1, float* s2, int C, float* part) {
 }
 
 // pass 1 of fwd: sum x and sum x^2 per channel
-__device__ unsigned g_fold_sync[2][2];
+constexpr int kFoldSlots = 4;  // one fold-count pair per stream that runs BatchNorms (compute + side branches)
+__device__ unsigned g_fold_sync[kFoldSlots][2][2];
 
 __global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __restrict__ x, uint64_t rows, int C,
-                                                      float* part) {
+                                                      float* part, unsigned* rearm) {
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_fold_sync[0][0] = 0u;  // re-arm the apply pass's fold count
+  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) *rearm = 0u;  // re-arm the apply pass's fold count
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -203,9 +204,9 @@ __global__ void bn_eval_affine_kernel(const float* __restrict__ gb, const float*
 __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* __restrict__ dy,
                                                            const __nv_bfloat16* __restrict__ x,
                                                            const uint8_t* __restrict__ mask, uint64_t rows, int C,
-                                                           float* part) {
+                                                           float* part, unsigned* rearm) {
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) g_fold_sync[1][0] = 0u;  // re-arm the apply pass's fold count
+  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) *rearm = 0u;  // re-arm the apply pass's fold count
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -348,9 +349,8 @@ __global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, in
                                                            const __nv_bfloat16* __restrict__ x,
                                                            const __nv_bfloat16* __restrict__ res,
                                                            __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
-                                                           int relu, int nfold) {
+                                                           int relu, int nfold, unsigned* sync) {
   pdl_wait();
-  unsigned* sync = g_fold_sync[0];
   // folding blocks: the first nfold (<= SMs, so they are resident before anyone spins), 2 channels per pass
   for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
     const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
@@ -415,9 +415,9 @@ __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part
                                                                const __nv_bfloat16* __restrict__ x,
                                                                const uint8_t* __restrict__ mask,
                                                                __nv_bfloat16* __restrict__ dx,
-                                                               __nv_bfloat16* __restrict__ dres, int nfold) {
+                                                               __nv_bfloat16* __restrict__ dres, int nfold,
+                                                               unsigned* sync) {
   pdl_wait();
-  unsigned* sync = g_fold_sync[1];
   for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
     const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
     double sdz, sdzx;
@@ -476,10 +476,32 @@ unsigned fold_grid(uint64_t nv, int C) {
   return g < need ? need : g;
 }
 
+// fold counts of the stream's slot: [0] forward, [2] backward (slots handed out to streams on first use)
+static unsigned* fold_counters(cudaStream_t st) {
+  static unsigned* base = nullptr;
+  static cudaStream_t owners[kFoldSlots] = {};
+  static int used = 0;
+  if (!base) {
+    void* a = nullptr;
+    if (cudaGetSymbolAddress(&a, g_fold_sync) != cudaSuccess) return nullptr;
+    base = (unsigned*)a;
+  }
+  int slot = -1;
+  for (int i = 0; i < used; ++i)
+    if (owners[i] == st) slot = i;
+  if (slot < 0) {
+    if (used == kFoldSlots) return nullptr;  // more concurrent BN streams than slots: caller folds separately
+    owners[used] = st;
+    slot = used++;
+  }
+  return base + slot * 4;
+}
+
 // The fused fold+apply stalls every block until the fold is done (a few us); that only beats a separate
 // finalize launch (~4 us of step time each) when the apply itself is long: ResNet-50's 56x56x256 layers
 // (8.3k vs 7.6k img/s) yes, ResNet-18's (2.61 vs 2.71 ms/step) no.
-bool fold_in_apply(uint64_t rows, int C) {
+bool fold_in_apply(uint64_t rows, int C, cudaStream_t st) {
+  if (!fold_counters(st)) return false;
   const char* e = getenv("NSK_BN_FOLD_APPLY");
   if (e) return e[0] == '1';
   return rows * (uint64_t)C >= (1ull << 25);
@@ -505,14 +527,7 @@ int check(uint64_t rows, int C, const void* a, const void* b) {
 
 // device address of the forward fold count, zeroed by the conv statistics epilogue (umma_gemm.cu) that feeds
 // nsk_bn_fwd_partials
-unsigned* nsk::bn_fold_counter_fwd() {
-  static unsigned* p = nullptr;
-  if (!p) {
-    void* a = nullptr;
-    if (cudaGetSymbolAddress(&a, g_fold_sync) == cudaSuccess) p = (unsigned*)a;
-  }
-  return p;
-}
+unsigned* nsk::bn_fold_counter_fwd(cudaStream_t st) { return fold_counters(st); }
 
 extern "C" {
 
@@ -532,9 +547,10 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   float* part = ws;
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
-  nsk::launch_pdl(bn_stats_kernel, nb, BT, smem, st, (const __nv_bfloat16*)x, rows, C, part);
+  unsigned* fc = fold_counters(st);
+  nsk::launch_pdl(bn_stats_kernel, nb, BT, smem, st, (const __nv_bfloat16*)x, rows, C, part, fc);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  if (!fold_in_apply(rows, C)) {
+  if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
     nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
@@ -545,7 +561,8 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   }
   nsk::launch_pdl(bn_apply_fold_kernel, fold_grid(nv, C), AT, 2 * C * sizeof(float), st, (const float*)part, nb, rows,
                   C, eps, gamma_beta, mean, invstd, running, momentum, scale, (const __nv_bfloat16*)x,
-                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C));
+                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C),
+                  fold_counters(st));
   NSK_LAUNCH_CHECK("bn_fwd");
   return NSK_OK;
 }
@@ -562,7 +579,7 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   float* scale = ws + (size_t)MAXBLK * 2 * C;
   float* shift = scale + C;
   const uint64_t nv = rows * (uint64_t)C / 8;
-  if (!fold_in_apply(rows, C)) {
+  if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
     nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
@@ -573,7 +590,8 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   }
   nsk::launch_pdl(bn_apply_fold_kernel, fold_grid(nv, C), AT, 2 * C * sizeof(float), st, partials, nparts, rows, C, eps,
                   gamma_beta, mean, invstd, running, momentum, scale, (const __nv_bfloat16*)x,
-                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C));
+                  (const __nv_bfloat16*)residual, (__nv_bfloat16*)y, (uint8_t*)relu_mask, relu, fold_blocks(C),
+                  fold_counters(st));
   NSK_LAUNCH_CHECK("bn_fwd_partials");
   return NSK_OK;
 }
@@ -615,10 +633,11 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   const size_t smem = 2 * (size_t)RPB * C * sizeof(float);
   float* part = ws;
   float* coef = ws + (size_t)MAXBLK * 2 * C;  // 3*C floats (workspace reserves 4*C)
+  unsigned* fc = fold_counters(st);
   nsk::launch_pdl(bn_bwd_reduce_kernel, nb, BT, smem, st, (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
-                                             (const uint8_t*)relu_mask, rows, C, part);
+                  (const uint8_t*)relu_mask, rows, C, part, fc ? fc + 2 : nullptr);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  if (!fold_in_apply(rows, C)) {
+  if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, gamma_beta, mean, invstd,
                     dgamma_beta, beta_acc, coef);
     nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)dy,
@@ -630,7 +649,7 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   nsk::launch_pdl(bn_bwd_apply_fold_kernel, fold_grid(nv, C), AT, 3 * C * sizeof(float), st, (const float*)part, nb,
                   rows, C, gamma_beta, mean, invstd, dgamma_beta, beta_acc, coef, (const __nv_bfloat16*)dy,
                   (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres,
-                  fold_blocks(C));
+                  fold_blocks(C), fold_counters(st) + 2);
   NSK_LAUNCH_CHECK("bn_bwd");
   return NSK_OK;
 }

@@ -55,7 +55,7 @@ int encode_tmap_im2col(CUtensorMap* map, const void* gaddr, int N, int H, int W,
 // NSK_PDL=0 turns the attribute off (plain stream order).
 bool pdl_enabled();
 // device word counting the channels folded by a fused BatchNorm apply (bn.cu); producers of its partials zero it
-unsigned* bn_fold_counter_fwd();
+unsigned* bn_fold_counter_fwd(cudaStream_t st);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -1329,7 +1329,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
     if (stats_floats < (uint64_t)2 * nsk::sm_count() * 2 * d->K)
       return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
     p.stats = stats;
-    p.fold_reset = nsk::bn_fold_counter_fwd();
+    p.fold_reset = nsk::bn_fold_counter_fwd((cudaStream_t)stream);
   }
   if (splits > 1) return conv_split_run(p, ma, mb, splits, fsteps, y, 0.f, stats, nparts, (cudaStream_t)stream);
   CUtensorMap mc;

@@ -185,13 +185,20 @@ class ResNet50:
         pool = self.s.pool
         blk = self.blocks[i]
         st = blk["stride"]
-        # projection shortcut first: its (stride-2) dgrad then accumulates into dx last and skips tapless classes
+        # projection shortcut first: its (stride-2) dgrad then accumulates into dx last and skips tapless classes.
+        # Its forward is an independent branch on the side stream, beside conv1 and conv2 (side.py)
         if "wsc" in blk:
+            fork = SIDE.enabled()
+            if fork:
+                SIDE.branch_begin()
             sc = layers.conv_bn(h, blk["wsc"], blk["bnsc"], st, 0, pool, relu=False, training=train)
+            if fork:
+                SIDE.branch_end()
         else:
             sc = h
         o = layers.conv_bn(h, blk["w1"], blk["bn1"], 1, 0, pool, relu=True, training=train)
         o = layers.conv_bn(o, blk["w2"], blk["bn2"], st, 1, pool, relu=True, training=train)
+        SIDE.branch_join()
         return layers.conv_bn(o, blk["w3"], blk["bn3"], 1, 0, pool, relu=True, residual=sc, training=train)
 
     def forward(self, x_nchw: Tensor, train: bool = True) -> Tensor:
