@@ -523,3 +523,43 @@ def test_conv2d_dgrad_accumulates_in_place(dev, case):
     got = bufs["dx"].host().reshape(dx0.shape)
     ref = dx0.astype(np.float64) + X.round_bf16(X.conv2d_dgrad(dy, wt, dx0.shape, st, pad))
     assert rel(got, X.round_bf16(ref)) < 1e-3
+
+
+@pytest.mark.parametrize("case", [(16, 4, 4, 512, 512, 3, 1, 1), (64, 4, 4, 512, 512, 3, 1, 1)])
+def test_conv_split_k_matches_unsplit(dev, case, monkeypatch):
+    """Split-K conv passes (few output tiles, long reduction: 256-wide tiles + fixed-order fold that also
+    writes the BN statistics partials) against the unsplit kernels: outputs and folded statistics agree to
+    bf16 rounding (the two sum the same products in different orders)."""
+    import ctypes as C
+
+    from paper_2409_11600_b200 import _lib
+    from paper_2409_11600_b200._lib import BF16, F32, ConvDesc
+    from paper_2409_11600_b200.tensor import Buffer
+
+    n, h, w, c, k, r, st, pad = case
+    p = (h + 2 * pad - r) // st + 1
+    rng = np.random.default_rng(sum(case))
+    x = X.round_bf16(rng.standard_normal((n, h, w, c)))
+    wt = X.round_bf16(rng.standard_normal((k, r, r, c)) / np.sqrt(r * r * c))
+    lib = _lib.lib()
+    d = ConvDesc(n, h, w, c, k, r, r, st, pad, p, p)
+    xb, wb, yb, dxb = Buffer(x.size, BF16), Buffer(wt.size, BF16), Buffer(n * p * p * k, BF16), Buffer(x.size, BF16)
+    xb.upload(x)
+    wb.upload(wt)
+    nst = int(lib.nsk_conv2d_stats_floats(k)) if hasattr(lib, "nsk_conv2d_stats_floats") else 4 * 148 * 2 * k + 8 * k
+    parts = Buffer(nst, F32)
+    out = {}
+    for split in ("1", "0"):
+        monkeypatch.setenv("NSK_CONV_SPLIT", split)
+        npart = C.c_int(0)
+        _lib.check(lib.nsk_conv2d_fprop_stats(C.byref(d), xb.ptr, wb.ptr, yb.ptr, parts.ptr, nst, C.byref(npart),
+                                               _lib.stream()))
+        y = yb.host().reshape(n, p, p, k).astype(np.float64)
+        stats = parts.host()[: npart.value * 2 * k].reshape(npart.value, 2, k).astype(np.float64).sum(0)
+        _lib.check(lib.nsk_conv2d_dgrad(C.byref(d), yb.ptr, wb.ptr, dxb.ptr, _lib.stream()))
+        out[split] = (y, stats, dxb.host().astype(np.float64).reshape(x.shape))
+    ys, ss, ds = out["1"]
+    yu, su, du = out["0"]
+    assert rel(ys, yu) < 4e-3 and rel(ss, su) < 4e-3
+    assert rel(ds, X.round_bf16(X.conv2d_dgrad(yu.astype(np.float32), wt, x.shape, st, pad))) < 1e-2
+    assert rel(ds, du) < 4e-3
