@@ -789,6 +789,163 @@ __global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float* __restri
   *d = t;
 }
 
+
+// ---- row-reuse weight gradient for 3x3 / stride 1 / 64 -> 64 channels on 32-wide images ----
+// dW[co][tap][ci] = sum_pix dy[pix][co] x[pix + tap][ci]. One work unit = a range of 64-pixel k-steps (two image
+// rows) for ALL nine taps: per k-step three 4-row x boxes (one per column offset dw, rows h-1..h+2, 16 KB each)
+// serve the three row offsets dh as K-views shifted by whole rows (32 pixels = 4 KB, a multiple of the 1 KB
+// swizzle atom), and the dy box (8 KB) is loaded once for all taps -- 56 KB per k-step instead of 5 x 24 KB.
+// M = 9 taps x 64 channels is issued as five 128-row MMA tiles whose two 64-channel atoms sit at a per-tile
+// leading-byte offset: (dh -1, dh +1) of one box (8 KB apart) x3, (dh 0 of dw -1, dh 0 of dw 0) across two
+// boxes (16 KB), and (dh 0 of dw +1, unused). Five TMEM accumulators (320 columns), fp32 partials per unit
+// into ws[split][co][Mpad] (rows m = tap * 64 + ci), folded by wgrad_reduce_kernel.
+struct WgrrProb {
+  int k_steps, per, units;
+  int HW, Wimg;  // pixels per image, image width (32)
+  float* ws;
+  int Mpad;
+};
+constexpr int kWgrrStages = 3;
+constexpr int kWgrrStage = 3 * 16384 + 8192;
+__constant__ signed char c_wgrr_tap[5][2] = {{0, 6}, {1, 7}, {2, 8}, {3, 4}, {5, -1}};
+
+__global__ void __launch_bounds__(256, 1) wgrad_rr64_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                            const __grid_constant__ CUtensorMap tmDY,
+                                                            const WgrrProb p) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + kWgrrStages * kWgrrStage);
+  uint64_t* empty = full + kWgrrStages;
+  uint64_t* tfull = empty + kWgrrStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWgrrStages; ++s) {
+      mbar_init(&full[s], 2);  // two producer threads arrive per stage
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmDY);
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if ((warp == 0 || warp == 2) && lane == 0) {
+    // producers: warp 0 the dw = -1 box and dy, warp 2 the dw = 0 and +1 boxes
+    int i = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int kb = u * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk, ++i) {
+        const int s = i % kWgrrStages;
+        if (i >= kWgrrStages) mbar_wait_backoff(&empty[s], ((i / kWgrrStages) - 1) & 1);
+        uint8_t* st = smem + s * kWgrrStage;
+        const int pix0 = kk * 64;
+        const int n = pix0 / p.HW;
+        const int hh = (pix0 - n * p.HW) / p.Wimg;
+        if (warp == 0) {
+          mbar_expect_tx(&full[s], 16384 + 8192);
+          tma_load_4d(&tmX, &full[s], st, 0, -1, hh - 1, n);
+          tma_load_2d(&tmDY, &full[s], st + 3 * 16384, 0, pix0);
+        } else {
+          mbar_expect_tx(&full[s], 2 * 16384);
+          tma_load_4d(&tmX, &full[s], st + 16384, 0, 0, hh - 1, n);
+          tma_load_4d(&tmX, &full[s], st + 2 * 16384, 0, 1, hh - 1, n);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    // gate: mbarrier waits on behalf of the MMA warp (released through named barriers)
+    int i = 0, j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      if (j >= 1) {
+        mbar_wait(tempty, (j - 1) & 1);
+        gate_arrive(kBarAcc);
+      }
+      const int kb = u * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk, ++i) {
+        const int s = i % kWgrrStages;
+        mbar_wait(&full[s], (i / kWgrrStages) & 1);
+        gate_arrive(kBarFull + s);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(1u, 1u, 1u, 128u, 64u);
+    const uint32_t smem0 = smem_u32(smem);
+    int s = 0, j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      if (j >= 1) gate_sync(kBarAcc);
+      tc_fence_after();
+      const int kb = u * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk) {
+        gate_sync(kBarFull + s);
+        tc_fence_after();
+        const uint32_t st = smem0 + s * kWgrrStage;
+        const uint64_t b0 = sdesc_sw128(st + 3 * 16384, 8192, 1024);
+        const uint64_t t0 = sdesc_sw128(st, 8192, 1024), t1 = sdesc_sw128(st + 16384, 8192, 1024);
+        const uint64_t t2 = sdesc_sw128(st + 2 * 16384, 8192, 1024), t3 = sdesc_sw128(st + 4096, 16384, 1024);
+        const uint64_t t4 = sdesc_sw128(st + 2 * 16384 + 4096, 8192, 1024);
+        if (elect_one()) {
+          const bool acc = kk > kb;
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 0 * 64, t0, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 1 * 64, t1, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 2 * 64, t2, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 3 * 64, t3, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 4 * 64, t4, b0, idesc, acc);
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == kWgrrStages) s = 0;
+      }
+      if (elect_one()) umma_commit(tfull);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // accumulator row: atom r / 64, input channel r % 64
+    const int atom = r >> 6, ci = r & 63;
+    int j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      mbar_wait_backoff(tfull, j & 1);
+      tc_fence_after();
+      float* out = p.ws + (size_t)u * 64 * p.Mpad;
+#pragma unroll 1
+      for (int T = 0; T < 5; ++T) {
+        const int tap = c_wgrr_tap[T][atom];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + T * 64 + c * 32, v);
+          tmem_ld_wait();
+          if (tap >= 0) {
+            float* o = out + (size_t)(c * 32) * p.Mpad + tap * 64 + ci;
+#pragma unroll
+            for (int t = 0; t < 32; ++t) o[(size_t)t * p.Mpad] = __uint_as_float(v[t]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
 // split-K conv fold: y[m, :] = bf16(sum_z ws[z][m][:] (+ beta * y[m, :])) in split order, 8 channels per thread;
 // with `stats`, also per-block channel partials [gridDim.x][2][N] (sum, sum of squares of the stored bf16 values)
 // for the BatchNorm consuming y (nsk_bn_fwd_partials), as the conv epilogue would have written them.
@@ -1181,6 +1338,13 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   return NSK_OK;
 }
 
+bool wgrad_rr64_ok(const NskConvDesc* d) {
+  const char* e = getenv("NSK_WGRAD_RR");
+  if (e && e[0] == '0') return false;
+  return d->C == 64 && d->K == 64 && d->R == 3 && d->S == 3 && d->stride == 1 && d->pad == 1 && d->W == 32 &&
+         d->Q == 32 && d->H == d->P && d->H % 2 == 0 && ((long long)d->N * d->P * d->Q) % 64 == 0;
+}
+
 int check_desc(const NskConvDesc* d) {
   if (d->N < 1 || d->H < 1 || d->W < 1 || d->C < 1 || d->K < 1 || d->R < 1 || d->S < 1 || d->stride < 1)
     return nsk::set_error(NSK_ERR_SHAPE, "conv2d: invalid descriptor");
@@ -1476,6 +1640,13 @@ int nsk_wgrad_grid_cap(int ctas) {
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
+  if (wgrad_rr64_ok(d)) {  // one split per SM (wgrad_rr64_kernel): 640 x 64 fp32 partials each
+    const long long pix = (long long)d->N * d->P * d->Q;
+    const int k_steps = (int)(pix / 64);
+    int splits = nsk::sm_count();
+    if (splits > k_steps / 8) splits = k_steps / 8;
+    return (uint64_t)(splits < 1 ? 1 : splits) * 640 * 64 * sizeof(float);
+  }
   const int M = d->R * d->S * d->C;
   const int Mpad = ((M + 127) / 128) * 128;
   const long long pix = (long long)d->N * d->P * d->Q;
@@ -1496,6 +1667,57 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
                      uint64_t ws_bytes, void* stream) {
   int rc = check_desc(d);
   if (rc) return rc;
+  if (wgrad_rr64_ok(d)) {
+    const long long npix = (long long)d->N * d->P * d->Q;
+    const int k_steps = (int)(npix / 64);
+    int splits = (int)(ws_bytes / (640ull * 64 * sizeof(float)));
+    if (splits > nsk::sm_count()) splits = nsk::sm_count();
+    if (splits > k_steps / 8) splits = k_steps / 8;
+    if (splits >= 1) {
+      const int per = (k_steps + splits - 1) / splits;
+      splits = (k_steps + per - 1) / per;
+      CUtensorMap mx, mdy;
+      if ((rc = nhwc_map(&mx, x, d->N, d->H, d->W, 64, 64, 32, 4, 1, 1))) return rc;
+      {
+        uint64_t dims[2] = {64, (uint64_t)npix};
+        uint64_t str[1] = {64 * 2};
+        uint32_t box[2] = {64, 64};
+        if ((rc = nsk::encode_tmap(&mdy, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dy, dims, str, box, nullptr,
+                                   CU_TENSOR_MAP_SWIZZLE_128B)))
+          return rc;
+      }
+      WgrrProb q{};
+      q.k_steps = k_steps;
+      q.per = per;
+      q.units = splits;
+      q.HW = d->H * d->W;
+      q.Wimg = d->W;
+      q.ws = (float*)ws;
+      q.Mpad = 640;
+      const int smem = kWgrrStages * kWgrrStage + 1024 + 256;
+      static bool configured = false;
+      if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(wgrad_rr64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(wgrad_rr64)");
+        configured = true;
+      }
+      int grid = splits;
+      if (grid > nsk::sm_count()) grid = nsk::sm_count();
+      nsk::launch_pdl(wgrad_rr64_kernel, grid, 256, smem, (cudaStream_t)stream, mx, mdy, q);
+      NSK_LAUNCH_CHECK("wgrad_rr64_kernel");
+      const long long total = 576LL * 64;
+      if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
+        return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: dw and workspace must be 16-byte aligned");
+      if (total / 4 < (long long)nsk::sm_count() * 512 && splits >= 16)
+        nsk::launch_pdl(wgrad_reduce_kernel<8>, (unsigned)((total / 4 + 31) / 32), dim3(32, 8), 0,
+                        (cudaStream_t)stream, (const float*)ws, splits, 640, 576, 64, dw, beta);
+      else
+        nsk::launch_pdl(wgrad_reduce_kernel<1>, (unsigned)((total / 4 + 255) / 256), dim3(256, 1), 0,
+                        (cudaStream_t)stream, (const float*)ws, splits, 640, 576, 64, dw, beta);
+      NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
+      return NSK_OK;
+    }
+  }
   const int P = d->P, Q = d->Q;
   int Wt = 0, Ht = 0, Nt = 0;
   const long long pix = (long long)d->N * P * Q;
