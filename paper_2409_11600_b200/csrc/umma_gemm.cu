@@ -946,6 +946,151 @@ __global__ void __launch_bounds__(256, 1) wgrad_rr64_kernel(const __grid_constan
   }
 }
 
+
+// Row-reuse weight gradient for 3x3 / stride 1 / 128 -> 128 channels on 16-wide images. Nine 128-row tiles do not
+// fit TMEM at N = 128, so a work unit is (column offset dw, range of k-steps): per 64-pixel k-step (4 rows) two
+// 6-row x boxes (the two 64-channel halves, 12 KB each) serve the three row offsets dh as K views shifted by
+// 16 pixels (2 KB), dy (both 64-wide halves of the 128 outputs) is one 16 KB load; three 128x128 tiles (one per
+// dh; atoms = the two channel halves, 12 KB apart) accumulate in TMEM. 40 KB per k-step for 12 MMAs of N = 128,
+// against 32 KB per 4 MMAs in the generic tiling.
+constexpr int kWg128Stages = 4;
+constexpr int kWg128Stage = 2 * 12288 + 16384;
+
+__global__ void __launch_bounds__(256, 1) wgrad_rr128_kernel(const __grid_constant__ CUtensorMap tmX,
+                                                             const __grid_constant__ CUtensorMap tmDY,
+                                                             const WgrrProb p) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + kWg128Stages * kWg128Stage);
+  uint64_t* empty = full + kWg128Stages;
+  uint64_t* tfull = empty + kWg128Stages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kWg128Stages; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 4);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmDY);
+  }
+  if (warp == 2) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  if ((warp == 0 || warp == 2) && lane == 0) {
+    // warp 0: channel half 0 and dy; warp 2: channel half 1
+    int i = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const int dw = u % 3 - 1, z = u / 3;
+      const int kb = z * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk, ++i) {
+        const int s = i % kWg128Stages;
+        if (i >= kWg128Stages) mbar_wait_backoff(&empty[s], ((i / kWg128Stages) - 1) & 1);
+        uint8_t* st = smem + s * kWg128Stage;
+        const int pix0 = kk * 64;
+        const int n = pix0 / p.HW;
+        const int hh = (pix0 - n * p.HW) / p.Wimg;
+        if (warp == 0) {
+          mbar_expect_tx(&full[s], 12288 + 16384);
+          tma_load_4d(&tmX, &full[s], st, 0, dw, hh - 1, n);
+          tma_load_3d(&tmDY, &full[s], st + 2 * 12288, 0, pix0, 0);
+        } else {
+          mbar_expect_tx(&full[s], 12288);
+          tma_load_4d(&tmX, &full[s], st + 12288, 64, dw, hh - 1, n);
+        }
+      }
+    }
+  } else if (warp == 3) {
+    int i = 0, j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      if (j >= 1) {
+        mbar_wait(tempty, (j - 1) & 1);
+        gate_arrive(kBarAcc);
+      }
+      const int z = u / 3;
+      const int kb = z * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk, ++i) {
+        const int s = i % kWg128Stages;
+        mbar_wait(&full[s], (i / kWg128Stages) & 1);
+        gate_arrive(kBarFull + s);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(1u, 1u, 1u, 128u, 128u);
+    const uint32_t smem0 = smem_u32(smem);
+    int s = 0, j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      if (j >= 1) gate_sync(kBarAcc);
+      tc_fence_after();
+      const int z = u / 3;
+      const int kb = z * p.per, ke = min(p.k_steps, kb + p.per);
+      for (int kk = kb; kk < ke; ++kk) {
+        gate_sync(kBarFull + s);
+        tc_fence_after();
+        const uint32_t st = smem0 + s * kWg128Stage;
+        const uint64_t b0 = sdesc_sw128(st + 2 * 12288, 8192, 1024);  // two 64-wide output halves, 8 KB apart
+        const uint64_t a0 = sdesc_sw128(st, 12288, 1024);             // dh = -1: rows 0..63 of both halves
+        const uint64_t a1 = sdesc_sw128(st + 2048, 12288, 1024);      // dh =  0: rows 16..79
+        const uint64_t a2 = sdesc_sw128(st + 4096, 12288, 1024);      // dh = +1: rows 32..95
+        if (elect_one()) {
+          const bool acc = kk > kb;
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 0 * 128, a0, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 1 * 128, a1, b0, idesc, acc);
+          mma_slab_at<0, 0, 2048, 2048, false>(tmem_base + 2 * 128, a2, b0, idesc, acc);
+          umma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == kWg128Stages) s = 0;
+      }
+      if (elect_one()) umma_commit(tfull);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const int ci = (r >> 6) * 64 + (r & 63);  // atom = channel half
+    int j = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++j) {
+      const int dw = u % 3, z = u / 3;
+      mbar_wait_backoff(tfull, j & 1);
+      tc_fence_after();
+      float* out = p.ws + (size_t)z * 128 * p.Mpad;
+#pragma unroll 1
+      for (int T = 0; T < 3; ++T) {
+        const int tap = T * 3 + dw;  // (dh + 1) * 3 + (dw + 1)
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + T * 128 + c * 32, v);
+          tmem_ld_wait();
+          float* o = out + (size_t)(c * 32) * p.Mpad + tap * 128 + ci;
+#pragma unroll
+          for (int t = 0; t < 32; ++t) o[(size_t)t * p.Mpad] = __uint_as_float(v[t]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
 // split-K conv fold: y[m, :] = bf16(sum_z ws[z][m][:] (+ beta * y[m, :])) in split order, 8 channels per thread;
 // with `stats`, also per-block channel partials [gridDim.x][2][N] (sum, sum of squares of the stored bf16 values)
 // for the BatchNorm consuming y (nsk_bn_fwd_partials), as the conv epilogue would have written them.
@@ -1338,6 +1483,13 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   return NSK_OK;
 }
 
+bool wgrad_rr128_ok(const NskConvDesc* d) {
+  const char* e = getenv("NSK_WGRAD_RR");
+  if (e && (e[0] == '0' || e[0] == '1')) return e[0] != '0' && e[1] != '6';  // "64": the 64-channel path only
+  return d->C == 128 && d->K == 128 && d->R == 3 && d->S == 3 && d->stride == 1 && d->pad == 1 && d->W == 16 &&
+         d->Q == 16 && d->H == d->P && d->H % 4 == 0 && ((long long)d->N * d->P * d->Q) % 64 == 0;
+}
+
 bool wgrad_rr64_ok(const NskConvDesc* d) {
   const char* e = getenv("NSK_WGRAD_RR");
   if (e && e[0] == '0') return false;
@@ -1640,6 +1792,12 @@ int nsk_wgrad_grid_cap(int ctas) {
 }
 
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d) {
+  if (wgrad_rr128_ok(d)) {  // three column-offset units per split, ~one unit per SM
+    const int k_steps = (int)((long long)d->N * d->P * d->Q / 64);
+    int splits = nsk::sm_count() / 3;
+    if (splits > k_steps / 8) splits = k_steps / 8;
+    return (uint64_t)(splits < 1 ? 1 : splits) * 1152 * 128 * sizeof(float);
+  }
   if (wgrad_rr64_ok(d)) {  // one split per SM (wgrad_rr64_kernel): 640 x 64 fp32 partials each
     const long long pix = (long long)d->N * d->P * d->Q;
     const int k_steps = (int)(pix / 64);
@@ -1667,6 +1825,57 @@ int nsk_conv2d_wgrad(const NskConvDesc* d, const void* x, const void* dy, float*
                      uint64_t ws_bytes, void* stream) {
   int rc = check_desc(d);
   if (rc) return rc;
+  if (wgrad_rr128_ok(d)) {
+    const long long npix = (long long)d->N * d->P * d->Q;
+    const int k_steps = (int)(npix / 64);
+    int splits = (int)(ws_bytes / (1152ull * 128 * sizeof(float)));
+    if (splits > nsk::sm_count() / 3) splits = nsk::sm_count() / 3;
+    if (splits > k_steps / 8) splits = k_steps / 8;
+    if (splits >= 1) {
+      const int per = (k_steps + splits - 1) / splits;
+      splits = (k_steps + per - 1) / per;
+      CUtensorMap mx, mdy;
+      if ((rc = nhwc_map(&mx, x, d->N, d->H, d->W, 128, 64, 16, 6, 1, 1))) return rc;
+      {  // dy as {64 outputs, pixels, 2 halves (128 B apart)}: both 64-wide N atoms in one box, 8 KB apart
+        uint64_t dims[3] = {64, (uint64_t)npix, 2};
+        uint64_t str[2] = {128 * 2, 128};
+        uint32_t box[3] = {64, 64, 2};
+        if ((rc = nsk::encode_tmap(&mdy, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, dy, dims, str, box, nullptr,
+                                   CU_TENSOR_MAP_SWIZZLE_128B)))
+          return rc;
+      }
+      WgrrProb q{};
+      q.k_steps = k_steps;
+      q.per = per;
+      q.units = 3 * splits;
+      q.HW = d->H * d->W;
+      q.Wimg = d->W;
+      q.ws = (float*)ws;
+      q.Mpad = 1152;
+      const int smem = kWg128Stages * kWg128Stage + 1024 + 256;
+      static bool configured = false;
+      if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(wgrad_rr128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return nsk::cuda_status(e, "cudaFuncSetAttribute(wgrad_rr128)");
+        configured = true;
+      }
+      int grid = q.units;
+      if (grid > nsk::sm_count()) grid = nsk::sm_count();
+      nsk::launch_pdl(wgrad_rr128_kernel, grid, 256, smem, (cudaStream_t)stream, mx, mdy, q);
+      NSK_LAUNCH_CHECK("wgrad_rr128_kernel");
+      const long long total = 1152LL * 128;
+      if (((uintptr_t)dw & 15) || ((uintptr_t)ws & 15))
+        return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d wgrad: dw and workspace must be 16-byte aligned");
+      if (total / 4 < (long long)nsk::sm_count() * 512 && splits >= 16)
+        nsk::launch_pdl(wgrad_reduce_kernel<8>, (unsigned)((total / 4 + 31) / 32), dim3(32, 8), 0,
+                        (cudaStream_t)stream, (const float*)ws, splits, 1152, 1152, 128, dw, beta);
+      else
+        nsk::launch_pdl(wgrad_reduce_kernel<1>, (unsigned)((total / 4 + 255) / 256), dim3(256, 1), 0,
+                        (cudaStream_t)stream, (const float*)ws, splits, 1152, 1152, 128, dw, beta);
+      NSK_LAUNCH_CHECK("wgrad_reduce_kernel");
+      return NSK_OK;
+    }
+  }
   if (wgrad_rr64_ok(d)) {
     const long long npix = (long long)d->N * d->P * d->Q;
     const int k_steps = (int)(npix / 64);
