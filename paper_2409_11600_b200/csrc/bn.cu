@@ -151,16 +151,26 @@ __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __res
                                                       __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
                                                       uint64_t rows, int C, int relu) {
   pdl_wait();
+  extern __shared__ float ss[];  // [2][C] scale, shift (float4 reads instead of 16 scalar global loads)
+  for (int k = threadIdx.x; k < C; k += BT) {
+    ss[k] = scale[k];
+    ss[C + k] = shift[k];
+  }
+  __syncthreads();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
     const int c0 = (int)(i % CV) * 8;
-    float f[8], r[8];
+    float f[8], r[8], sc[8], sh[8];
     ld8(x + i * 8, f);
     if (res) ld8(res + i * 8, r);
+    *(float4*)sc = *(const float4*)(ss + c0);
+    *(float4*)(sc + 4) = *(const float4*)(ss + c0 + 4);
+    *(float4*)sh = *(const float4*)(ss + C + c0);
+    *(float4*)(sh + 4) = *(const float4*)(ss + C + c0 + 4);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float v = f[j] * scale[c0 + j] + shift[c0 + j];
+      float v = f[j] * sc[j] + sh[j];
       if (res) v += r[j];
       if (relu) v = v > 0.f ? v : 0.f;
       f[j] = v;
@@ -264,6 +274,11 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ dx,
                                                           __nv_bfloat16* __restrict__ dres, uint64_t rows, int C) {
   pdl_wait();
+  // per-channel coefficients staged in shared memory and read as float4 (24 scalar global loads per 8 elements
+  // made the pass load-instruction bound)
+  extern __shared__ float cf[];  // [3][C]
+  for (int k = threadIdx.x; k < 3 * C; k += BT) cf[k] = coef[k];
+  __syncthreads();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
@@ -277,9 +292,16 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
       for (int j = 0; j < 8; ++j) g[j] = ((m >> j) & 1u) ? g[j] : 0.f;
     }
     if (dres) st8(dres + i * 8, g);
+    float a[8], b[8], cc[8];
+    *(float4*)a = *(const float4*)(cf + c0);
+    *(float4*)(a + 4) = *(const float4*)(cf + c0 + 4);
+    *(float4*)b = *(const float4*)(cf + C + c0);
+    *(float4*)(b + 4) = *(const float4*)(cf + C + c0 + 4);
+    *(float4*)cc = *(const float4*)(cf + 2 * C + c0);
+    *(float4*)(cc + 4) = *(const float4*)(cf + 2 * C + c0 + 4);
     float o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = coef[c0 + j] * g[j] + coef[C + c0 + j] * xv[j] + coef[2 * C + c0 + j];
+    for (int j = 0; j < 8; ++j) o[j] = a[j] * g[j] + b[j] * xv[j] + cc[j];
     st8(dx + i * 8, o);
   }
 }
@@ -553,7 +575,7 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
-    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                     (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
                     (uint8_t*)relu_mask, rows, C, relu);
     NSK_LAUNCH_CHECK("bn_fwd");
@@ -582,7 +604,7 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
-    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                     (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
                     (uint8_t*)relu_mask, rows, C, relu);
     NSK_LAUNCH_CHECK("bn_fwd_partials");
@@ -616,7 +638,7 @@ int nsk_bn_fwd_eval(const void* x, const float* gamma_beta, const float* running
   float* shift = scale + C;
   nsk::launch_pdl(bn_eval_affine_kernel, (C + 127) / 128, 128, 0, st, gamma_beta, running, C, eps, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)x,
+  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                   (const __nv_bfloat16*)residual, scale, shift, (__nv_bfloat16*)y, (uint8_t*)nullptr, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd_eval");
   return NSK_OK;
@@ -640,7 +662,7 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, gamma_beta, mean, invstd,
                     dgamma_beta, beta_acc, coef);
-    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 0, st, (const __nv_bfloat16*)dy,
+    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 3 * C * sizeof(float), st, (const __nv_bfloat16*)dy,
                     (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (const float*)coef, (__nv_bfloat16*)dx,
                     (__nv_bfloat16*)dres, rows, C);
     NSK_LAUNCH_CHECK("bn_bwd");
