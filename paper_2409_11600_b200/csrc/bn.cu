@@ -408,12 +408,16 @@ __global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, in
   const int CV = C / 8;
   for (uint64_t i = (uint64_t)blockIdx.x * AT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * AT) {
     const int c0 = (int)(i % CV) * 8;
-    float f[8], r[8];
+    float f[8], r[8], sc[8], sh[8];
     ld8(x + i * 8, f);
     if (res) ld8(res + i * 8, r);
+    *(float4*)sc = *(const float4*)(scale + c0);
+    *(float4*)(sc + 4) = *(const float4*)(scale + c0 + 4);
+    *(float4*)sh = *(const float4*)(shift + c0);
+    *(float4*)(sh + 4) = *(const float4*)(shift + c0 + 4);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      float v = f[j] * scale[c0 + j] + shift[c0 + j];
+      float v = f[j] * sc[j] + sh[j];
       if (res) v += r[j];
       if (relu) v = v > 0.f ? v : 0.f;
       f[j] = v;
@@ -479,9 +483,16 @@ __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part
       for (int j = 0; j < 8; ++j) g[j] = ((m >> j) & 1u) ? g[j] : 0.f;
     }
     if (dres) st8(dres + i * 8, g);
+    float a[8], b[8], cc[8];
+    *(float4*)a = *(const float4*)(coef + c0);
+    *(float4*)(a + 4) = *(const float4*)(coef + c0 + 4);
+    *(float4*)b = *(const float4*)(coef + C + c0);
+    *(float4*)(b + 4) = *(const float4*)(coef + C + c0 + 4);
+    *(float4*)cc = *(const float4*)(coef + 2 * C + c0);
+    *(float4*)(cc + 4) = *(const float4*)(coef + 2 * C + c0 + 4);
     float o[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[j] = coef[c0 + j] * g[j] + coef[C + c0 + j] * xv[j] + coef[2 * C + c0 + j];
+    for (int j = 0; j < 8; ++j) o[j] = a[j] * g[j] + b[j] * xv[j] + cc[j];
     st8(dx + i * 8, o);
   }
 }
