@@ -220,7 +220,33 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
-  for (uint64_t r = (uint64_t)blockIdx.x * RPB + ro; r < rows; r += (uint64_t)gridDim.x * RPB) {
+  const uint64_t stride = (uint64_t)gridDim.x * RPB;
+  uint64_t r = (uint64_t)blockIdx.x * RPB + ro;
+  // two rows in flight per thread (same accumulation order as one at a time)
+  for (; r + stride < rows; r += 2 * stride) {
+    const uint64_t o0 = r * C + cv * 8, o1 = (r + stride) * C + cv * 8;
+    float g0[8], x0[8], g1[8], x1[8];
+    ld8(dy + o0, g0);
+    ld8(x + o0, x0);
+    ld8(dy + o1, g1);
+    ld8(x + o1, x1);
+    if (mask) {
+      const unsigned m0 = __ldg(mask + o0 / 8), m1 = __ldg(mask + o1 / 8);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        g0[j] = ((m0 >> j) & 1u) ? g0[j] : 0.f;
+        g1[j] = ((m1 >> j) & 1u) ? g1[j] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s1[j] += g0[j];
+      s2[j] += g0[j] * x0[j];
+      s1[j] += g1[j];
+      s2[j] += g1[j] * x1[j];
+    }
+  }
+  if (r < rows) {
     const uint64_t off = r * C + cv * 8;
     float g[8], xv[8];
     ld8(dy + off, g);
