@@ -159,8 +159,12 @@ __global__ void __launch_bounds__(BT) bn_apply_kernel(const __nv_bfloat16* __res
   __syncthreads();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
-  for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
-    const int c0 = (int)(i % CV) * 8;
+  // channel group carried incrementally (no 64-bit modulo per iteration)
+  const uint64_t i0 = (uint64_t)blockIdx.x * BT + threadIdx.x, istep = (uint64_t)gridDim.x * BT;
+  int cvi = (int)(i0 % CV);
+  const int cstep = (int)(istep % CV);
+  for (uint64_t i = i0; i < nv; i += istep, cvi = (cvi + cstep >= CV) ? cvi + cstep - CV : cvi + cstep) {
+    const int c0 = cvi * 8;
     float f[8], r[8], sc[8], sh[8];
     ld8(x + i * 8, f);
     if (res) ld8(res + i * 8, r);
@@ -307,8 +311,12 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
   __syncthreads();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
-  for (uint64_t i = (uint64_t)blockIdx.x * BT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * BT) {
-    const int c0 = (int)(i % CV) * 8;
+  // channel group carried incrementally (no 64-bit modulo per iteration)
+  const uint64_t i0 = (uint64_t)blockIdx.x * BT + threadIdx.x, istep = (uint64_t)gridDim.x * BT;
+  int cvi = (int)(i0 % CV);
+  const int cstep = (int)(istep % CV);
+  for (uint64_t i = i0; i < nv; i += istep, cvi = (cvi + cstep >= CV) ? cvi + cstep - CV : cvi + cstep) {
+    const int c0 = cvi * 8;
     float g[8], xv[8];
     ld8(dy + i * 8, g);
     ld8(x + i * 8, xv);
@@ -432,8 +440,11 @@ __global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, in
   const float* shift = aff + C;
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
-  for (uint64_t i = (uint64_t)blockIdx.x * AT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * AT) {
-    const int c0 = (int)(i % CV) * 8;
+  const uint64_t i0 = (uint64_t)blockIdx.x * AT + threadIdx.x, istep = (uint64_t)gridDim.x * AT;
+  int cvi = (int)(i0 % CV);
+  const int cstep = (int)(istep % CV);
+  for (uint64_t i = i0; i < nv; i += istep, cvi = (cvi + cstep >= CV) ? cvi + cstep - CV : cvi + cstep) {
+    const int c0 = cvi * 8;
     float f[8], r[8], sc[8], sh[8];
     ld8(x + i * 8, f);
     if (res) ld8(res + i * 8, r);
@@ -498,8 +509,11 @@ __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part
   __syncthreads();
   const uint64_t nv = rows * (uint64_t)C / 8;
   const int CV = C / 8;
-  for (uint64_t i = (uint64_t)blockIdx.x * AT + threadIdx.x; i < nv; i += (uint64_t)gridDim.x * AT) {
-    const int c0 = (int)(i % CV) * 8;
+  const uint64_t i0 = (uint64_t)blockIdx.x * AT + threadIdx.x, istep = (uint64_t)gridDim.x * AT;
+  int cvi = (int)(i0 % CV);
+  const int cstep = (int)(istep % CV);
+  for (uint64_t i = i0; i < nv; i += istep, cvi = (cvi + cstep >= CV) ? cvi + cstep - CV : cvi + cstep) {
+    const int c0 = cvi * 8;
     float g[8], xv[8];
     ld8(dy + i * 8, g);
     ld8(x + i * 8, xv);
