@@ -59,12 +59,14 @@ __global__ void maxpool_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfl
   const int CV = C / 8;
   const long long n_out = (long long)N * P * Q * CV;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_out; i += (long long)gridDim.x * blockDim.x) {
-    const int cv = (int)(i % CV);
-    long long t = i / CV;
-    const int q = (int)(t % Q);
-    t /= Q;
-    const int p = (int)(t % P);
-    const long long n = t / P;
+    // 32-bit index arithmetic (the host checks N*P*Q*C/8 < 2^31): 64-bit divisions cost ~4x more
+    const unsigned iu = (unsigned)i;
+    const int cv = (int)(iu % (unsigned)CV);
+    unsigned t = iu / (unsigned)CV;
+    const int q = (int)(t % (unsigned)Q);
+    t /= (unsigned)Q;
+    const int p = (int)(t % (unsigned)P);
+    const long long n = t / (unsigned)P;
     float best[8];
     uint32_t at[8];
 #pragma unroll
@@ -118,12 +120,13 @@ __global__ void maxpool_bwd_kernel(const uint8_t* __restrict__ arg, const __nv_b
   const int CV = C / 8;
   const long long n_in = (long long)N * H * W * CV;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_in; i += (long long)gridDim.x * blockDim.x) {
-    const int cv = (int)(i % CV);
-    long long t = i / CV;
-    const int w = (int)(t % W);
-    t /= W;
-    const int h = (int)(t % H);
-    const long long n = t / H;
+    const unsigned iu = (unsigned)i;  // 32-bit index arithmetic (host-checked)
+    const int cv = (int)(iu % (unsigned)CV);
+    unsigned t = iu / (unsigned)CV;
+    const int w = (int)(t % (unsigned)W);
+    t /= (unsigned)W;
+    const int h = (int)(t % (unsigned)H);
+    const long long n = t / (unsigned)H;
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     // outputs p with p*st - pad <= h <= p*st - pad + k - 1
     int p_lo = h + pad - k + 1 <= 0 ? 0 : (h + pad - k + 1 + st - 1) / st;
@@ -351,6 +354,8 @@ int nsk_maxpool_fwd(const void* x, void* y, void* argmax, int N, int H, int W, i
   if (C % 8 || ((uintptr_t)x & 15) || ((uintptr_t)y & 15) || ((uintptr_t)argmax & 7) || k * k > 255)
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: C must be a multiple of 8, buffers aligned, k*k < 256");
   long long n = (long long)N * P * Q * C;
+  if ((long long)N * P * Q * (C / 8) >= (1ll << 31) || (long long)N * H * W * (C / 8) >= (1ll << 31))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: more than 2^31 channel groups");
   nsk::launch_pdl(maxpool_fwd_kernel, nsk::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream,
       (const __nv_bfloat16*)x, (__nv_bfloat16*)y, (uint8_t*)argmax, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_fwd");
@@ -362,6 +367,7 @@ int nsk_maxpool_bwd(const void* argmax, const void* dy, void* dx, int N, int H, 
   if (C % 8 || ((uintptr_t)dy & 15) || ((uintptr_t)dx & 15) || ((uintptr_t)argmax & 7))
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: C must be a multiple of 8, buffers aligned");
   long long n = (long long)N * H * W * C;
+  if (n / 8 >= (1ll << 31)) return nsk::set_error(NSK_ERR_UNSUPPORTED, "maxpool: more than 2^31 channel groups");
   nsk::launch_pdl(maxpool_bwd_kernel, nsk::grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream,
       (const uint8_t*)argmax, (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, N, H, W, C, k, stride, pad, P, Q);
   NSK_LAUNCH_CHECK("maxpool_bwd");
