@@ -71,7 +71,8 @@ class SmallCNNOracle:
         self.params = d.params
         self.opt = _Opt(self.params)
 
-    def loss_and_grads(self, x_nchw, y, bf16=False):
+    def loss_and_grads(self, x_nchw, y, bf16=False, acts=None):
+        """``acts`` (a dict) receives the activations h1, h2 (NHWC) and the logits."""
         q = X.round_bf16 if bf16 else (lambda a: np.asarray(a, np.float64))
         p = self.params
         x = q(np.transpose(x_nchw, (0, 2, 3, 1)))
@@ -85,10 +86,14 @@ class SmallCNNOracle:
         f = h2.reshape(h2.shape[0], -1)
         fcw = q(p["fc_w"]) if bf16 else p["fc_w"].astype(np.float64)
         logits = (f @ fcw.T).astype(np.float32) + p["fc_b"]
+        if acts is not None:
+            acts.update(h1=h1, h2=h2, logits=logits)
         loss, probs = R.cross_entropy(logits, y)
         g = R.cross_entropy_grad(probs, y).astype(np.float64)
         grads = {"fc_b": g.sum(axis=0)}
-        grads["fc_w"] = (q(g) if bf16 else g).T @ f
+        # the device keeps this weight gradient in float32 (10-wide gradient rows are not 16-byte aligned for the
+        # bf16 tensor-core path; tensor._matmul) and sums it exactly: no bf16 rounding of g here
+        grads["fc_w"] = g.T @ f
         df = q(g @ p["fc_w"].astype(np.float64))
         dh2 = df.reshape(h2.shape)
         da2 = dh2 * (a2 > 0)

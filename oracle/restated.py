@@ -57,26 +57,46 @@ def col2im(dcols, x_shape, R, S, stride, pad):
     return dxp[:, pad:pad + H, pad:pad + W, :]
 
 
+_CHUNK_ELEMS = 1 << 25  # im2col elements per chunk (256 MiB of float64): bench-size batches go image-block-wise
+
+
+def _image_chunks(n, per_image):
+    step = max(1, _CHUNK_ELEMS // max(1, per_image))
+    return [(i, min(n, i + step)) for i in range(0, n, step)]
+
+
 def conv2d_fwd(x, w, stride, pad):
     """y[n,p,q,k] = sum_{r,s,c} x[n, p*st-pad+r, q*st-pad+s, c] * w[k,r,s,c]  (float64)."""
-    N = x.shape[0]
+    N, H, W_, _ = x.shape
     K, R, S, C = w.shape
-    cols = im2col(x, R, S, stride, pad)
-    y = cols @ np.asarray(w, np.float64).reshape(K, -1).T
-    P, Q = conv_out(x.shape[1], R, stride, pad), conv_out(x.shape[2], S, stride, pad)
-    return y.reshape(N, P, Q, K)
+    P, Q = conv_out(H, R, stride, pad), conv_out(W_, S, stride, pad)
+    wm = np.asarray(w, np.float64).reshape(K, -1).T
+    y = np.empty((N, P, Q, K), np.float64)
+    for a, b in _image_chunks(N, P * Q * R * S * C):
+        y[a:b] = (im2col(x[a:b], R, S, stride, pad) @ wm).reshape(b - a, P, Q, K)
+    return y
 
 
 def conv2d_dgrad(dy, w, x_shape, stride, pad):
     K, R, S, C = w.shape
-    dcols = np.asarray(dy, np.float64).reshape(-1, K) @ np.asarray(w, np.float64).reshape(K, -1)
-    return col2im(dcols, x_shape, R, S, stride, pad)
+    N = x_shape[0]
+    wm = np.asarray(w, np.float64).reshape(K, -1)
+    P, Q = np.shape(dy)[1], np.shape(dy)[2]
+    dx = np.empty(x_shape, np.float64)
+    for a, b in _image_chunks(N, P * Q * R * S * C):
+        dcols = np.asarray(dy[a:b], np.float64).reshape(-1, K) @ wm
+        dx[a:b] = col2im(dcols, (b - a,) + tuple(x_shape[1:]), R, S, stride, pad)
+    return dx
 
 
 def conv2d_wgrad(x, dy, w_shape, stride, pad):
     K, R, S, C = w_shape
-    cols = im2col(x, R, S, stride, pad)
-    return (np.asarray(dy, np.float64).reshape(-1, K).T @ cols).reshape(K, R, S, C)
+    N = x.shape[0]
+    P, Q = np.shape(dy)[1], np.shape(dy)[2]
+    dw = np.zeros((K, R * S * C), np.float64)
+    for a, b in _image_chunks(N, P * Q * R * S * C):
+        dw += np.asarray(dy[a:b], np.float64).reshape(-1, K).T @ im2col(x[a:b], R, S, stride, pad)
+    return dw.reshape(K, R, S, C)
 
 
 def batchnorm_fwd(x, gamma, beta, eps=1e-5, relu=False, residual=None):

@@ -74,7 +74,7 @@ __device__ unsigned g_fold_sync[kFoldSlots][2][2];
 __global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __restrict__ x, uint64_t rows, int C,
                                                       float* part, unsigned* rearm) {
   pdl_wait();
-  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) *rearm = 0u;  // re-arm the apply pass's fold count
+  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) rearm[0] = rearm[1] = 0u;  // re-arm fold count + ticket
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(BT) bn_bwd_reduce_kernel(const __nv_bfloat16* 
                                                            const uint8_t* __restrict__ mask, uint64_t rows, int C,
                                                            float* part, unsigned* rearm) {
   pdl_wait();
-  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) *rearm = 0u;  // re-arm the apply pass's fold count
+  if (rearm && blockIdx.x == 0 && threadIdx.x == 0) rearm[0] = rearm[1] = 0u;  // re-arm fold count + ticket
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
@@ -345,11 +345,12 @@ __global__ void __launch_bounds__(BT) bn_bwd_apply_kernel(const __nv_bfloat16* _
 // skipping them). Instead the first C/2 blocks of the apply grid fold one channel per 128 threads (float64, fixed
 // order: threads stride the partial rows, butterfly, warp sums in order), publish scale/shift (or the backward coefficients) and
 // count themselves done; every block waits for the count, stages the per-channel values in shared memory and
-// applies. The folding blocks have the lowest indices, so they are resident before any block spins on them. The
+// applies. The folding blocks are the first nfold to take an arrival ticket, so they are running before anyone
+// can spin on them. The
 // count is re-armed by the kernel that produced the partials (bn_stats / bn_bwd_reduce / the conv statistics
 // epilogue zero it at their start, nsk_bn_fold_counter), so the apply needs no exit accounting (2.4k
 // same-address atomics per launch were measurable).
-// g_fold_sync[fwd | bwd][0]: folded channels (declared with bn_stats_kernel)
+// g_fold_sync[fwd | bwd]: [0] folded channels, [1] arrival ticket (declared with bn_stats_kernel)
 
 __device__ __forceinline__ void fold_wait(unsigned* sync, unsigned target) {
   if (threadIdx.x == 0) {
@@ -362,6 +363,14 @@ __device__ __forceinline__ void fold_wait(unsigned* sync, unsigned target) {
     }
   }
   __syncthreads();
+}
+
+// arrival ticket of this block (sync[1], re-armed with the count sync[0] by the producer of the partials)
+__device__ __forceinline__ int fold_ticket(unsigned* sync) {
+  __shared__ unsigned ticket;
+  if (threadIdx.x == 0) ticket = atomicAdd(&sync[1], 1u);
+  __syncthreads();
+  return (int)ticket;
 }
 
 // float64 fold of channel c's two partial columns over nblk rows of [nblk][2][C] by the 128 threads of one half
@@ -407,8 +416,11 @@ __global__ void __launch_bounds__(AT) bn_apply_fold_kernel(const float* part, in
                                                            __nv_bfloat16* __restrict__ y, uint8_t* __restrict__ mask,
                                                            int relu, int nfold, unsigned* sync) {
   pdl_wait();
-  // folding blocks: the first nfold (<= SMs, so they are resident before anyone spins), 2 channels per pass
-  for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
+  // folding blocks: the first nfold (<= SMs) blocks to ARRIVE, 2 channels per pass. Roles come from an arrival
+  // ticket, not blockIdx: a block that holds a ticket is running, so the fold never waits on an undispatched block
+  // whatever order the hardware schedules the grid in (or however side-stream kernels occupy the SMs).
+  const int role = fold_ticket(sync);
+  for (int cg = role; role < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
     const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
     double a, b;
     group_fold(part, nblk, C, c, &a, &b);
@@ -481,7 +493,8 @@ __global__ void __launch_bounds__(AT) bn_bwd_apply_fold_kernel(const float* part
                                                                __nv_bfloat16* __restrict__ dres, int nfold,
                                                                unsigned* sync) {
   pdl_wait();
-  for (int cg = blockIdx.x; blockIdx.x < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
+  const int role = fold_ticket(sync);  // arrival-ordered fold roles (see bn_apply_fold_kernel)
+  for (int cg = role; role < nfold && cg * (AT / FOLD_T) < C; cg += nfold) {
     const int c = cg * (AT / FOLD_T) + threadIdx.x / FOLD_T;
     double sdz, sdzx;
     group_fold(part, nblk, C, c, &sdz, &sdzx);

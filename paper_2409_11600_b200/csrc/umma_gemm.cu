@@ -13,7 +13,9 @@
 // Every smem stage holds 128 bytes of K per operand row: 4 UMMA k-substeps.
 // Operands can be K-major (TMA box {128B of K, rows}) or MN-major
 // (boxes of 64 bf16 / 32 fp32 MN-elements x KS K-rows), all 128B-swizzled.
+#include <mutex>
 #include <type_traits>
+#include <unordered_map>
 
 #include "common.cuh"
 #include "../../include/nskb.h"
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmC, const UmmaProb p) {
   pdl_wait();
-  if (p.fold_reset && blockIdx.x == 0 && threadIdx.x == 0) *p.fold_reset = 0u;
+  if (p.fold_reset && blockIdx.x == 0 && threadIdx.x == 0) p.fold_reset[0] = p.fold_reset[1] = 0u;
   using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
   using T = KT<ESZ>;
   constexpr bool kGate = Launch<S>::kGate;
@@ -1168,30 +1170,35 @@ __global__ void splitk_fold_kernel(const float* __restrict__ ws, int splits, int
   }
 }
 
-// Library-owned grow-only scratch for split-K partials. Grows only outside stream capture (the first,
-// eager execution of a captured step sizes it).
+// Library-owned grow-only scratch for split-K partials, one buffer per launching stream: split-K problems
+// issued concurrently on the compute stream and a side stream never share partials. Grows only outside
+// stream capture (the first, eager execution of a captured step sizes it); an outgrown buffer is freed
+// after a device-wide synchronize, since kernels on any stream may still read it.
 int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
-  static float* buf = nullptr;
-  static size_t cap = 0;
-  if (floats > cap) {
+  struct Slot { float* buf = nullptr; size_t cap = 0; };
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, Slot> slots;
+  std::lock_guard<std::mutex> lk(mu);
+  Slot& s = slots[st];
+  if (floats > s.cap) {
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(st, &cs);
     if (cs != cudaStreamCaptureStatusNone)
       return nsk::set_error(NSK_ERR_UNSUPPORTED, "gemm: split-K scratch must be sized before graph capture");
-    if (buf) {
-      cudaStreamSynchronize(st);
-      cudaFree(buf);
+    if (s.buf) {
+      cudaDeviceSynchronize();
+      cudaFree(s.buf);
     }
     size_t want = floats < (1u << 20) ? (1u << 20) : floats;
-    if (cudaMalloc(&buf, want * sizeof(float)) != cudaSuccess) {
+    if (cudaMalloc(&s.buf, want * sizeof(float)) != cudaSuccess) {
       cudaGetLastError();
-      buf = nullptr;
-      cap = 0;
+      s.buf = nullptr;
+      s.cap = 0;
       return nsk::set_error(NSK_ERR_OOM, "out of memory: gemm split-K scratch");
     }
-    cap = want;
+    s.cap = want;
   }
-  *out = buf;
+  *out = s.buf;
   return NSK_OK;
 }
 

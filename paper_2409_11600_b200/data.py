@@ -94,16 +94,25 @@ class ImageDataset:
 
     ``features``: float32 [N, C, H, W] (NCHW, fed as is) or uint8 [N, H, W, C] images (augmented on the GPU).
     ``labels``: [N] class ids (float32 on the device, like the reference's CSV labels).
+
+    Data parallelism: ``batch_size`` is the GLOBAL batch. Every rank draws the same global
+    permutation (same seed, same Generator) and takes rows [rank*B_loc, (rank+1)*B_loc) of each global batch,
+    B_loc = batch_size / world, so the union over ranks is bit-identical to the single-process batch.
     """
 
-    def __init__(self, features, labels, batch_size: int, seed: int = 0, shuffle: bool = True):
+    def __init__(self, features, labels, batch_size: int, seed: int = 0, shuffle: bool = True, rank: int = 0,
+                 world: int = 1):
         self.features = np.ascontiguousarray(features)
         self.labels = np.ascontiguousarray(labels, dtype=np.float32).reshape(-1)
         if len(self.features) != len(self.labels):
             raise NskRuntimeError(f"dataset has {len(self.features)} rows but {len(self.labels)} labels")
         if batch_size < 1:
             raise NskRuntimeError(f"batch size must be at least 1, got {batch_size}")
+        if world < 1 or not 0 <= rank < world or batch_size % world:
+            raise NskRuntimeError(f"global batch {batch_size} cannot be split over {world} ranks (rank {rank})")
         self.batch_size = batch_size
+        self.rank, self.world = rank, world
+        self.local_batch = batch_size // world
         self.seed = seed
         self.shuffle = shuffle
         self.num_rows = len(self.labels)
@@ -122,12 +131,21 @@ class ImageDataset:
         self.epoch += 1
         self.permutation = self._rng.permutation(self.num_rows) if self.shuffle else np.arange(self.num_rows)
 
+    def global_rows(self, index: int) -> int:
+        """Rows in global batch ``index`` (the last one may be partial, dataset.py:118-121)."""
+        lo = index * self.batch_size
+        return max(0, min(lo + self.batch_size, self.num_rows) - lo)
+
     def batch_rows(self, index: int) -> np.ndarray:
-        """Row ids of batch ``index`` under the current permutation (dataset.py:114-121)."""
+        """Row ids of this rank's share of batch ``index`` under the current permutation (dataset.py:114-121):
+        the contiguous global batch, then the rank's contiguous slice of it."""
         if self.permutation is None:
             self.reset_epoch()
         lo = index * self.batch_size
-        return self.permutation[lo:min(lo + self.batch_size, self.num_rows)]
+        rows = self.permutation[lo:min(lo + self.batch_size, self.num_rows)]
+        if self.world == 1:
+            return rows
+        return rows[self.rank * self.local_batch:(self.rank + 1) * self.local_batch]
 
 
 def _draw_crop_flip(rng: np.random.Generator, n: int, pad: int) -> np.ndarray:
@@ -168,7 +186,7 @@ class DeviceLoader:
         from .tensor import check_index_values
 
         check_index_values(ds.labels, trainer.classes, "target")
-        b = ds.batch_size
+        b = ds.local_batch
         x_shape = (b,) + ds.features.shape[1:]
         self.slots = [PinnedSlot(x_shape, ds.features.dtype, b, ds.uint8) for _ in range(self.capacity + 1)]
         lib = _lib.lib()
@@ -178,14 +196,9 @@ class DeviceLoader:
         self._free: queue.Queue = queue.Queue()
         for sl in self.slots:
             self._free.put(sl)
-        self._ready: queue.Queue | None = None
+        self._epoch: _Epoch | None = None
         self._threads: list[threading.Thread] = []
-        self._stop = threading.Event()
         self._cursor = 0
-        self._next_index = 0
-        self._active = 0
-        self._lock = threading.Lock()
-        self._current: PinnedSlot | None = None
 
     # -- producers --
     def _fill(self, slot: PinnedSlot, index: int) -> None:
@@ -196,75 +209,72 @@ class DeviceLoader:
         np.take(ds.features, rows, axis=0, out=slot.arrays["x"][:n])
         np.take(ds.labels, rows, axis=0, out=slot.arrays["y"][:n])
         if ds.uint8:
-            slot.arrays["offs"][:n] = _draw_crop_flip(batch_generator(ds.seed, ds.epoch, index), n, self.pad)
+            offs = _draw_crop_flip(batch_generator(ds.seed, ds.epoch, index), ds.global_rows(index), self.pad)
+            slot.arrays["offs"][:n] = offs[ds.rank * ds.local_batch:ds.rank * ds.local_batch + n]
         slot.index, slot.rows = index, n
 
-    def _claim(self) -> int | None:
-        with self._lock:
-            if self._next_index >= self.ds.num_batches():
-                return None
-            i = self._next_index
-            self._next_index += 1
-            return i
-
-    def _put(self, item) -> None:
-        while not self._stop.is_set():
-            try:
-                self._ready.put(item, timeout=0.05)
-                return
-            except queue.Full:
-                continue
-
-    def _worker(self) -> None:
+    def _worker(self, ep: "_Epoch") -> None:
+        """One prefetch worker of epoch ``ep`` (concurrency.py:143-160). Everything it touches belongs to its own
+        epoch, so a reset_epoch while it runs cannot mix its batches or counters into the next epoch."""
         try:
-            while not self._stop.is_set():
-                i = self._claim()
+            while not ep.stop.is_set():
+                i = ep.claim(self.ds.num_batches())
                 if i is None:
                     break
-                slot = self._free.get()
+                slot = self._get_free(ep.stop)
+                if slot is None:
+                    break
                 try:
                     self._fill(slot, i)
                 except BaseException as exc:  # noqa: BLE001 - poison the queue (concurrency.py:143-147)
                     self._free.put(slot)
-                    self._put(_Poison(exc))
+                    ep.put(_Poison(exc))
                     return
-                self._put(slot)
+                if not ep.put(slot):  # epoch abandoned: the slot goes back to the ring
+                    self._free.put(slot)
+                    break
         finally:
-            with self._lock:
-                self._active -= 1
-                last = self._active == 0
-            if last:
-                self._put(END_OF_DATA)
+            if ep.retire():
+                ep.put(END_OF_DATA)
+
+    def _get_free(self, stop: threading.Event):
+        """A free ring slot, or None once ``stop`` is set (never blocks past a shutdown)."""
+        while not stop.is_set():
+            try:
+                return self._free.get(timeout=0.05)
+            except queue.Empty:
+                continue
+        return None
 
     def reset_epoch(self) -> None:
-        """New epoch (dataset.py:93-112): permutation, then W prefetch workers when W > 1."""
+        """New epoch (dataset.py:93-112): permutation, then W prefetch workers when W > 1. May be called at any
+        point of an epoch: the old epoch's workers are stopped and its staged slots return to the ring."""
         self.shutdown()
         self.ds.reset_epoch()
         self._cursor = 0
-        self._next_index = 0
-        self._stop.clear()
         if self.workers > 1:
-            self._ready = queue.Queue(maxsize=self.capacity)
-            self._active = self.workers
-            self._threads = [threading.Thread(target=self._worker, name=f"nsk-prefetch-{w}", daemon=True)
-                             for w in range(self.workers)]
+            ep = _Epoch(self.capacity, self.workers)
+            self._epoch = ep
+            self._threads = [threading.Thread(target=self._worker, args=(ep,), name=f"nsk-prefetch-{w}",
+                                              daemon=True) for w in range(self.workers)]
             for th in self._threads:
                 th.start()
         else:
-            self._ready = None
+            self._epoch = None
 
     # -- consumer --
     def _next_slot(self):
         if self.ds.permutation is None:
             self.reset_epoch()
-        if self._ready is not None:
-            item = self._ready.get()
+        ep = self._epoch
+        if ep is not None:
+            item = ep.ready.get()
             if item is END_OF_DATA:
-                self._ready.put(item)  # sticky (concurrency.py:174-177)
+                ep.ready.put(item)  # sticky (concurrency.py:174-177)
                 return END_OF_DATA
             if isinstance(item, _Poison):
-                self._stop.set()
-                self._ready.put(item)
+                ep.stop.set()
+                ep.ready.put(item)
                 raise item.error
             return item
         if self._cursor >= self.ds.num_batches():
@@ -279,7 +289,7 @@ class DeviceLoader:
         slot = self._next_slot()
         if slot is END_OF_DATA:
             return END_OF_DATA
-        if slot.rows != self.ds.batch_size:
+        if slot.rows != self.ds.local_batch:
             self._free.put(slot)
             raise NskRuntimeError("partial final batch: the captured step has a fixed batch shape "
                                   "(drop it or size the dataset to a multiple of the batch)")
@@ -302,7 +312,54 @@ class DeviceLoader:
         return slot.index
 
     def shutdown(self) -> None:
-        self._stop.set()
+        """Stop the current epoch's workers and return every slot they staged (or held) to the ring."""
+        ep, self._epoch = self._epoch, None
+        if ep is None:
+            return
+        ep.stop.set()
         for th in self._threads:
             th.join(timeout=5)
         self._threads = []
+        while True:
+            try:
+                item = ep.ready.get_nowait()
+            except queue.Empty:
+                break
+            if item is not END_OF_DATA and not isinstance(item, _Poison):
+                self._free.put(item)  # a staged slot
+
+
+class _Epoch:
+    """Per-epoch prefetch state (the reference builds a fresh PrefetchQueue per epoch, dataset.py:103-109):
+    the bounded ready queue, the stop flag, the batch-index cursor and the live-worker count."""
+
+    def __init__(self, capacity: int, workers: int):
+        self.ready: queue.Queue = queue.Queue(maxsize=capacity)
+        self.stop = threading.Event()
+        self.lock = threading.Lock()
+        self.next_index = 0
+        self.active = workers
+
+    def claim(self, num_batches: int) -> int | None:
+        with self.lock:
+            if self.next_index >= num_batches:
+                return None
+            i = self.next_index
+            self.next_index += 1
+            return i
+
+    def put(self, item) -> bool:
+        """Enqueue unless the epoch was stopped first (then False: the caller still owns the item)."""
+        while not self.stop.is_set():
+            try:
+                self.ready.put(item, timeout=0.05)
+                return True
+            except queue.Full:
+                continue
+        return False
+
+    def retire(self) -> bool:
+        """A worker exits; True for the last one of the epoch (it posts END_OF_DATA)."""
+        with self.lock:
+            self.active -= 1
+            return self.active == 0

@@ -40,18 +40,20 @@ class Workspace:
         return self.buf
 
 
-WGRAD_WS = Workspace()
 class _PerStream:
-    """One Workspace per stream (a forward branch on the side stream runs BatchNorms concurrently)."""
+    """One Workspace per stream: kernels on the compute stream and on the side stream (forward branches,
+    forked weight gradients) run concurrently and must never share scratch."""
 
     def __init__(self):
         self.ws: dict[int, Workspace] = {}
 
-    def get(self, nbytes: int) -> Buffer:
-        return self.ws.setdefault(_lib.stream(), Workspace()).get(nbytes)
+    def get(self, nbytes: int, stream: int | None = None) -> Buffer:
+        st = _lib.stream() if stream is None else stream
+        return self.ws.setdefault(st, Workspace()).get(nbytes)
 
 
 BN_WS = _PerStream()
+WGRAD_WS = _PerStream()  # split-K partials of conv weight gradients, keyed by the stream the wgrad runs on
 
 
 def _temp_bf16(t: Tensor, pool: Pool) -> tuple[int, Tensor | None]:
@@ -188,12 +190,12 @@ def _r_conv2d(node, g, pool, sinks):
         else:
             xp, xtmp = _temp_bf16(xin, pool)
             need = lib.nsk_conv2d_wgrad_workspace(C.byref(desc))
-            ws = WGRAD_WS.get(need)
             wst = st
             if sinks[1] is not None and SIDE.enabled():
                 # overlap the weight gradient with the rest of backward (side.py); its inputs stay alive to the join
                 wst = SIDE.fork(xin.buffer, g.buffer, None if xtmp is None else xtmp.buffer,
                                 None if gtmp is None else gtmp.buffer)
+            ws = WGRAD_WS.get(need, wst)
             check(lib.nsk_conv2d_wgrad(C.byref(desc), xp, gp, out_ptr, beta, ws.ptr, ws.nbytes, wst))
             if xtmp is not None:
                 release_tensor(pool, xtmp)

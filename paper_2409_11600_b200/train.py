@@ -240,6 +240,7 @@ class Trainer:
         sl = self._slots[self._cur]
         if sl.graph is not None:
             sl.graph.launch()
+            self.s.param_group.step_count += 1  # the replayed optimizer step (recording counted the captured one)
             sc = DeviceScalar(sl.loss_slot)
         elif self.use_graph and self.steps_done >= self.warmup:
             fresh = self.s.pool.stats()["fresh"]

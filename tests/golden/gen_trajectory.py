@@ -1,12 +1,13 @@
 """Generate the 100-step loss-trajectory goldens (north star: "the loss trajectory over 100 steps must stay
 within 1%") by running the float64 oracle on a fixed synthetic dataset.
 
-    python tests/golden/gen_trajectory.py [resnet18|smallcnn]
+    python tests/golden/gen_trajectory.py [resnet18|smallcnn|resnet18_c2]
 
-Dataset: TRAJ_ROWS synthetic images x ~ N(0,1) [3, 32, 32] (seed 7) with learnable labels (argmax of a fixed
+Dataset: ROWS synthetic images x ~ N(0,1) [3, 32, 32] (seed 7) with learnable labels (argmax of a fixed
 random projection of a 4x4-subsampled view, 30% replaced by random labels so the loss stays away from zero),
 shuffled per epoch exactly like the reference dataset (dataset.py:93-121 via
-oracle.ref_ops.epoch_permutation / batch_rows), batch TRAJ_BATCH, SGD momentum 0.9, per-model (steps, lr) in SETTINGS.
+oracle.ref_ops.epoch_permutation / batch_rows), SGD momentum 0.9, per-model (steps, lr, batch, rows) in SETTINGS.
+``resnet18_c2`` is BASELINE config C2 itself: ResNet-18/CIFAR, batch 256, SGD lr 0.1 momentum 0.9, 100 steps.
 Writes tests/golden/trajectory_<model>.npz with the per-step losses of the float64 oracle (bf16=False, the
 reference's own arithmetic) and of the bf16-emulating oracle (bf16=True). The GPU test replays the same
 schedule through the device Trainer.
@@ -29,38 +30,40 @@ from oracle import ref_ops as R  # noqa: E402
 TRAJ_ROWS = 1024
 TRAJ_BATCH = 32
 MOMENTUM = 0.9
-# per model: (steps, lr). ResNet-18 + BatchNorm at batch 32 is chaotic under rounding (the oracle's own
-# bf16-emulating and float64 runs drift apart by several % per step after a few dozen steps at lr 0.01), so
-# its golden uses a gentler lr and 30 steps; the small CNN runs the full 100 steps.
-SETTINGS = {"smallcnn": (100, 0.01), "resnet18": (30, 0.002)}
+# per model: (steps, lr, batch, rows). ResNet-18 + BatchNorm at batch 32 is chaotic under rounding (the
+# oracle's own bf16-emulating and float64 runs drift apart by several % per step after a few dozen steps at
+# lr 0.01), so that golden uses a gentler lr and 30 steps; the small CNN runs the full 100 steps; resnet18_c2
+# is the C2 configuration (batch 256, lr 0.1) for 100 steps.
+SETTINGS = {"smallcnn": (100, 0.01, TRAJ_BATCH, TRAJ_ROWS), "resnet18": (30, 0.002, TRAJ_BATCH, TRAJ_ROWS),
+            "resnet18_c2": (100, 0.1, 256, 2560)}
 
 
-def dataset():
+def dataset(rows: int = TRAJ_ROWS):
     rng = np.random.default_rng(7)
-    x = rng.standard_normal((TRAJ_ROWS, 3, 32, 32)).astype(np.float32)
+    x = rng.standard_normal((rows, 3, 32, 32)).astype(np.float32)
     proj = rng.standard_normal((3 * 8 * 8, 10))
-    y = (x[:, :, ::4, ::4].reshape(TRAJ_ROWS, -1) @ proj).argmax(axis=1).astype(np.float32)
-    noise = rng.random(TRAJ_ROWS) < 0.3
+    y = (x[:, :, ::4, ::4].reshape(rows, -1) @ proj).argmax(axis=1).astype(np.float32)
+    noise = rng.random(rows) < 0.3
     y[noise] = rng.integers(0, 10, int(noise.sum()))
     return x, y
 
 
-def schedule(steps: int):
+def schedule(steps: int, batch: int = TRAJ_BATCH, rows: int = TRAJ_ROWS):
     """Row indices of each step's batch: per-epoch permutations (seed 11), contiguous batches."""
-    per_epoch = TRAJ_ROWS // TRAJ_BATCH
-    perms = R.epoch_permutation(11, TRAJ_ROWS, (steps + per_epoch - 1) // per_epoch)
-    return [R.batch_rows(perms[s // per_epoch], s % per_epoch, TRAJ_BATCH) for s in range(steps)]
+    per_epoch = rows // batch
+    perms = R.epoch_permutation(11, rows, (steps + per_epoch - 1) // per_epoch)
+    return [R.batch_rows(perms[s // per_epoch], s % per_epoch, batch) for s in range(steps)]
 
 
 def make_oracle(model: str):
-    return om.ResNet18Oracle(seed=0) if model == "resnet18" else om.SmallCNNOracle(seed=0)
+    return om.ResNet18Oracle(seed=0) if model.startswith("resnet18") else om.SmallCNNOracle(seed=0)
 
 
 def main():
     model = sys.argv[1] if len(sys.argv) > 1 else "resnet18"
-    steps, lr = SETTINGS[model]
-    x, y = dataset()
-    sched = schedule(steps)
+    steps, lr, batch, rows = SETTINGS[model]
+    x, y = dataset(rows)
+    sched = schedule(steps, batch, rows)
     out = {}
     for bf16 in (False, True):
         ref = make_oracle(model)

@@ -35,3 +35,111 @@ def test_crop_flip_draw_is_the_oracle_draw():
         b = X.draw_crop_flip(batch_generator(3, 1, 7), 33, pad)
         np.testing.assert_array_equal(a, b)
         assert a[:, :2].max() <= 2 * pad and a[:, 2].max() <= 1
+
+
+def test_rank_shards_union_is_the_global_batch():
+    """§8(e): every rank draws the same global permutation and takes its contiguous slice of each global batch;
+    the union over ranks (in rank order) is the single-process batch, bit for bit."""
+    from paper_2409_11600_b200.data import ImageDataset
+
+    n, b, seed = 96, 16, 3
+    feats = np.zeros((n, 3, 2, 2), np.float32)
+    single = ImageDataset(feats, np.arange(n) % 10, b, seed=seed)
+    for world in (2, 4):
+        shards = [ImageDataset(feats, np.arange(n) % 10, b, seed=seed, rank=r, world=world) for r in range(world)]
+        for e in range(2):
+            single.reset_epoch() if world == 2 else None
+            for ds in shards:
+                ds.reset_epoch()
+            if world == 4:  # single-process reference for the same epoch
+                ref = ImageDataset(feats, np.arange(n) % 10, b, seed=seed)
+                for _ in range(e + 1):
+                    ref.reset_epoch()
+            else:
+                ref = single
+            for i in range(ref.num_batches()):
+                parts = [ds.batch_rows(i) for ds in shards]
+                assert all(len(p) == b // world for p in parts)
+                np.testing.assert_array_equal(np.concatenate(parts), ref.batch_rows(i))
+
+
+def test_rank_shard_rejects_uneven_split():
+    import pytest
+
+    from paper_2409_11600_b200.data import ImageDataset
+    from paper_2409_11600_b200.errors import NskRuntimeError
+
+    with pytest.raises(NskRuntimeError):
+        ImageDataset(np.zeros((8, 1), np.float32), np.zeros(8), 6, rank=0, world=4)
+
+
+class _FakeSlot:
+    """Host-only stand-in for data.PinnedSlot (no pinned memory, no CUDA event)."""
+
+    def __init__(self, b):
+        self.arrays = {"x": np.zeros((b, 1), np.float32), "y": np.zeros(b, np.float32)}
+        self.index, self.rows = -1, 0
+
+    def wait_copied(self):
+        pass
+
+
+def _host_loader(n, b, workers, capacity):
+    """A DeviceLoader without device resources: the producer/consumer logic is host-only."""
+    import queue
+
+    from paper_2409_11600_b200.data import DeviceLoader, ImageDataset
+
+    ds = ImageDataset(np.arange(n, dtype=np.float32).reshape(n, 1), np.arange(n) % 10, b, seed=1)
+    ld = DeviceLoader.__new__(DeviceLoader)
+    ld.ds, ld.workers, ld.capacity, ld.pad = ds, workers, capacity, 0
+    ld.slots = [_FakeSlot(b) for _ in range(capacity + 1)]
+    ld._free = queue.Queue()
+    for sl in ld.slots:
+        ld._free.put(sl)
+    ld._epoch, ld._threads, ld._cursor = None, [], 0
+    return ld
+
+
+def _drain(ld, limit=None):
+    from paper_2409_11600_b200.data import END_OF_DATA
+
+    got = []
+    while limit is None or len(got) < limit:
+        sl = ld._next_slot()
+        if sl is END_OF_DATA:
+            break
+        got.append((sl.index, sl.arrays["x"][:sl.rows, 0].astype(np.int64).copy()))
+        ld._free.put(sl)  # what next() does once the copy is issued
+    return got
+
+
+def test_reset_epoch_mid_epoch_with_full_ring_does_not_deadlock():
+    """reset_epoch with workers blocked on a full ring must stop them, return every staged slot and
+    start a clean epoch (the reference builds a fresh queue per epoch, dataset.py:103-109)."""
+    import threading
+    import time
+
+    n, b, workers, cap = 200, 8, 3, 2
+    ld = _host_loader(n, b, workers, cap)
+    ld.reset_epoch()
+    _drain(ld, limit=2)
+    time.sleep(0.2)  # workers fill the ring and block
+    done = threading.Event()
+
+    def reset_and_read():
+        ld.reset_epoch()
+        done.result = _drain(ld)
+        done.set()
+
+    th = threading.Thread(target=reset_and_read, daemon=True)
+    th.start()
+    assert done.wait(20), "reset_epoch mid-epoch deadlocked"
+    got = done.result
+    assert sorted(i for i, _ in got) == list(range(ld.ds.num_batches()))
+    rows = np.sort(np.concatenate([r for _, r in got]))
+    np.testing.assert_array_equal(rows, np.arange(n))  # exact coverage of the NEW epoch's permutation
+    for i, r in got:
+        np.testing.assert_array_equal(r, ld.ds.batch_rows(i))
+    ld.shutdown()
+    assert ld._free.qsize() == len(ld.slots)  # every slot back in the ring

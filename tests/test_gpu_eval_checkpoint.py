@@ -62,6 +62,7 @@ def test_checkpoint_restores_training_bit_for_bit(dev, tmp_path):
         float(tr.step(x, y))
     path = str(tmp_path / "ckpt.npz")
     checkpoint.save(s, path)
+    assert int(np.load(path)["meta/step_count"][0]) == 4  # eager + captured + replayed SGD steps all counted
     cont = [float(tr.step(x, y)) for x, y in zip(xs[4:], ys[4:])]
     eval_a = tr.evaluate(xs[0], ys[0])
     s2, tr2 = _resnet_trainer()
@@ -71,6 +72,7 @@ def test_checkpoint_restores_training_bit_for_bit(dev, tmp_path):
     checkpoint.load(s2, path)
     resumed = [float(tr2.step(x, y)) for x, y in zip(xs[4:], ys[4:])]
     assert resumed == cont, (resumed, cont)
+    assert s2.param_group.step_count == s.param_group.step_count == 7
     eval_b = tr2.evaluate(xs[0], ys[0])
     assert eval_a == eval_b
 

@@ -14,28 +14,50 @@ def _rel(a, b):
 
 
 def test_small_cnn_one_sgd_step_matches_oracle(session):
-    """C1: small CNN, one SGD step; loss and every updated parameter vs the bf16-emulating oracle."""
+    """C1: small CNN, one SGD step at batch 32. Every activation (h1, h2, logits), the loss,
+    every parameter gradient and every applied update against the bf16-emulating oracle at the north star's
+    1e-3 (normwise relative); init bit-identical."""
+    from paper_2409_11600_b200 import autodiff, nn
     from paper_2409_11600_b200.models import SmallCNN
-    from paper_2409_11600_b200.train import Trainer
 
     rng = np.random.default_rng(0)
     x = rng.standard_normal((32, 3, 32, 32)).astype(np.float32)
     y = rng.integers(0, 10, 32).astype(np.float32)
     model = SmallCNN(session)
     w0 = {n: t.data.copy() for n, t in session.param_group.params}
-    tr = Trainer(session, model, x.shape, 10, optimizer=("sgd", 0.01, 0.9), graph=False)
-    loss = float(tr.step(x, y))
     ref = om.SmallCNNOracle(seed=0)
     names = ["w1", "b1", "w2", "b2", "fc_w", "fc_b"]
     for (n, _t), key in zip(session.param_group.params, names):
         np.testing.assert_array_equal(w0[n], ref.params[key])  # bit-identical init (seed plumbing)
-    ref_loss = ref.train_step(x, y, lr=0.01, momentum=0.9, bf16=True)
-    assert abs(loss - ref_loss) <= 1e-3 * abs(ref_loss)
+    acts = {}
+    push = session.push_named
+
+    def record(name, t):  # every statement the model pushes: read its value before backward reclaims it
+        acts[name.split(".")[-1]] = t.data.copy()
+        push(name, t)
+
+    session.push_named = record
+    pool = session.pool
+    logits = model.forward(autodiff.make_data(pool, x))
+    loss = nn.cross_entropy(logits, autodiff.make_data(pool, y), pool)
+    push("loss", loss)
+    lv = loss.item()
+    autodiff.backward(session.tape(), session.grad_cache, pool)
+    grads = {n: session.grad_cache.get(n).copy() for n, _t in session.param_group.params}
+    nn.sgd_step(session.param_group, session.grad_cache, 0.01, 0.9)
+    session.grad_cache.zero_after_step()
+
+    ref_acts = {}
+    ref_loss, ref_grads, _ = ref.loss_and_grads(x, y, bf16=True, acts=ref_acts)
+    ref.opt.sgd(ref.params, ref_grads, 0.01, 0.9)
+    assert abs(lv - ref_loss) <= 1e-3 * abs(ref_loss), (lv, ref_loss)
+    for a in ("h1", "h2", "logits"):
+        assert _rel(acts[a], ref_acts[a]) < 1e-3, (a, _rel(acts[a], ref_acts[a]))
     for (pname, t), key in zip(session.param_group.params, names):
-        # the applied update (w0 - w1)/lr is the gradient: within 1% (bf16 storage on both sides)
-        upd = (w0[pname].astype(np.float64) - t.data) / 0.01
-        ref_upd = (w0[pname].astype(np.float64) - ref.params[key]) / 0.01
-        assert _rel(upd, ref_upd) < 1e-2, (pname, key, _rel(upd, ref_upd))
+        assert _rel(grads[pname], ref_grads[key]) < 1e-3, (key, _rel(grads[pname], ref_grads[key]))
+        upd = w0[pname].astype(np.float64) - t.data  # the applied update lr * v
+        ref_upd = w0[pname].astype(np.float64) - ref.params[key]
+        assert _rel(upd, ref_upd) < 1e-3, (key, _rel(upd, ref_upd))
 
 
 def test_resnet18_gradients_match_oracle(session):

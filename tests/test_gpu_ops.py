@@ -221,7 +221,7 @@ def test_batchnorm_fwd_bwd(session, shape, relu, res, fold_apply, monkeypatch):
     y = layers.batchnorm(xt, gbt, pool, relu=relu, residual=rt)
     ref_y, cache = X.batchnorm_fwd(x, gb[0], gb[1], relu=relu, residual=r)
     yd = y.data
-    assert rel(yd, X.round_bf16(ref_y)) < 2e-3
+    assert rel(yd, X.round_bf16(ref_y)) < 1e-3
     gy = X.round_bf16(rng.standard_normal(shape))
     gyt = autodiff.make_data(pool, gy, dtype=BF16)
     loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", y, gyt, pool), pool)
@@ -231,7 +231,7 @@ def test_batchnorm_fwd_bwd(session, shape, relu, res, fold_apply, monkeypatch):
     autodiff.backward(tape, session.grad_cache, pool)
     dx, dg, db, dres = X.batchnorm_bwd(gy, cache, y_out=yd, relu=relu)
     assert rel(session.grad_cache.get("gb"), np.stack([dg, db])) < 1e-3
-    assert rel(session.grad_cache.get("x"), X.round_bf16(dx)) < 2e-3
+    assert rel(session.grad_cache.get("x"), X.round_bf16(dx)) < 1e-3
     if res:
         assert rel(session.grad_cache.get("r"), X.round_bf16(dres)) < 1e-3
 
@@ -560,6 +560,6 @@ def test_conv_split_k_matches_unsplit(dev, case, monkeypatch):
         out[split] = (y, stats, dxb.host().astype(np.float64).reshape(x.shape))
     ys, ss, ds = out["1"]
     yu, su, du = out["0"]
-    assert rel(ys, yu) < 4e-3 and rel(ss, su) < 4e-3
-    assert rel(ds, X.round_bf16(X.conv2d_dgrad(yu.astype(np.float32), wt, x.shape, st, pad))) < 1e-2
-    assert rel(ds, du) < 4e-3
+    assert rel(ys, yu) < 1e-3 and rel(ss, su) < 1e-3
+    assert rel(ds, X.round_bf16(X.conv2d_dgrad(yu.astype(np.float32), wt, x.shape, st, pad))) < 1e-3
+    assert rel(ds, du) < 1e-3

@@ -1,0 +1,148 @@
+"""Per-op parity at the BASELINE configuration C2 (ResNet-18/CIFAR, batch 256): every distinct conv geometry of
+the network at N = 256, through the same layer calls the training step makes, against the float64 oracle fed
+the same bf16 operands.
+
+At N = 256 each persistent CTA walks many tiles: the weight-resident fprop, the row-reuse (rr64 / rr128)
+weight-gradient kernels, the TMEM double-buffered tile loop and the split-K folds all run exactly as in the
+bench, which the small-N cases in test_gpu_ops.py do not reach.
+
+Bar: the north star's 1e-3 normwise relative error per op (bf16 inputs, fp32 accumulation), the oracle's
+output rounded to the device's storage precision (bf16 activations, fp32 weight gradients).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import restated as X
+
+pytestmark = pytest.mark.gpu
+
+B = 256
+TOL = 1e-3
+
+# (H=W, Cin, Cout, R, stride, pad) of every distinct conv in ResNet-18/CIFAR
+C2_CONVS = [
+    (32, 64, 64, 3, 1, 1),     # layer1 3x3 (x4)
+    (32, 64, 128, 3, 2, 1),    # layer2 first conv1
+    (32, 64, 128, 1, 2, 0),    # layer2 projection shortcut
+    (16, 128, 128, 3, 1, 1),   # layer2 3x3 (x3)
+    (16, 128, 256, 3, 2, 1),   # layer3 first conv1
+    (16, 128, 256, 1, 2, 0),   # layer3 projection shortcut
+    (8, 256, 256, 3, 1, 1),    # layer3 3x3 (x3)
+    (8, 256, 512, 3, 2, 1),    # layer4 first conv1
+    (8, 256, 512, 1, 2, 0),    # layer4 projection shortcut
+    (4, 512, 512, 3, 1, 1),    # layer4 3x3 (x3)
+]
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _ids(c):
+    hw, ci, co, r, st, _p = c
+    return f"{hw}x{hw}_{ci}to{co}_{r}x{r}_s{st}"
+
+
+@pytest.mark.parametrize("case", C2_CONVS, ids=_ids)
+def test_conv_bn_chain_at_batch_256(session, case):
+    """conv2d (BN statistics fused into the tcgen05 epilogue) -> batchnorm(+ReLU) forward, then the backward
+    chain BN -> dgrad / wgrad (wgrad forked onto the side stream), at the bench batch."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+
+    hw, c, k, r, st, pad = case
+    rng = np.random.default_rng(1000 + sum(case))
+    x = X.round_bf16(rng.standard_normal((B, hw, hw, c)))
+    wt = (rng.standard_normal((k, r, r, c)) * np.sqrt(2.0 / (c * r * r))).astype(np.float32)
+    gb = np.stack([rng.uniform(0.5, 1.5, k), rng.uniform(-0.5, 0.5, k)]).astype(np.float32)
+    pool = session.pool
+    xt = autodiff.make_param(pool, x, "x", dtype=BF16)
+    wp = autodiff.make_param(pool, wt, "w")
+    gbt = autodiff.make_param(pool, gb, "gb")
+    conv = layers.conv2d(xt, wp, st, pad, pool, bn_stats=True)
+    y = layers.batchnorm(conv, gbt, pool, relu=True)
+    conv_d, y_d = conv.data, y.data
+
+    wq = X.round_bf16(wt)
+    ref_c = X.round_bf16(X.conv2d_fwd(x, wq, st, pad))
+    assert rel(conv_d, ref_c) < TOL, ("conv y", rel(conv_d, ref_c))
+    ref_y, cache = X.batchnorm_fwd(ref_c, gb[0], gb[1], relu=True)
+    assert rel(y_d, X.round_bf16(ref_y)) < TOL, ("bn y", rel(y_d, X.round_bf16(ref_y)))
+
+    gy = X.round_bf16(rng.standard_normal(y.shape))
+    gyt = autodiff.make_data(pool, gy, dtype=BF16)
+    loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", y, gyt, pool), pool)
+    tape = session.tape()
+    autodiff.push_assignment(tape, "t.gy", gyt)
+    autodiff.push_assignment(tape, "t.loss", loss)
+    autodiff.backward(tape, session.grad_cache, pool)
+
+    dc, dg, db, _ = X.batchnorm_bwd(gy, cache, y_out=y_d, relu=True)
+    dcq = X.round_bf16(dc)  # the device stores the conv-output gradient as bf16
+    got_gb = session.grad_cache.get("gb")
+    assert rel(got_gb, np.stack([dg, db])) < TOL, ("dgamma/dbeta", rel(got_gb, np.stack([dg, db])))
+    dw_ref = X.conv2d_wgrad(x, dcq, wt.shape, st, pad)
+    got_dw = session.grad_cache.get("w")
+    assert rel(got_dw, dw_ref) < TOL, ("dw", rel(got_dw, dw_ref))
+    dx_ref = X.round_bf16(X.conv2d_dgrad(dcq, wq, x.shape, st, pad))
+    got_dx = session.grad_cache.get("x")
+    assert rel(got_dx, dx_ref) < TOL, ("dx", rel(got_dx, dx_ref))
+
+
+@pytest.mark.parametrize("case", C2_CONVS, ids=_ids)
+def test_conv_passes_at_batch_256(session, case):
+    """The three conv passes alone (no BN between): fprop, dgrad, wgrad with a random bf16 output gradient."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+
+    hw, c, k, r, st, pad = case
+    rng = np.random.default_rng(2000 + sum(case))
+    x = X.round_bf16(rng.standard_normal((B, hw, hw, c)))
+    wt = (rng.standard_normal((k, r, r, c)) / np.sqrt(c * r * r)).astype(np.float32)
+    pool = session.pool
+    xt = autodiff.make_param(pool, x, "x", dtype=BF16)
+    wp = autodiff.make_param(pool, wt, "w")
+    y = layers.conv2d(xt, wp, st, pad, pool)
+    wq = X.round_bf16(wt)
+    ref_y = X.round_bf16(X.conv2d_fwd(x, wq, st, pad))
+    assert rel(y.data, ref_y) < TOL
+    gy = X.round_bf16(rng.standard_normal(y.shape))
+    gyt = autodiff.make_data(pool, gy, dtype=BF16)
+    loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", y, gyt, pool), pool)
+    tape = session.tape()
+    autodiff.push_assignment(tape, "t.gy", gyt)
+    autodiff.push_assignment(tape, "t.loss", loss)
+    autodiff.backward(tape, session.grad_cache, pool)
+    dw_ref = X.conv2d_wgrad(x, gy, wt.shape, st, pad)
+    dx_ref = X.round_bf16(X.conv2d_dgrad(gy, wq, x.shape, st, pad))
+    assert rel(session.grad_cache.get("w"), dw_ref) < TOL, rel(session.grad_cache.get("w"), dw_ref)
+    assert rel(session.grad_cache.get("x"), dx_ref) < TOL, rel(session.grad_cache.get("x"), dx_ref)
+
+
+def test_stem_at_batch_256(session):
+    """The image stem: NCHW float32 host batch -> fused layout change + im2col -> tcgen05 GEMM (K = 27 padded),
+    BN statistics, and its weight gradient (the stem has no input gradient)."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((B, 3, 32, 32)).astype(np.float32)
+    wt = (rng.standard_normal((64, 3, 3, 3)) / np.sqrt(27)).astype(np.float32)
+    pool = session.pool
+    xt = autodiff.make_data(pool, x)
+    wp = autodiff.make_param(pool, wt, "w")
+    y = layers.conv2d(xt, wp, 1, 1, pool, layout="nchw")
+    xq = X.round_bf16(np.transpose(x, (0, 2, 3, 1)))
+    wq = X.round_bf16(wt)
+    assert rel(y.data, X.round_bf16(X.conv2d_fwd(xq, wq, 1, 1))) < TOL
+    gy = X.round_bf16(rng.standard_normal(y.shape))
+    gyt = autodiff.make_data(pool, gy, dtype=BF16)
+    loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", y, gyt, pool), pool)
+    tape = session.tape()
+    autodiff.push_assignment(tape, "t.gy", gyt)
+    autodiff.push_assignment(tape, "t.loss", loss)
+    autodiff.backward(tape, session.grad_cache, pool)
+    dw_ref = X.conv2d_wgrad(xq, gy, wt.shape, 1, 1)
+    assert rel(session.grad_cache.get("w"), dw_ref) < TOL
