@@ -8,9 +8,10 @@ synthetic batch of 256 images per GPU (weak scaling), replayed as one CUDA graph
 device-timed (CUDA events per step, L2 flushed between timed steps, max over ranks); ``e2e``
 goes through the public Trainer.step_async(host x, host y) call (pinned staging, H2D on a copy
 stream into double-buffered input slots) with the H2D copy of every batch and an async D2H read of
-every step's loss inside the timed region. ``--impl reference`` times the reference's
-CPU path (the oracle port of the reference arithmetic + restated conv/BN ops, float64, all host
-cores) on a bounded sample.
+every step's loss inside the timed region. ``--impl reference`` times the reference's own
+CPU training step through its API (oracle/refapi.py: the unmodified nsk package with the restated
+conv/BN/pooling registered as ops; float32 storage, float64 accumulation, all host cores) at the
+full configuration: 256 images per step, W warm-up + K timed steps, nothing extrapolated.
 """
 
 from __future__ import annotations
@@ -35,12 +36,12 @@ BATCH = 256
 # --model: resnet18 is the headline (BASELINE.json configs[1] / C2, C5); resnet50 is config C4
 # (ImageNet-shape 3x224x224, batch 256/GPU, bf16), reported on its own line when asked for.
 MODELS = {
-    "resnet18": {"image": (3, 32, 32), "classes": 10, "oracle_sample": 16,
+    "resnet18": {"image": (3, 32, 32), "classes": 10,
                  "workload": "CIFAR-10-shape ResNet-18 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C2/C5",
                  "model": "resnet18-cifar (11,173,962 params)",
                  # dominant tensor-core kernel timed alone: stage-1 3x3 conv fprop 64->64 at 32x32
                  "conv": (32, 64, 64, 3, 1, 1)},
-    "resnet50": {"image": (3, 224, 224), "classes": 1000, "oracle_sample": 1,
+    "resnet50": {"image": (3, 224, 224), "classes": 1000,
                  "workload": "ImageNet-shape ResNet-50 v1.5 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C4",
                  "model": "resnet50-v1.5 (25,557,032 params)",
                  "conv": (56, 64, 64, 3, 1, 1)},
@@ -121,12 +122,30 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
-def run_oracle(sample_imgs: int, steps: int, warmup: int = 1, model: str = "resnet18"):
-    """The reference CPU path (oracle port, float64) on a bounded sample: returns (img/s, per-step seconds)."""
-    from oracle import models as om
+def run_reference_cpu(imgs: int, steps: int, warmup: int, model: str = "resnet18"):
+    """The reference CPU path on ``imgs`` images per step: returns (img/s, per-step seconds, kind, description).
 
-    ref = om.ResNet18Oracle(seed=0) if model == "resnet18" else om.ResNet50Oracle(seed=0)
-    x, y = synthetic_batch(1234, sample_imgs, model)
+    ResNet-18 runs through the reference package's own API (oracle/refapi.py: nsk.autodiff / nsk.nn / its Pool
+    and GradCache, with the restated conv / BN / pooling registered as ops); ResNet-50 (and ResNet-18 when the
+    reference package is absent) through the float64 oracle port of the same arithmetic."""
+    kind, desc = "port", "oracle port of the reference arithmetic + restated conv/BN (float32 storage, float64 accumulation)"
+    ref = None
+    if model == "resnet18":
+        try:
+            from oracle import refapi
+
+            ref = refapi.RefAPIResNet18(seed=0)
+            kind = "reference"
+            desc = ("reference package nsk (baseline/_ref) driven through its API: make_data/record/push_assignment/"
+                    "backward/nn.linear/nn.cross_entropy/nn.sgd_step, restated conv2d/batchnorm/avgpool registered "
+                    "as ops (float32 storage, float64 accumulation)")
+        except ImportError:
+            ref = None
+    if ref is None:
+        from oracle import models as om
+
+        ref = om.ResNet18Oracle(seed=0) if model == "resnet18" else om.ResNet50Oracle(seed=0)
+    x, y = synthetic_batch(1234, imgs, model)
     for _ in range(warmup):
         ref.train_step(x, y, lr=0.1, momentum=0.9)
     times = []
@@ -134,28 +153,36 @@ def run_oracle(sample_imgs: int, steps: int, warmup: int = 1, model: str = "resn
         t0 = time.perf_counter()
         ref.train_step(x, y, lr=0.1, momentum=0.9)
         times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
-    return sample_imgs / med, times
+    return imgs * len(times) / sum(times), times, kind, desc
 
 
-def reference_arm(args, rank):
+def bench_config(model: str, world: int) -> dict:
+    """The workload config both arms report (identical dicts: same model, batch, data)."""
+    spec = MODELS[model]
+    return {"workload": spec["workload"], "model": spec["model"], "global_batch": BATCH * world,
+            "per_gpu_batch": BATCH, "seq_len": None, "image": list(spec["image"]), "parallelism": f"dp{world}",
+            "l2": "GPU arm: flushed between timed steps (256 MiB write outside the step events)"}
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the reference's CPU training step at the full configuration (B = 256 images per step,
+    no extrapolation), W warm-up + K timed steps on this host's cores; rank 0 only under torchrun."""
     if rank != 0:
         return
+    from oracle.refapi import cpu_model
+
     cores = cpu_cores()
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores))
-    spec = MODELS[args.model]
-    sample = spec["oracle_sample"]
-    ips, times = run_oracle(sample, max(1, min(args.steps, 3)), warmup=1, model=args.model)
+    ips, times, kind, desc = run_reference_cpu(BATCH, args.steps, args.warmup, model=args.model)
+    ms = 1000.0 * sum(times) / len(times)
     line = {
         "metric": METRIC, "value": ips, "unit": "images/s", "n_gpus": args.gpus, "steps": len(times),
-        "warmup": 1, "ms_per_step": 1000.0 * statistics.median(times) * BATCH / sample,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": spec["workload"] + ", reference CPU path "
-                               "(oracle port: reference arithmetic + restated conv/BN, float64)",
-                   "global_batch": BATCH, "sample_images_per_step": sample, "parallelism": "cpu"},
-        "cpu_baseline": {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample} images/step x {len(times)} steps of the B=256 workload"},
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 storage, f64 accumulation", "data": "synthetic (N(0,1) images, "
+        "uniform labels, the same random init as the GPU arm)", "impl": "reference",
+        "config": bench_config(args.model, 1),  # one CPU host runs one 256-image step: the N=1 configuration
+        "cpu_baseline": {"value": ips, "unit": "images/s", "cores": cores, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"the full workload: {BATCH} images/step x {len(times)} timed steps after "
+                                   f"{args.warmup} warm-up steps; {desc}"},
         "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -297,11 +324,8 @@ def ours_arm(args, rank, world, local_rank):
         "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) images, uniform labels, random init)",
-        "config": {"workload": spec["workload"],
-                   "model": spec["model"], "global_batch": BATCH * world,
-                   "per_gpu_batch": BATCH, "seq_len": None, "image": list(spec["image"]), "parallelism": f"dp{world}",
-                   "l2": "flushed between timed steps (256 MiB write outside the step events)",
-                   "final_loss": loss},
+        "config": bench_config(args.model, world),
+        "final_loss": loss,
         "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(x.nbytes + y.nbytes),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(tr.launches_per_step * args.steps),
@@ -315,12 +339,14 @@ def ours_arm(args, rank, world, local_rank):
         "clocks": clk.summary(),
     }
     if world == 1:
-        cores = cpu_cores()
-        sample = spec["oracle_sample"]
-        ips, times = run_oracle(sample, 2, warmup=1, model=args.model)
-        line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port",
+        from oracle.refapi import cpu_model
+
+        sample = 64 if args.model == "resnet18" else 2
+        ips, times, kind, desc = run_reference_cpu(sample, 2, 1, model=args.model)
+        line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": cpu_cores(), "kind": kind,
+                                "cpu_model": cpu_model(),
                                 "sample": f"{sample} images/step x {len(times)} timed steps (1 warm-up) of the "
-                                          "B=256 workload, float64 oracle port"}
+                                          f"B={BATCH} workload; {desc}"}
     print(json.dumps(line), flush=True)
 
 
@@ -336,7 +362,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        reference_arm(args, rank)
+        reference_arm(args, rank, world)
         return
     ours_arm(args, rank, world, local_rank)
 

@@ -103,6 +103,59 @@ def install() -> None:
     _INSTALLED = True
 
 
+_COMPAT = False
+
+
+def install_compat() -> None:
+    """Compat mode: rebind the reference's hot-path MODULES -- ``nsk.tensor``,
+    ``nsk.autodiff``, ``nsk.nn``, ``nsk.gradcheck`` and the error types of ``nsk.errors`` -- to this package, so
+    code written against the reference's Python API (its own unit tests: pkg/tests/test_tensor.py,
+    test_autodiff.py, test_nn.py) runs on the device unchanged. Must run before that code imports names from
+    those modules by value. The reference's pure-numpy ``gradient_rule`` / ``_saved_dict`` / ``plain_matmul``
+    stay (they are tested as functions of numpy arrays and are not on the device path)."""
+    global _COMPAT
+    if _COMPAT:
+        return
+    _import_reference()
+    import nsk
+    import nsk.errors as r_errors
+
+    from . import errors as E
+
+    for name in ("NskError", "NskRuntimeError", "NskTypeError", "DataLoadError"):
+        setattr(r_errors, name, getattr(E, name))
+        if hasattr(nsk, name):
+            setattr(nsk, name, getattr(E, name))
+    import nsk.autodiff as r_autodiff
+    import nsk.gradcheck as r_gradcheck
+    import nsk.nn as r_nn
+    import nsk.tensor as r_tensor
+
+    from . import autodiff as A
+    from . import nn as N
+    from . import tensor as T
+    from . import _lib
+
+    _lib.ctx.init()
+    tensor_names = ("Buffer", "Pool", "Tensor", "GradCache", "tensor_from_array", "empty_tensor", "release_tensor",
+                    "matmul_t", "elementwise", "bias_add", "onehot")
+    for mod in (r_tensor, r_autodiff, r_nn, r_gradcheck):
+        for name in tensor_names:
+            if hasattr(mod, name):
+                setattr(mod, name, getattr(T, name))
+    for name in ("BackwardNode", "Tape", "operand_node", "record", "push_assignment", "make_param", "make_data",
+                 "rec_matmul_t", "rec_elementwise", "rec_bias_add", "rec_onehot", "rec_sum_loss",
+                 "rec_cross_entropy", "reclaim", "backward"):
+        setattr(r_autodiff, name, getattr(A, name))
+    for name in ("Tape", "backward", "push_assignment"):
+        setattr(r_gradcheck, name, getattr(A, name))
+    for name in ("Hyperparams", "ParamGroup", "xavier_uniform_init", "linear", "cross_entropy", "sum_loss",
+                 "sgd_step", "adamw_step", "clip_grad_norm", "rec_bias_add", "rec_cross_entropy", "rec_matmul_t",
+                 "rec_sum_loss"):
+        setattr(r_nn, name, getattr(N, name) if hasattr(N, name) else getattr(A, name))
+    _COMPAT = True
+
+
 def main(argv=None) -> int:
     argv = list(sys.argv[1:] if argv is None else argv)
     if not argv or argv[0] != "run":

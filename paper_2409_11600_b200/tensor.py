@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import numbers
 import threading
 
 import numpy as np
@@ -99,8 +100,11 @@ class Buffer:
 
     @property
     def storage(self) -> np.ndarray:
-        """Host snapshot of the contents (reference exposes a writable numpy view; use ``upload`` to write)."""
-        return self.host()
+        """The contents as a host array (reference tensor.py:40-48 exposes the memory itself): item assignment
+        on the returned array (``storage[:] = v``, ``storage[i] = v``) is written back to the device."""
+        view = self.host().view(_StorageView)
+        view._dev = self
+        return view
 
     def upload(self, array) -> None:
         arr = np.ascontiguousarray(np.asarray(array, dtype=np.float32).reshape(-1))
@@ -134,6 +138,20 @@ class Buffer:
         return f"Buffer(capacity={self.capacity}, dtype={_lib.DTYPE_NAME[self.dtype]}, origin={self.origin})"
 
 
+class _StorageView(np.ndarray):
+    """Host copy of a device Buffer whose item assignment writes the whole copy back (Buffer.storage)."""
+
+    _dev = None
+
+    def __array_finalize__(self, obj):
+        self._dev = None  # slices and results of arithmetic are plain host values
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        if self._dev is not None:
+            self._dev.upload(self.view(np.ndarray))
+
+
 def to_bf16_bits(a: np.ndarray) -> np.ndarray:
     """float32 -> bf16 bit patterns, round-to-nearest-even (matches __float2bfloat16_rn)."""
     u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
@@ -152,13 +170,18 @@ def round_bf16(a) -> np.ndarray:
     return (bits.astype(np.uint32) << 16).view(np.float32)
 
 
+def _pool_key(numel: int, dtype: int):
+    return numel if dtype == F32 else (numel, dtype)
+
+
 class Pool:
     """Size-keyed free lists of reusable device buffers (reference tensor.py:54-113)."""
 
     def __init__(self, enabled: bool = True, poison: bool = False):
         self.enabled = enabled
         self.poison = poison
-        self.free_lists: dict[tuple[int, int], list[Buffer]] = {}
+        # keyed by element count exactly as the reference (tensor.py:78) for float32; (numel, dtype) otherwise
+        self.free_lists: dict[int | tuple[int, int], list[Buffer]] = {}
         self.fresh_allocations = 0
         self.pool_hits = 0
         self.releases = 0
@@ -167,7 +190,7 @@ class Pool:
     def acquire(self, numel: int, dtype: int = F32) -> Buffer:
         if numel < 1:
             raise NskRuntimeError(f"cannot allocate a buffer of {numel} elements")
-        key = (numel, dtype)
+        key = _pool_key(numel, dtype)
         if self.enabled:
             with self._lock:
                 free = self.free_lists.get(key)
@@ -198,7 +221,7 @@ class Pool:
             if self.poison:
                 buffer.fill(float("nan"))
             buffer.in_pool = True
-            self.free_lists.setdefault((buffer.capacity, buffer.dtype), []).append(buffer)
+            self.free_lists.setdefault(_pool_key(buffer.capacity, buffer.dtype), []).append(buffer)
 
     def free_total(self) -> int:
         with self._lock:
@@ -263,6 +286,62 @@ class DeviceScalar:
 
     def __repr__(self):
         return f"DeviceScalar({float(self):g})"
+
+    # arithmetic / comparison read the value (a sync), so callers written against the reference's plain floats
+    # (nn.clip_grad_norm returns the scale, nn.py:122-139) keep working
+    def __eq__(self, other):
+        return float(self) == other
+
+    def __ne__(self, other):
+        return float(self) != other
+
+    def __lt__(self, other):
+        return float(self) < other
+
+    def __le__(self, other):
+        return float(self) <= other
+
+    def __gt__(self, other):
+        return float(self) > other
+
+    def __ge__(self, other):
+        return float(self) >= other
+
+    __hash__ = object.__hash__
+
+    def __add__(self, other):
+        return float(self) + other
+
+    __radd__ = __add__
+
+    def __sub__(self, other):
+        return float(self) - other
+
+    def __rsub__(self, other):
+        return other - float(self)
+
+    def __mul__(self, other):
+        return float(self) * other
+
+    __rmul__ = __mul__
+
+    def __truediv__(self, other):
+        return float(self) / other
+
+    def __rtruediv__(self, other):
+        return other / float(self)
+
+    def __neg__(self):
+        return -float(self)
+
+    def __abs__(self):
+        return abs(float(self))
+
+    def __bool__(self):
+        return bool(float(self))
+
+
+numbers.Real.register(DeviceScalar)
 
 
 # --- tensors --------------------------------------------------------------------------

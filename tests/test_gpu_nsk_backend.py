@@ -21,7 +21,8 @@ def _ref_path():
     for c in REF_CANDIDATES:
         if os.path.isdir(os.path.join(c, "nsk")):
             return c
-    pytest.skip("the reference package is not installed (baseline/_ref)")
+    raise AssertionError("the reference package is not installed: run tools/install_reference.sh (baseline/_ref "
+                         "travels to the GPU box with the working tree)")
 
 
 def _dataset(d):
