@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(ROOT, "baseline", "_ref")
 REF_TESTS = os.path.join(REF, "ref_tests")
-FILES = ("test_tensor.py", "test_autodiff.py", "test_nn.py")
+# test counts of each file on the reference's own CPU path (pkg/tests): all of them must pass here
+FILES = {"test_tensor.py": 33, "test_autodiff.py": 25, "test_nn.py": 27}
 
 
 def _run(files, plugin=True):
@@ -36,14 +37,15 @@ def _run(files, plugin=True):
     return r
 
 
-@pytest.mark.parametrize("name", FILES)
+@pytest.mark.parametrize("name", sorted(FILES))
 def test_reference_unit_tests_pass_on_device(name):
     r = _run([name])
     tail = (r.stdout + r.stderr)[-4000:]
     assert r.returncode == 0, tail
-    m = re.search(r"(\d+) passed", r.stdout)
-    assert m and int(m.group(1)) > 0, tail
-    assert "failed" not in r.stdout.splitlines()[-1], tail
+    last = r.stdout.strip().splitlines()[-1]
+    m = re.search(r"(\d+) passed", last)
+    assert m and int(m.group(1)) == FILES[name], tail  # every reference test ran and passed (none skipped)
+    assert "failed" not in last and "skipped" not in last and "error" not in last, tail
 
 
 def test_compat_mode_really_binds_the_device_backend():
