@@ -223,6 +223,17 @@ uint64_t nsk_gru_bwd_workspace(int T, int B, int H);
 int nsk_gru_bwd(const float* dhs, const float* U, const float* hs, const float* gates, int T, int B, int H, float* dgx,
                 float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream);
 
+/* tensor-core GRU recurrence (gru_tc.cu): one thread-block cluster of H/32 CTAs for all T steps, U resident
+ * in shared memory as bf16 (Ubf [3H, H] = the bf16 shadow of U), h / dgh exchanged per step through rings in
+ * `ws` (nsk_gru_tc_workspace bytes), one tcgen05.mma chain per step, fp32 state and gate math. Same outputs as
+ * nsk_gru_fwd / nsk_gru_bwd. Shapes: 1 <= B <= 64, H in 128..512 with H % 64 == 0 (nsk_gru_tc_supported). */
+int nsk_gru_tc_supported(int B, int H);
+uint64_t nsk_gru_tc_workspace(int B, int H);
+int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, float* gates,
+                   void* ws, uint64_t ws_bytes, void* stream);
+int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const float* gates, int T, int B, int H,
+                   float* dgx, float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream);
+
 /* ---- communication (comm.cu): NCCL over NVLink / NVSwitch ---- */
 int nsk_comm_unique_id(uint8_t* out128);
 int nsk_comm_init(int rank, int world, const uint8_t* uid128, void** comm_out);

@@ -344,18 +344,28 @@ class GRUOracle:
         self.params["head_b"] = np.zeros(classes, np.float32)
         self.order = ["table", "w", "b", "u", "c", "head_w", "head_b"]
 
-    def loss_and_grads(self, tokens, y):
+    def loss_and_grads(self, tokens, y, bf16=False, recurrent_bf16=None):
+        """float64 composition of the reference primitives. ``bf16=True`` rounds to bfloat16 exactly where the
+        device feeds its tensor cores (layers.gru / gru_tc.cu): the embedded inputs and W for the input
+        projection, h and U for the recurrent product, dgh for the recurrent backward product, and the operands
+        of the batched weight / input gradients (dgx, dgh, x, h_prev, W); the input gradient is stored bf16.
+        Gate math, state and accumulation stay float64 (the device: fp32). ``recurrent_bf16=False`` keeps the
+        recurrence itself exact (the fp32 cooperative kernel the device uses for shapes the cluster kernel does
+        not tile)."""
+        q = X.round_bf16 if bf16 else (lambda a: np.asarray(a, np.float64))
+        qr = q if (bf16 if recurrent_bf16 is None else recurrent_bf16) else (lambda a: np.asarray(a, np.float64))
         p = {k: v.astype(np.float64) for k, v in self.params.items()}
         H = self.H
         tok = np.asarray(tokens).astype(np.int64)  # [B, T]
         B, T = tok.shape
         W, b, U, c = p["w"], p["b"], p["u"], p["c"]
-        xs = [p["table"][tok[:, t]] for t in range(T)]
+        Wq, Uq = q(W).astype(np.float64), qr(U).astype(np.float64)
+        xs = [q(p["table"][tok[:, t]]).astype(np.float64) for t in range(T)]
         h = np.zeros((B, H))
         cache = []
         for t in range(T):
-            gx = xs[t] @ W.T + b
-            gh = h @ U.T + c
+            gx = xs[t] @ Wq.T + b
+            gh = qr(h).astype(np.float64) @ Uq.T + c
             r = _sig(gx[:, :H] + gh[:, :H])
             z = _sig(gx[:, H:2 * H] + gh[:, H:2 * H])
             a = gh[:, 2 * H:]
@@ -380,11 +390,12 @@ class GRUOracle:
             dzp = dz * z * (1 - z)
             dgx = np.concatenate([drp, dzp, dnp], axis=1)
             dgh = np.concatenate([drp, dzp, dnp * r], axis=1)
-            gW += dgx.T @ xs[t]
+            dgxq, dghq = q(dgx).astype(np.float64), q(dgh).astype(np.float64)
+            gW += dgxq.T @ xs[t]
             gb += dgx.sum(axis=0)
-            gU += dgh.T @ hp
+            gU += dghq.T @ q(hp).astype(np.float64)
             gc += dgh.sum(axis=0)
-            np.add.at(gtable, tok[:, t], dgx @ W)
-            dh = dh * z + dgh @ U
+            np.add.at(gtable, tok[:, t], q(dgxq @ Wq).astype(np.float64))
+            dh = dh * z + qr(dgh).astype(np.float64) @ Uq
         grads.update({"w": gW, "b": gb, "u": gU, "c": gc, "table": gtable})
         return loss, grads, logits

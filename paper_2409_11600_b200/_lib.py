@@ -109,6 +109,10 @@ SIGNATURES = {
     "nsk_gru_fwd": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
     "nsk_gru_bwd": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
     "nsk_gru_bwd_workspace": (u64, [i32, i32, i32]),
+    "nsk_gru_tc_supported": (i32, [i32, i32]),
+    "nsk_gru_tc_workspace": (u64, [i32, i32]),
+    "nsk_gru_fwd_tc": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp, u64, vp]),
+    "nsk_gru_bwd_tc": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
     "nsk_comm_unique_id": (i32, [vp]),
     "nsk_comm_init": (i32, [i32, i32, vp, C.POINTER(vp)]),
     "nsk_comm_destroy": (i32, [vp]),
@@ -119,6 +123,22 @@ SIGNATURES = {
 
 _lib = None
 _lock = threading.Lock()
+
+
+def _bundled_nccl() -> str | None:
+    """Path of the libnccl.so.2 PyTorch ships (nvidia-nccl wheel), found without importing torch. One process
+    holds one libnccl.so.2 and torch needs its own version, so libnskb uses the same file."""
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
 
 
 def load():
@@ -133,6 +153,10 @@ def load():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(there is no CPU fallback)")
+        if "NSK_NCCL_LIB" not in os.environ:  # comm.cu binds NCCL at run time: prefer PyTorch's bundled copy
+            nccl = _bundled_nccl()
+            if nccl:
+                os.environ["NSK_NCCL_LIB"] = nccl
         lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name, None)

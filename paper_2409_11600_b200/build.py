@@ -26,7 +26,7 @@ CFLAGS = ARCH + [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
 ] + os.environ.get("NSK_CFLAGS_EXTRA", "").split()
-LDFLAGS = ["-shared", "-lcudart", "-l:libnccl.so.2"]
+LDFLAGS = ["-shared", "-lcudart", "-ldl"]
 
 
 def _sources():

@@ -1,0 +1,550 @@
+// Fused GRU recurrence on the tensor cores (K16, tcgen05): one thread-block cluster walks all T steps.
+//
+// Reference: the reference has no GRU op; SURVEY.md A26 defines it as the composition of its primitives
+// (linear = matmul_t + bias-add, sigmoid, tanh, hadamard, add, neg, scalar-add: tensor.py:213-296,
+// autodiff.py:253-293):
+//   r = s(gx_r + h U_r^T + c_r)      z = s(gx_z + h U_z^T + c_z)
+//   a = h U_n^T + c_n                 n = tanh(gx_n + r * a)
+//   h' = n - z * n + z * h
+// gx = x W^T + b for all T steps is one tcgen05 GEMM on the host side; this file is the recurrence.
+//
+// Forward (one cluster of CL = H / 32 CTAs, CTA q owns hidden units [32q, 32q + 32)):
+//   * the CTA's 96 rows of U (r, z, n rows of its units) stay resident in shared memory (bf16, 128B-swizzled
+//     K-major, loaded once by TMA) -- the B operand of every step;
+//   * per step the full h_t (bf16, [B, H]) is TMA-loaded from a global exchange ring into shared memory (the A
+//     operand, K-major; M = 128 rows of which the first B are the batch -- rows past B are never read back);
+//   * one elected thread issues H/16 tcgen05.mma (M = 128, N = 96, K = 16) into TMEM: D[b][g*32 + u] = h U_g^T;
+//   * four epilogue warps read D with tcgen05.ld (thread = batch row), fuse the gate math in fp32 with the
+//     fp32 state h (kept in registers for the whole sequence), write h_{t+1} (fp32, and bf16 into the ring),
+//     the saved gates (r, z, n, a) for backward;
+//   * one hardware cluster barrier per step publishes h_{t+1} (release/acquire; the ring's other slot is the
+//     one being written, so a step never overwrites what a peer may still be loading).
+//
+// Backward (BPTT, reverse sweep; the same cluster, arranged RG x CG):
+//   dh_{t-1} = dh_t * z_t + dgh_t U       (dgh = [dr', dz', dn' * r], the gradient w.r.t. h U^T + c)
+// CTA (i, j) owns units [j*H/CG + 32 i, +32); it keeps U[rows of row group i, cols of column group j] resident
+// (bf16, MN-major B operand), and per step:
+//   A) forms dh_t for its units from the partial products of step t+1, the gate derivatives (fp32), writes
+//      dgx / dgh (fp32, for the batched weight-gradient GEMMs) and its dgh block (bf16) into a global ring;
+//   -- cluster barrier --
+//   B) TMA-loads the dgh of its row group (K = 3*32*CG gate rows) and issues tcgen05.mma into TMEM:
+//      P[b][k] = sum over the row group's gate rows of dgh * U, k over its column group; the epilogue writes the
+//      slice of P that belongs to each CTA of the column group into a global partial ring;
+//   -- cluster barrier --
+// so each CTA exchanges 1/CG of dgh and 1/RG of the partial sums per step instead of the full dgh.
+//
+// Precision: the MMA operands are bf16 (h, dgh, U), accumulation and all gate math / state fp32 (SURVEY.md
+// §7 hard part 5; oracle/restated.gru_*_bf16 emulates exactly these roundings).
+#include "common.cuh"
+#include "../../include/nskb.h"
+
+namespace {
+
+constexpr int kUC = 32;         // hidden units per CTA
+constexpr int kThreads = 256;   // 8 warps: 0,1,4,5 epilogue | 2 TMA | 3 MMA + TMEM | 6,7 idle
+constexpr int kMaxB = 64;       // batch rows (A operand rows that are read back)
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// 32 lanes x 16 consecutive fp32 columns (thread t of the warp: lane base + t)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* f) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float sigm(float x) {  // the reference's stable sigmoid (tensor.py:237-244)
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+
+__device__ __forceinline__ void ld16(const float* p, float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) *(float4*)(v + 4 * i) = __ldcg((const float4*)(p + 4 * i));
+}
+__device__ __forceinline__ void st16(float* p, const float* v) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) *(float4*)(p + 4 * i) = *(const float4*)(v + 4 * i);
+}
+__device__ __forceinline__ void st16_bf16(__nv_bfloat16* p, const float* v) {
+  uint4 a, b;
+  a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]); a.z = pack_bf16x2(v[4], v[5]);
+  a.w = pack_bf16x2(v[6], v[7]);
+  b.x = pack_bf16x2(v[8], v[9]); b.y = pack_bf16x2(v[10], v[11]); b.z = pack_bf16x2(v[12], v[13]);
+  b.w = pack_bf16x2(v[14], v[15]);
+  ((uint4*)p)[0] = a;
+  ((uint4*)p)[1] = b;
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// forward
+// smem: [U rows: H/64 chunks x 96 rows x 128 B] [h: H/64 chunks x 64 rows x 128 B] [8 KB slack: M = 128 rows of
+// the last chunk] [mbarriers]
+struct FwdArgs {
+  const float* gx;   // [T][B][3H] (includes b)
+  const float* c;    // [3H]
+  float* hs;         // [T+1][B][H], hs[0] = h0 on entry
+  float* gates;      // [T][B][4][H]  (r, z, n, a)
+  __nv_bfloat16* hx; // [2][B][H] exchange ring
+  int T, B, H;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
+                                                                 const __grid_constant__ CUtensorMap tmH,
+                                                                 const FwdArgs p) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H;
+  const int NCH = H / 64;                  // K chunks
+  uint8_t* us = smem;                      // NCH x 12 KB
+  uint8_t* hsm = us + NCH * 12288;         // NCH x 8 KB (+8 KB slack)
+  uint64_t* bars = (uint64_t*)(hsm + NCH * 8192 + 8192);
+  uint64_t* ufull = bars;                  // 1
+  uint64_t* hfull = bars + 1;              // NCH (one per K chunk: the MMAs start on chunk 0 while the rest land)
+  uint64_t* mdone = hfull + NCH;           // 1
+  uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int q = (int)cluster_rank();
+  const int j0 = q * kUC;
+  if (threadIdx.x == 0) {
+    mbar_init(ufull, 1);
+    for (int c = 0; c < NCH; ++c) mbar_init(&hfull[c], 1);
+    mbar_init(mdone, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmH);
+  }
+  if (warp == 3) {
+    tmem_alloc(tmem_slot, 128);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // epilogue identity: warps 0,1,4,5 -> batch row b (TMEM lane), units [16 hf, 16 hf + 16) of this CTA
+  const bool epi = (warp & 2) == 0;
+  const int sp = warp & 1, hf = warp >> 2;
+  const int b = sp * 32 + lane;
+  const bool row_ok = epi && b < B;
+  const int ju = j0 + hf * 16;  // first global unit of this thread
+  float h[16], cr[16], cz[16], cn[16];
+  if (row_ok) {
+    ld16(p.hs + (size_t)b * H + ju, h);
+    ld16(p.c + ju, cr);
+    ld16(p.c + H + ju, cz);
+    ld16(p.c + 2 * H + ju, cn);
+    st16_bf16(p.hx + (size_t)b * H + ju, h);  // ring slot 0 = bf16(h0)
+  }
+  if (warp == 2 && elect_one()) {  // U rows of this CTA: 3 gates x NCH chunks of {64 k, 32 rows}
+    mbar_expect_tx(ufull, (uint32_t)(NCH * 12288));
+    for (int c = 0; c < NCH; ++c)
+      for (int g = 0; g < 3; ++g) tma_load_2d(&tmU, ufull, us + c * 12288 + g * 4096, c * 64, g * H + j0);
+  }
+  fence_proxy_async_global();
+
+  const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
+  for (int t = 0; t < T; ++t) {
+    // h_t (ring slot t & 1) is complete in global memory once every CTA of the cluster has passed this point
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    fence_proxy_async_global();
+    if (warp == 2) {
+      if (elect_one()) {
+        for (int c = 0; c < NCH; ++c) {
+          mbar_expect_tx(&hfull[c], (uint32_t)(B * 128));
+          tma_load_2d(&tmH, &hfull[c], hsm + c * 8192, c * 64, (t & 1) * B);
+        }
+      }
+      __syncwarp();
+    } else if (warp == 3) {
+      if (t == 0) mbar_wait(ufull, 0);
+      const uint32_t sh = smem_u32(hsm), su = smem_u32(us);
+      for (int c = 0; c < NCH; ++c) {
+        mbar_wait(&hfull[c], t & 1);
+        tc_fence_after();
+        const uint64_t ad = sdesc_sw128(sh + c * 8192, 16, 1024);
+        const uint64_t bd = sdesc_sw128(su + c * 12288, 16, 1024);
+        if (elect_one()) {
+          umma_off<0, 0, false>(tmem, ad, bd, idesc, c > 0 ? 1u : 0u);
+          umma_off<2, 2, false>(tmem, ad, bd, idesc, 1u);
+          umma_off<4, 4, false>(tmem, ad, bd, idesc, 1u);
+          umma_off<6, 6, false>(tmem, ad, bd, idesc, 1u);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(mdone);
+      __syncwarp();
+    } else if (epi) {
+      float gr[16], gz[16], gn[16];
+      if (row_ok) {  // independent of the MMA: in flight while it runs
+        const float* g3 = p.gx + ((size_t)t * B + b) * H3 + ju;
+        ld16(g3, gr);
+        ld16(g3 + H, gz);
+        ld16(g3 + 2 * H, gn);
+      }
+      mbar_wait_backoff(mdone, t & 1);
+      tc_fence_after();
+      float dr[16], dz[16], dn[16];
+      const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16) + hf * 16;
+      tmem_ld16(ta, dr);
+      tmem_ld16(ta + 32, dz);
+      tmem_ld16(ta + 64, dn);
+      tmem_ld_wait();
+      if (row_ok) {
+        float r[16], z[16], n[16], a[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          r[u] = sigm(gr[u] + dr[u] + cr[u]);
+          z[u] = sigm(gz[u] + dz[u] + cz[u]);
+          a[u] = dn[u] + cn[u];
+          n[u] = tanhf(gn[u] + r[u] * a[u]);
+          h[u] = n[u] - z[u] * n[u] + z[u] * h[u];
+        }
+        st16(p.hs + ((size_t)(t + 1) * B + b) * H + ju, h);
+        float* gs = p.gates + ((size_t)t * B + b) * 4 * H + ju;
+        st16(gs, r);
+        st16(gs + H, z);
+        st16(gs + 2 * H, n);
+        st16(gs + 3 * H, a);
+        st16_bf16(p.hx + ((size_t)((t + 1) & 1) * B + b) * H + ju, h);
+      }
+      fence_proxy_async_global();  // h_{t+1} is read by peers' TMA (async proxy) after the barrier
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 3) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 128);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------------------
+// backward
+struct BwdArgs {
+  const float* dhs;    // [T][B][H] external gradient of each h_{t+1}
+  const float* hs;     // [T+1][B][H]
+  const float* gates;  // [T][B][4][H]
+  float* dgx;          // [T][B][3H]
+  float* dgh;          // [T][B][3H]
+  float* dh0;          // [B][H]
+  __nv_bfloat16* gex;  // [2][RG][B][KR] dgh exchange ring (bf16)
+  float* pex;          // [2][CL][RG][B][32] partial-product ring
+  int T, B, H, RG, CG;
+};
+
+__global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
+                                                                 const __grid_constant__ CUtensorMap tmG,
+                                                                 const BwdArgs p) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, RG = p.RG, CG = p.CG;
+  const int CL = RG * CG;
+  const int NC = H / CG;            // column-group width (MMA N)
+  const int KR = 3 * kUC * CG;      // gate rows of a row group (MMA K)
+  const int NB = NC / 64;           // 64-column MN blocks of the U block
+  const int NKC = KR / 64;          // 64-row K chunks of the dgh block
+  uint8_t* ub = smem;                              // NB x (KR x 128 B)
+  uint8_t* gsm = ub + NB * KR * 128;               // NKC x 8 KB (+8 KB slack)
+  uint64_t* bars = (uint64_t*)(gsm + NKC * 8192 + 8192);
+  uint64_t* ufull = bars;
+  uint64_t* gfull = bars + 1;                      // NKC
+  uint64_t* mdone = gfull + NKC;
+  uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int q = (int)cluster_rank();
+  const int gi = q / CG, gj = q % CG;              // row group, column group
+  const int j0 = gj * NC + gi * kUC;               // first owned unit
+  if (threadIdx.x == 0) {
+    mbar_init(ufull, 1);
+    for (int c = 0; c < NKC; ++c) mbar_init(&gfull[c], 1);
+    mbar_init(mdone, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmU);
+    tma_prefetch_desc(&tmG);
+  }
+  if (warp == 3) {
+    tmem_alloc(tmem_slot, NC <= 32 ? 32 : (NC <= 64 ? 64 : (NC <= 128 ? 128 : 256)));
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 2 && elect_one()) {
+    // U block: for each owner column j' of row group gi and gate g, the 32 rows g*H + (j' NC + 32 gi) .. +32,
+    // as MN-major K rows (128 B = 64 columns per block)
+    mbar_expect_tx(ufull, (uint32_t)(NB * KR * 128));
+    for (int nb = 0; nb < NB; ++nb)
+      for (int jj = 0; jj < CG; ++jj)
+        for (int g = 0; g < 3; ++g)
+          tma_load_2d(&tmU, ufull, ub + nb * KR * 128 + (jj * 3 + g) * kUC * 128, gj * NC + nb * 64,
+                      g * H + jj * NC + gi * kUC);
+  }
+  const bool epi = (warp & 2) == 0;
+  const int sp = warp & 1, hf = warp >> 2;
+  const int b = sp * 32 + lane;
+  const bool row_ok = epi && b < B;
+  const int ju = j0 + hf * 16;   // first global unit of this thread (phase A)
+  const int uo = hf * 16;        // its offset inside the CTA's 32 units
+  float dhz[16];                 // dh_{t+1} * z_{t+1} carried to the next (earlier) step
+#pragma unroll
+  for (int u = 0; u < 16; ++u) dhz[u] = 0.f;
+  const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
+  for (int t = T - 1; t >= 0; --t) {
+    // ---- A: dh_t for own units, gate derivatives, dgh block ----
+    if (epi) {
+      if (row_ok) {
+        float dh[16], v[16];
+        ld16(p.dhs + ((size_t)t * B + b) * H + ju, dh);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) dh[u] += dhz[u];
+        if (t < T - 1) {
+          const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + (size_t)b * kUC + uo;
+          for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
+            ld16(pp + (size_t)s * B * kUC, v);
+#pragma unroll
+            for (int u = 0; u < 16; ++u) dh[u] += v[u];
+          }
+        }
+        const float* gs = p.gates + ((size_t)t * B + b) * 4 * H + ju;
+        float r[16], z[16], n[16], a[16], hp[16];
+        ld16(gs, r);
+        ld16(gs + H, z);
+        ld16(gs + 2 * H, n);
+        ld16(gs + 3 * H, a);
+        ld16(p.hs + ((size_t)t * B + b) * H + ju, hp);
+        float drp[16], dzp[16], dnp[16], dnr[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const float dn = dh[u] * (1.f - z[u]);
+          const float dz = dh[u] * (hp[u] - n[u]);
+          dnp[u] = dn * (1.f - n[u] * n[u]);
+          drp[u] = dnp[u] * a[u] * r[u] * (1.f - r[u]);
+          dzp[u] = dz * z[u] * (1.f - z[u]);
+          dnr[u] = dnp[u] * r[u];
+          dhz[u] = dh[u] * z[u];
+        }
+        float* gxo = p.dgx + ((size_t)t * B + b) * H3 + ju;
+        float* gho = p.dgh + ((size_t)t * B + b) * H3 + ju;
+        st16(gxo, drp);
+        st16(gxo + H, dzp);
+        st16(gxo + 2 * H, dnp);
+        st16(gho, drp);
+        st16(gho + H, dzp);
+        st16(gho + 2 * H, dnr);
+        if (t == 0) {
+          // dh0 = dh_0 * z_0 + (dgh_0 U)[own units], the partials of step 0 are added after the last barrier
+          st16(p.dh0 + (size_t)b * H + ju, dhz);
+        }
+        __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + b) * KR + gj * 3 * kUC + uo;
+        st16_bf16(ge, drp);
+        st16_bf16(ge + kUC, dzp);
+        st16_bf16(ge + 2 * kUC, dnr);
+      }
+      fence_proxy_async_global();
+    }
+    tc_fence_before();
+    cluster_sync_all();  // every dgh block of step t is in the ring
+    tc_fence_after();
+    // ---- B: P = dgh(row group) . U(row group rows, column group cols), slices to the column group ----
+    fence_proxy_async_global();
+    if (warp == 2) {
+      if (elect_one()) {
+        for (int c = 0; c < NKC; ++c) {
+          mbar_expect_tx(&gfull[c], (uint32_t)(B * 128));
+          tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B);
+        }
+      }
+      __syncwarp();
+    } else if (warp == 3) {
+      if (t == T - 1) mbar_wait(ufull, 0);
+      const uint32_t sg = smem_u32(gsm), su = smem_u32(ub);
+      const uint64_t bd0 = sdesc_sw128(su, (uint32_t)(KR * 128), 1024);
+      for (int c = 0; c < NKC; ++c) {
+        mbar_wait(&gfull[c], (T - 1 - t) & 1);
+        tc_fence_after();
+        const uint64_t ad = sdesc_sw128(sg + c * 8192, 16, 1024);
+        const uint64_t bd = bd0 + (uint64_t)((c * 64 * 128) >> 4);  // 64 K rows further
+        if (elect_one()) {
+          umma_off<0, 0, false>(tmem, ad, bd, idesc, c > 0 ? 1u : 0u);
+          umma_off<2, 128, false>(tmem, ad, bd, idesc, 1u);
+          umma_off<4, 256, false>(tmem, ad, bd, idesc, 1u);
+          umma_off<6, 384, false>(tmem, ad, bd, idesc, 1u);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(mdone);
+      __syncwarp();
+    } else if (epi) {
+      mbar_wait_backoff(mdone, (T - 1 - t) & 1);
+      tc_fence_after();
+      // thread (b, hf) holds columns [hf NC/2, (hf+1) NC/2) = the slices of row groups s in [hf RG/2, (hf+1) RG/2)
+      const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16);
+      for (int s = hf * (RG / 2); s < (hf + 1) * (RG / 2); ++s) {
+        float v0[16], v1[16];
+        tmem_ld16(ta + s * kUC, v0);
+        tmem_ld16(ta + s * kUC + 16, v1);
+        tmem_ld_wait();
+        if (row_ok) {
+          const int dest = s * CG + gj;
+          float* po = p.pex + ((size_t)((t & 1) * CL + dest) * RG + gi) * B * kUC + (size_t)b * kUC;
+          st16(po, v0);
+          st16(po + 16, v1);
+        }
+      }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // partials of step t visible (read in A of step t-1)
+    tc_fence_after();
+  }
+  // dh0 += the step-0 partial products of this CTA's units
+  if (row_ok) {
+    float dh[16], v[16];
+    ld16(p.dh0 + (size_t)b * H + ju, dh);
+    const float* pp = p.pex + ((size_t)q * RG) * B * kUC + (size_t)b * kUC + uo;  // slot (0 & 1) = 0
+    for (int s = 0; s < RG; ++s) {
+      ld16(pp + (size_t)s * B * kUC, v);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) dh[u] += v[u];
+    }
+    st16(p.dh0 + (size_t)b * H + ju, dh);
+  }
+  if (warp == 3) {
+    tc_fence_after();
+    tmem_dealloc(tmem, NC <= 32 ? 32 : (NC <= 64 ? 64 : (NC <= 128 ? 128 : 256)));
+  }
+}
+
+// backward arrangement: CG column groups x RG row groups of CL = H / 32 CTAs with NC = H / CG and KR = 96 CG
+// multiples of 64 (NSK_GRU_CG overrides the choice)
+int bwd_groups(int H, int* rg, int* cg) {
+  const int CL = H / kUC;
+  const char* e = getenv("NSK_GRU_CG");
+  const int want = e ? atoi(e) : 0;
+  int best = 0;
+  for (int c = 1; c <= CL; ++c) {
+    if (CL % c || (H / c) % 64 || (3 * kUC * c) % 64 || H / c > 256 || (CL / c) % 2) continue;
+    if (want ? c == want : (best == 0 || (c <= 4 && c > best))) best = c;
+  }
+  if (!best) return 0;
+  *cg = best;
+  *rg = CL / best;
+  return 1;
+}
+
+size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * (12288 + 8192) + 8192 + 256; }
+size_t bwd_smem(int H, int rg, int cg) {
+  const int NB = H / cg / 64, KR = 3 * kUC * cg;
+  return 1024 + (size_t)NB * KR * 128 + (size_t)(KR / 64) * 8192 + 8192 + 256;
+}
+
+int launch_cluster(const void* fn, int cl, size_t smem, void** args, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && cl > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  if (e != cudaSuccess) return nsk::cuda_status(e, "gru_tc: cudaFuncSetAttribute");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelExC(&cfg, fn, args);
+  if (e != cudaSuccess) return nsk::cuda_status(e, "gru_tc: cluster launch");
+  return NSK_OK;
+}
+
+int tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  const uint64_t dims[2] = {cols, rows};
+  const uint64_t str[1] = {cols * 2};
+  const uint32_t box[2] = {64, box_rows};
+  return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, str, box, nullptr,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsk_gru_tc_supported(int B, int H) {
+  int rg, cg;
+  return B >= 1 && B <= kMaxB && H % 64 == 0 && H >= 128 && H <= 16 * kUC && bwd_groups(H, &rg, &cg);
+}
+
+uint64_t nsk_gru_tc_workspace(int B, int H) {
+  int rg = 1, cg = 1;
+  bwd_groups(H, &rg, &cg);
+  const uint64_t CL = (uint64_t)H / kUC, KR = 3ull * kUC * cg;
+  const uint64_t hx = 2ull * B * H * 2;                // forward ring
+  const uint64_t gex = 2ull * rg * B * KR * 2;         // backward dgh ring
+  const uint64_t pex = 2ull * CL * rg * B * kUC * 4;   // backward partial ring
+  return ((hx + 255) / 256 + (gex + 255) / 256) * 256 + pex;
+}
+
+int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, float* gates,
+                   void* ws, uint64_t ws_bytes, void* stream) {
+  if (!nsk_gru_tc_supported(B, H) || T < 1)
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: needs 1 <= B <= 64 and H in 128..512, H % 64 == 0");
+  if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
+  CUtensorMap tmU, tmH;
+  int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
+  if (rc) return rc;
+  __nv_bfloat16* hx = (__nv_bfloat16*)ws;
+  if ((rc = tmap_2d_bf16(&tmH, hx, (uint64_t)2 * B, (uint64_t)H, (uint32_t)B))) return rc;
+  FwdArgs a{gx, c, hs, gates, hx, T, B, H};
+  void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
+  return launch_cluster((const void*)gru_fwd_tc_kernel, H / kUC, fwd_smem(H), args, (cudaStream_t)stream);
+}
+
+int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const float* gates, int T, int B, int H,
+                   float* dgx, float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream) {
+  if (!nsk_gru_tc_supported(B, H) || T < 1)
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: needs 1 <= B <= 64 and H in 128..512, H % 64 == 0");
+  if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
+  int rg, cg;
+  bwd_groups(H, &rg, &cg);
+  const int KR = 3 * kUC * cg;
+  uint8_t* w = (uint8_t*)ws;
+  const uint64_t hx_bytes = ((2ull * B * H * 2 + 255) / 256) * 256;
+  __nv_bfloat16* gex = (__nv_bfloat16*)(w + hx_bytes);
+  float* pex = (float*)(w + hx_bytes + ((2ull * rg * B * KR * 2 + 255) / 256) * 256);
+  CUtensorMap tmU, tmG;
+  int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
+  if (rc) return rc;
+  if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)B))) return rc;
+  BwdArgs a{dhs, hs, gates, dgx, dgh, dh0, gex, pex, T, B, H, rg, cg};
+  void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
+  return launch_cluster((const void*)gru_bwd_tc_kernel, H / kUC, bwd_smem(H, rg, cg), args, (cudaStream_t)stream);
+}
+
+}  // extern "C"

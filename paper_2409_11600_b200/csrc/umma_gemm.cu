@@ -83,8 +83,10 @@ struct UmmaProb {
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
-constexpr int kStgPitch = 64;          // epilogue staging: dense 32 x 32 bf16 blocks (TMA-store source)
+constexpr int kStgPitch = 64;          // epilogue staging: 32 x 32 bf16 blocks, 64B-swizzled (TMA-store source)
 constexpr int kStgBytes = 32 * kStgPitch;
+// byte offset of 16-byte chunk c (of 4) in row r of a staging block: the SWIZZLE_64B pattern (chunk ^= row / 2 % 4)
+__device__ __forceinline__ int stg_off(int r, int c) { return r * kStgPitch + ((c ^ ((r >> 1) & 3)) << 4); }
 
 template <int ESZ>
 struct KT {
@@ -103,7 +105,8 @@ struct Smem {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int W_OFF = STAGES * STAGE_BYTES;                      // resident filter taps (WRES)
   static constexpr int BAR_OFF = W_OFF + (WRES ? 9 * B1_BYTES : 0);
-  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 5) + 16 + 127) / 128 * 128;  // TMA-store source
+  // TMA-store source; 512-byte aligned: the SWIZZLE_64B pattern is taken from address bits 7-8
+  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 5) + 16 + 511) / 512 * 512;
   // staging buffers per epilogue warp: double-buffered with 8 warps (one CTA per SM anyway); single with 4 so
   // the 64/128-wide tiles keep two CTAs per SM
   static constexpr int NSTG = EPI == 8 ? 2 : 1;
@@ -650,11 +653,11 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             u4[t].z = pack_bf16x2(f[8 * t + 4], f[8 * t + 5]);
             u4[t].w = pack_bf16x2(f[8 * t + 6], f[8 * t + 7]);
           }
+          // 64-byte-swizzled staging (the TMA store map uses SWIZZLE_64B): 16-byte chunk c of row r sits at chunk
+          // c ^ ((r >> 1) & 3). Each quarter-warp store then covers all 32 banks exactly once, and the chunk index
+          // of the register operand stays static (a lane-dependent register index spilled u4 to local memory)
 #pragma unroll
-          for (int c4 = 0; c4 < 4; ++c4) {  // rotated 16-byte chunks: 4-way instead of 16-way bank conflicts
-            const int t = (c4 + lane) & 3;
-            *(uint4*)(stg + lane * kStgPitch + t * 16) = u4[t];
-          }
+          for (int c4 = 0; c4 < 4; ++c4) *(uint4*)(stg + stg_off(lane, c4)) = u4[c4];
           if (p.tma_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (p.stats) {
@@ -663,7 +666,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             float s1 = 0.f, s2 = 0.f;
 #pragma unroll 8
             for (int rr = 0; rr < 32; ++rr) {
-              const float v = __bfloat162float(*(const __nv_bfloat16*)(stg + rr * kStgPitch + lane * 2));
+              const float v =
+                  __bfloat162float(*(const __nv_bfloat16*)(stg + stg_off(rr, lane >> 3) + (lane & 7) * 2));
               if ((okm >> rr) & 1u) {
                 s1 += v;
                 s2 += v * v;
@@ -705,7 +709,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             const int ok = __shfl_sync(0xffffffffu, (int)row_ok, pr);
             if (ok) {
               uint4* dst = (uint4*)((__nv_bfloat16*)p.out + ro + col0 + part * 8);
-              uint4 val = *(const uint4*)(stg + pr * kStgPitch + part * 16);
+              uint4 val = *(const uint4*)(stg + stg_off(pr, part));
               if (p.beta != 0.f) val = bf16x8_axpby(*dst, p.beta, val);  // accumulate into an existing gradient
               *dst = val;
             }
@@ -1387,7 +1391,7 @@ bool out_map(CUtensorMap* m, void* out, long long M, int N, long long ldc) {
   uint64_t str[1] = {(uint64_t)ldc * 2};
   uint32_t box[2] = {32, 32};
   return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, str, box, nullptr,
-                          CU_TENSOR_MAP_SWIZZLE_NONE) == NSK_OK;
+                          CU_TENSOR_MAP_SWIZZLE_64B) == NSK_OK;  // matches the staging layout (stg_off)
 }
 
 bool force_i2c() {

@@ -36,17 +36,26 @@ def _event():
 
 
 class DataParallel:
-    def __init__(self, session, rank: int, world: int, bucket_mb: float = 4.0, uid: bytes | None = None):
+    """``allreduce`` (tests only): a callable ``(ptr, count, dtype, stream)`` used instead of NCCL -- e.g. a host
+    gloo all-reduce so two processes sharing one GPU can exercise the bucketing and hooks; no NCCL communicator
+    is created then."""
+
+    def __init__(self, session, rank: int, world: int, bucket_mb: float = 4.0, uid: bytes | None = None,
+                 allreduce=None):
         self.s = session
         self.rank, self.world = rank, world
         self.bucket_elems = max(1, int(bucket_mb * (1 << 20) / 4))
         lib = _lib.lib()
-        if uid is None:
-            uid = self._exchange_uid()
-        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
-        comm = C.c_void_p()
-        check(lib.nsk_comm_init(rank, world, buf, C.byref(comm)))
-        self.comm = comm.value
+        self.comm = None
+        self._allreduce_fn = allreduce
+        if allreduce is None:
+            if uid is None:
+                uid = self._exchange_uid()
+            buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+            comm = C.c_void_p()
+            check(lib.nsk_comm_init(rank, world, buf, C.byref(comm)))
+            self.comm = comm.value
+        self.launch_log: list[int] = []  # bucket indices in launch order (host-side record, for tests)
         s = C.c_void_p()
         check(lib.nsk_stream_create(C.byref(s)))
         self.comm_stream = s.value
@@ -57,6 +66,13 @@ class DataParallel:
         self.ev_done = _event()
         session.param_group.grad_scale = 1.0 / world
         session.grad_cache.hooks.append(self._on_param_final)
+
+    def allreduce(self, ptr: int, count: int, dtype: int, stream) -> None:
+        """In-place sum over ranks of ``count`` elements at ``ptr``, enqueued on ``stream``."""
+        if self._allreduce_fn is not None:
+            self._allreduce_fn(ptr, count, dtype, stream)
+        else:
+            check(_lib.lib().nsk_allreduce(self.comm, ptr, count, dtype, stream))
 
     def _exchange_uid(self) -> bytes:
         import torch.distributed as dist
@@ -78,7 +94,7 @@ class DataParallel:
         for _name, t in self.s.param_group.params:
             if self.rank != 0:
                 check(lib.nsk_fill_f32(t.ptr, t.numel, 0.0, st))
-            check(lib.nsk_allreduce(self.comm, t.ptr, t.numel, F32, st))
+            self.allreduce(t.ptr, t.numel, F32, st)
             t.version += 1
         _lib.sync()
 
@@ -122,8 +138,9 @@ class DataParallel:
         check(lib.nsk_event_record(self.ev_compute[i], _lib.stream()))
         check(lib.nsk_event_wait(self.comm_stream, self.ev_compute[i]))
         SIDE.order_after(self.comm_stream)  # weight gradients forked onto the side stream (side.py)
-        check(lib.nsk_allreduce(self.comm, ptr, count, F32, self.comm_stream))
+        self.allreduce(ptr, count, F32, self.comm_stream)
         self.launched[i] = True
+        self.launch_log.append(i)
 
     def begin_step(self):
         if self.buckets is None and self.s.grad_cache.arena is not None:
@@ -138,8 +155,9 @@ class DataParallel:
         cache = self.s.grad_cache
         if self.buckets is None:
             # first (eager) step: the arena does not exist yet -> reduce parameter by parameter
+            SIDE.order_after(st)
             for name, buf in cache.grads.items():
-                check(lib.nsk_allreduce(self.comm, buf.ptr, buf.capacity, F32, st))
+                self.allreduce(buf.ptr, buf.capacity, F32, st)
             return
         for i, done in enumerate(self.launched):
             if not done:
@@ -152,6 +170,13 @@ class DataParallel:
         """Sum of an integer over ranks (e.g. correct predictions for accuracy, bit-exact)."""
         from .tensor import Buffer
 
+        if self.comm is None:  # injected transport (tests): the host process group sums it
+            import torch
+            import torch.distributed as dist
+
+            t = torch.tensor([int(value)], dtype=torch.int64)
+            dist.all_reduce(t)
+            return int(t[0])
         b = Buffer(1, F32)
         arr = np.array([value], np.int32)
         lib, st = _lib.lib(), _lib.stream()

@@ -407,11 +407,12 @@ def _r_layout(node, g, pool, sinks):
 
 # --- sequence ops: embedding + fused GRU -------------------------------------------------------------
 
-def embedding(tokens: Tensor, table: Tensor, pool: Pool) -> Tensor:
-    """tokens [B, T] (float ids, as loaded) -> rows of table [V, E], time-major [T*B, E] float32.
+def embedding(tokens: Tensor, table: Tensor, pool: Pool, dtype: int = F32) -> Tensor:
+    """tokens [B, T] (float ids, as loaded) -> rows of table [V, E], time-major [T*B, E] (float32, or bf16 when
+    the consumer is a bf16 tensor-core GEMM: the GRU input projection).
 
     Equals onehot(tokens) @ E exactly (a one-term float64 sum), the reference's embedding path
-    (tensor.py:299-317 + :213-229); range errors keep onehot's message."""
+    (tensor.py:299-317 + :213-229), rounded to the output dtype; range errors keep onehot's message."""
     from .tensor import check_index_values, device_index_check
 
     if tokens.rank != 2 or table.rank != 2:
@@ -423,8 +424,8 @@ def embedding(tokens: Tensor, table: Tensor, pool: Pool) -> Tensor:
         check_index_values(tokens.host_src, v, "onehot")
     else:
         device_index_check(Tensor((b * t,), tokens.buffer), v, "onehot")
-    out = empty_tensor(pool, (t * b, e), F32)
-    check(_lib.lib().nsk_embedding_fwd(table.ptr, tokens.ptr, b * t, e, v, t, F32, out.ptr, None, _lib.stream()))
+    out = empty_tensor(pool, (t * b, e), dtype)
+    check(_lib.lib().nsk_embedding_fwd(table.ptr, tokens.ptr, b * t, e, v, t, dtype, out.ptr, None, _lib.stream()))
     record("embedding", out, tokens, table, saved=(tokens,), attrs={"T": t, "V": v})
     return out
 
@@ -463,16 +464,34 @@ def gru(x: Tensor, w: Tensor, b: Tensor, u: Tensor, c: Tensor, steps: int, pool:
     bsz = tb // steps
     lib, st = _lib.lib(), _lib.stream()
     gx = empty_tensor(pool, (tb, h3), F32)
-    _gemm(x.ptr, 0, e, w.ptr, 0, e, tb, h3, e, gx.ptr, h3, dtype=F32, bias_ptr=b.ptr)
+    if x.dtype == BF16:  # bf16 tensor-core input projection (W through its bf16 shadow), fp32 out + b
+        _gemm(x.ptr, 0, e, w.bf16_ptr(), 0, e, tb, h3, e, gx.ptr, h3, dtype=BF16, bias_ptr=b.ptr)
+    else:
+        _gemm(x.ptr, 0, e, w.ptr, 0, e, tb, h3, e, gx.ptr, h3, dtype=F32, bias_ptr=b.ptr)
     hs = _internal_tensor(empty_tensor(pool, ((steps + 1) * bsz, h), F32))
     check(lib.nsk_fill_f32(hs.ptr, bsz * h, 0.0, st))
     gates = _internal_tensor(empty_tensor(pool, (tb, 4 * h), F32))
-    check(lib.nsk_gru_fwd(gx.ptr, u.ptr, c.ptr, steps, bsz, h, hs.ptr, gates.ptr, st))
+    tc = _gru_tc(bsz, h)
+    if tc:  # tensor-core recurrence: one cluster, U resident as bf16 (gru_tc.cu)
+        ws = GRU_WS.get(lib.nsk_gru_tc_workspace(bsz, h))
+        check(lib.nsk_gru_fwd_tc(gx.ptr, u.bf16_ptr(), c.ptr, steps, bsz, h, hs.ptr, gates.ptr, ws.ptr, ws.nbytes,
+                                 st))
+    else:  # shapes the cluster kernel does not tile: fp32 cooperative kernel (gru.cu)
+        check(lib.nsk_gru_fwd(gx.ptr, u.ptr, c.ptr, steps, bsz, h, hs.ptr, gates.ptr, st))
     release_tensor(pool, gx)
     out = empty_tensor(pool, (bsz, h), F32)
     check(lib.nsk_memcpy_d2d(out.ptr, hs.ptr + 4 * steps * bsz * h, 4 * bsz * h, st))
-    record("gru", out, x, w, b, u, c, saved=(x, hs, gates, w, u), attrs={"T": steps, "B": bsz, "H": h, "E": e})
+    record("gru", out, x, w, b, u, c, saved=(x, hs, gates, w, u),
+           attrs={"T": steps, "B": bsz, "H": h, "E": e, "tc": tc})
     return out
+
+
+def _gru_tc(bsz: int, h: int) -> bool:
+    """The tcgen05 cluster recurrence covers 1 <= B <= 64, H in 128..512 (H % 64 == 0); NSK_GRU_TC=0 forces the
+    fp32 cooperative kernel (A/B and precision studies)."""
+    import os
+
+    return os.environ.get("NSK_GRU_TC", "1") != "0" and bool(_lib.lib().nsk_gru_tc_supported(bsz, h))
 
 
 @rule("gru")
@@ -489,9 +508,14 @@ def _r_gru(node, g, pool, sinks):
     dgx = empty_tensor(pool, (TB, H3), F32)
     dgh = empty_tensor(pool, (TB, H3), F32)
     dh0 = empty_tensor(pool, (B, H), F32)
-    ws = GRU_WS.get(lib.nsk_gru_bwd_workspace(T, B, H))
-    check(lib.nsk_gru_bwd(dhs.ptr, u.ptr, hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr, ws.nbytes,
-                          st))
+    if node.attrs.get("tc"):
+        ws = GRU_WS.get(lib.nsk_gru_tc_workspace(B, H))
+        check(lib.nsk_gru_bwd_tc(dhs.ptr, u.bf16_ptr(), hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr,
+                                 ws.nbytes, st))
+    else:
+        ws = GRU_WS.get(lib.nsk_gru_bwd_workspace(T, B, H))
+        check(lib.nsk_gru_bwd(dhs.ptr, u.ptr, hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr,
+                              ws.nbytes, st))
     release_tensor(pool, dhs)
     release_tensor(pool, dh0)
     outs = [None] * 5
@@ -506,8 +530,9 @@ def _r_gru(node, g, pool, sinks):
     hprev = Tensor((TB, H), Buffer(TB * H, F32, base=hs.buffer, offset=0))
     with _Operands(pool, BF16, dgx, dgh, x, w, hprev) as (pgx, pgh, px, pw, ph):
         if node.inputs[0].requires_grad:
-            dx = empty_tensor(pool, (TB, E), F32)
-            _gemm(pgx, 0, H3, pw, 1, E, TB, E, H3, dx.ptr, E, dtype=BF16)  # dx = dgx . W
+            xdt = node.inputs[0].tensor.dtype  # the gradient takes the input's dtype
+            dx = empty_tensor(pool, (TB, E), xdt)
+            _gemm(pgx, 0, H3, pw, 1, E, TB, E, H3, dx.ptr, E, dtype=BF16, out_f32=xdt == F32)  # dx = dgx . W
             outs[0] = dx
         if node.inputs[1].requires_grad:
             ptr, beta, outs[1] = target(1, (H3, E))

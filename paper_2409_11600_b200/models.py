@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import numpy as np
 
+from ._lib import BF16
 from .side import SIDE
 from . import autodiff, layers, nn
 from .runtime import Session
@@ -268,7 +269,7 @@ class GRUClassifier:
     def forward(self, tokens: Tensor) -> Tensor:
         pool, push = self.s.pool, self.s.push_named
         steps = tokens.shape[1]
-        x = layers.embedding(tokens, self.table, pool)
+        x = layers.embedding(tokens, self.table, pool, dtype=BF16)  # feeds the bf16 input projection
         push("gru.x", x)
         h = layers.gru(x, self.w, self.b, self.u, self.c, steps, pool)
         push("gru.h", h)
