@@ -228,6 +228,8 @@ int nsk_gru_bwd(const float* dhs, const float* U, const float* hs, const float* 
  * `ws` (nsk_gru_tc_workspace bytes), one tcgen05.mma chain per step, fp32 state and gate math. Same outputs as
  * nsk_gru_fwd / nsk_gru_bwd. Shapes: 1 <= B <= 64, H in 128..512 with H % 64 == 0 (nsk_gru_tc_supported). */
 int nsk_gru_tc_supported(int B, int H);
+/* diagnostics: 16 globaltimer stamps per (CTA, step) of the last forward launched with NSK_GRU_TRACE=1 */
+int nsk_gru_trace(long long* out, int steps);
 uint64_t nsk_gru_tc_workspace(int B, int H);
 int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, float* gates,
                    void* ws, uint64_t ws_bytes, void* stream);

@@ -110,6 +110,7 @@ SIGNATURES = {
     "nsk_gru_bwd": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
     "nsk_gru_bwd_workspace": (u64, [i32, i32, i32]),
     "nsk_gru_tc_supported": (i32, [i32, i32]),
+    "nsk_gru_trace": (i32, [vp, i32]),
     "nsk_gru_tc_workspace": (u64, [i32, i32]),
     "nsk_gru_fwd_tc": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp, u64, vp]),
     "nsk_gru_bwd_tc": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),

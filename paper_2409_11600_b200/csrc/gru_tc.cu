@@ -43,10 +43,16 @@ namespace {
 constexpr int kUC = 32;         // hidden units per CTA
 constexpr int kThreads = 256;   // 8 warps: 0,1,4,5 epilogue | 2 TMA | 3 MMA + TMEM | 6,7 idle
 constexpr int kMaxB = 64;       // batch rows (A operand rows that are read back)
+constexpr int kDP = 100;        // row pitch (floats) of the forward's accumulator tile: conflict-free float4 rows
+long long* g_trace = nullptr;   // NSK_GRU_TRACE: per-step timestamps of the forward (diagnostics)
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// split cluster barrier: the arrive publishes (release) what the peers need, work that only this CTA needs runs
+// between arrive and wait, off the critical path
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -69,10 +75,29 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* f) {
   for (int i = 0; i < 16; ++i) f[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float sigm(float x) {  // the reference's stable sigmoid (tensor.py:237-244)
-  if (x >= 0.f) return 1.f / (1.f + expf(-x));
-  const float e = expf(x);
-  return e / (1.f + e);
+// Gate nonlinearities, branch-free (MUFU ex2 + rcp, no IEEE slow paths, so the 8 units of a thread interleave):
+// the reference's stable sigmoid (tensor.py:237-244: exp of -|x| only, nothing overflows) and tanh from the same
+// e = exp(-2|x|). Relative error ~1e-6 (absolute ~1e-7 near 0), far below the bf16 rounding of the recurrent
+// product's operands.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sigm(float x) {
+  const float e = ex2_approx(-1.4426950408889634f * fabsf(x));
+  const float r = rcp_approx(1.f + e);
+  return x >= 0.f ? r : e * r;
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+  const float e = ex2_approx(-2.8853900817779268f * fabsf(x));
+  const float t = (1.f - e) * rcp_approx(1.f + e);
+  return copysignf(t, x);
 }
 
 __device__ __forceinline__ void ld16(const float* p, float* v) {
@@ -83,6 +108,22 @@ __device__ __forceinline__ void st16(float* p, const float* v) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) *(float4*)(p + 4 * i) = *(const float4*)(v + 4 * i);
 }
+__device__ __forceinline__ void ld8(const float* p, float* v) {
+  *(float4*)v = __ldcg((const float4*)p);
+  *(float4*)(v + 4) = __ldcg((const float4*)(p + 4));
+}
+__device__ __forceinline__ void st8(float* p, const float* v) {
+  *(float4*)p = *(const float4*)v;
+  *(float4*)(p + 4) = *(const float4*)(v + 4);
+}
+__device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float* v) {
+  uint4 a;
+  a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]); a.z = pack_bf16x2(v[4], v[5]);
+  a.w = pack_bf16x2(v[6], v[7]);
+  *(uint4*)p = a;
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ void st16_bf16(__nv_bfloat16* p, const float* v) {
   uint4 a, b;
   a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]); a.z = pack_bf16x2(v[4], v[5]);
@@ -104,19 +145,27 @@ struct FwdArgs {
   float* gates;      // [T][B][4][H]  (r, z, n, a)
   __nv_bfloat16* hx; // [2][B][H] exchange ring
   int T, B, H;
+  long long* trace;  // optional per-step timestamps of CTA 0 (NSK_GRU_TRACE), 8 per step
 };
+
+__device__ __forceinline__ long long gclock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                  const __grid_constant__ CUtensorMap tmH,
                                                                  const FwdArgs p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   const int H = p.H, B = p.B, T = p.T, H3 = 3 * H;
   const int NCH = H / 64;                  // K chunks
   uint8_t* us = smem;                      // NCH x 12 KB
   uint8_t* hsm = us + NCH * 12288;         // NCH x 8 KB (+8 KB slack)
-  uint64_t* bars = (uint64_t*)(hsm + NCH * 8192 + 8192);
+  float* dsm = (float*)(hsm + NCH * 8192 + 8192);   // [64][kDP] accumulator tile for the gate math
+  uint64_t* bars = (uint64_t*)(dsm + 64 * kDP);
   uint64_t* ufull = bars;                  // 1
   uint64_t* hfull = bars + 1;              // NCH (one per K chunk: the MMAs start on chunk 0 while the rest land)
   uint64_t* mdone = hfull + NCH;           // 1
@@ -142,19 +191,21 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // epilogue identity: warps 0,1,4,5 -> batch row b (TMEM lane), units [16 hf, 16 hf + 16) of this CTA
-  const bool epi = (warp & 2) == 0;
+  // TMEM readers: warps 0,1,4,5 (sub-partitions 0 and 1 hold accumulator rows = batch rows 0..63); they copy D to a
+  // shared-memory tile so that ALL eight warps (all four schedulers) share the gate math: thread -> batch row
+  // gb = tid / 4, units [8 gq, 8 gq + 8) of this CTA
+  const bool rd = (warp & 2) == 0;
   const int sp = warp & 1, hf = warp >> 2;
-  const int b = sp * 32 + lane;
-  const bool row_ok = epi && b < B;
-  const int ju = j0 + hf * 16;  // first global unit of this thread
-  float h[16], cr[16], cz[16], cn[16];
+  const int gb = threadIdx.x >> 2, gq = threadIdx.x & 3;
+  const bool row_ok = gb < B;
+  const int ju = j0 + gq * 8;  // first global unit of this thread
+  float h[8], cr[8], cz[8], cn[8];
   if (row_ok) {
-    ld16(p.hs + (size_t)b * H + ju, h);
-    ld16(p.c + ju, cr);
-    ld16(p.c + H + ju, cz);
-    ld16(p.c + 2 * H + ju, cn);
-    st16_bf16(p.hx + (size_t)b * H + ju, h);  // ring slot 0 = bf16(h0)
+    ld8(p.hs + (size_t)gb * H + ju, h);
+    ld8(p.c + ju, cr);
+    ld8(p.c + H + ju, cz);
+    ld8(p.c + 2 * H + ju, cn);
+    st8_bf16(p.hx + (size_t)gb * H + ju, h);  // ring slot 0 = bf16(h0)
   }
   if (warp == 2 && elect_one()) {  // U rows of this CTA: 3 gates x NCH chunks of {64 k, 32 rows}
     mbar_expect_tx(ufull, (uint32_t)(NCH * 12288));
@@ -164,25 +215,38 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   fence_proxy_async_global();
 
   const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
+  float gr[8], gz[8], gn[8];
+  if (row_ok) {  // step 0's input projections
+    const float* g3 = p.gx + (size_t)gb * H3 + ju;
+    ld8(g3, gr);
+    ld8(g3 + H, gz);
+    ld8(g3 + 2 * H, gn);
+  }
+  tc_fence_before();
+  cluster_arrive();  // h_0 published
   for (int t = 0; t < T; ++t) {
-    // h_t (ring slot t & 1) is complete in global memory once every CTA of the cluster has passed this point
-    tc_fence_before();
-    cluster_sync_all();
+    // h_t (ring slot t & 1) is complete in global memory once every CTA of the cluster has arrived
+    cluster_wait();
     tc_fence_after();
     fence_proxy_async_global();
-    if (warp == 2) {
-      if (elect_one()) {
-        for (int c = 0; c < NCH; ++c) {
-          mbar_expect_tx(&hfull[c], (uint32_t)(B * 128));
-          tma_load_2d(&tmH, &hfull[c], hsm + c * 8192, c * 64, (t & 1) * B);
-        }
+    long long* tr = p.trace ? p.trace + ((size_t)q * T + t) * 16 : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = gclock();
+    if ((warp & 2) && lane == 0) {
+      // four issuing threads (warps 2, 3, 6, 7): a single thread sustains about one box per L2 round trip
+      const int w4 = (warp & 1) | ((warp >> 1) & 2);
+      for (int c = w4; c < NCH; c += 4) {
+        mbar_expect_tx(&hfull[c], (uint32_t)(B * 128));
+        tma_load_2d(&tmH, &hfull[c], hsm + c * 8192, c * 64, (t & 1) * B);
       }
-      __syncwarp();
+    }
+    __syncwarp();
+    if (warp == 2) {
     } else if (warp == 3) {
       if (t == 0) mbar_wait(ufull, 0);
       const uint32_t sh = smem_u32(hsm), su = smem_u32(us);
       for (int c = 0; c < NCH; ++c) {
         mbar_wait(&hfull[c], t & 1);
+        if (tr && lane == 0 && (c == 0 || c == NCH - 1)) tr[c == 0 ? 1 : 2] = gclock();
         tc_fence_after();
         const uint64_t ad = sdesc_sw128(sh + c * 8192, 16, 1024);
         const uint64_t bd = sdesc_sw128(su + c * 12288, 16, 1024);
@@ -196,45 +260,68 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
       }
       if (elect_one()) umma_commit(mdone);
       __syncwarp();
-    } else if (epi) {
-      float gr[16], gz[16], gn[16];
-      if (row_ok) {  // independent of the MMA: in flight while it runs
-        const float* g3 = p.gx + ((size_t)t * B + b) * H3 + ju;
-        ld16(g3, gr);
-        ld16(g3 + H, gz);
-        ld16(g3 + 2 * H, gn);
-      }
-      mbar_wait_backoff(mdone, t & 1);
-      tc_fence_after();
-      float dr[16], dz[16], dn[16];
+    }
+    // ---- epilogue: all warps ----
+    mbar_wait_backoff(mdone, t & 1);
+    if (tr && threadIdx.x == 0) tr[3] = gclock();
+    tc_fence_after();
+    if (rd) {  // D row (32 sp + lane), columns [16 hf, +16) of each gate -> dsm[row][g*32 + col]
+      float d[16];
       const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16) + hf * 16;
-      tmem_ld16(ta, dr);
-      tmem_ld16(ta + 32, dz);
-      tmem_ld16(ta + 64, dn);
-      tmem_ld_wait();
-      if (row_ok) {
-        float r[16], z[16], n[16], a[16];
+      float* drow = dsm + (sp * 32 + lane) * kDP + hf * 16;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          r[u] = sigm(gr[u] + dr[u] + cr[u]);
-          z[u] = sigm(gz[u] + dz[u] + cz[u]);
-          a[u] = dn[u] + cn[u];
-          n[u] = tanhf(gn[u] + r[u] * a[u]);
-          h[u] = n[u] - z[u] * n[u] + z[u] * h[u];
-        }
-        st16(p.hs + ((size_t)(t + 1) * B + b) * H + ju, h);
-        float* gs = p.gates + ((size_t)t * B + b) * 4 * H + ju;
-        st16(gs, r);
-        st16(gs + H, z);
-        st16(gs + 2 * H, n);
-        st16(gs + 3 * H, a);
-        st16_bf16(p.hx + ((size_t)((t + 1) & 1) * B + b) * H + ju, h);
+      for (int g = 0; g < 3; ++g) {
+        tmem_ld16(ta + g * 32, d);
+        tmem_ld_wait();
+        st16(drow + g * 32, d);
       }
-      fence_proxy_async_global();  // h_{t+1} is read by peers' TMA (async proxy) after the barrier
+    }
+    tc_fence_before();
+    named_sync(1, kThreads);
+    if (tr && threadIdx.x == 0) tr[5] = gclock();
+    float dr[8], dz[8], dn[8];
+    if (row_ok) {
+      const float* drow = dsm + gb * kDP + gq * 8;
+      *(float4*)dr = *(const float4*)drow;
+      *(float4*)(dr + 4) = *(const float4*)(drow + 4);
+      *(float4*)dz = *(const float4*)(drow + 32);
+      *(float4*)(dz + 4) = *(const float4*)(drow + 36);
+      *(float4*)dn = *(const float4*)(drow + 64);
+      *(float4*)(dn + 4) = *(const float4*)(drow + 68);
+      if (tr && threadIdx.x == 0) tr[8] = gclock() + (dr[0] + dz[7] + dn[3] == 12345.f);
+      if (tr && threadIdx.x == 0) tr[9] = gclock() + (gr[0] + gz[7] + gn[3] == 12345.f);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        dr[u] = sigm(gr[u] + dr[u] + cr[u]);            // r
+        dz[u] = sigm(gz[u] + dz[u] + cz[u]);            // z
+        dn[u] = dn[u] + cn[u];                          // a
+        gn[u] = tanh_fast(gn[u] + dr[u] * dn[u]);       // n
+        h[u] = gn[u] - dz[u] * gn[u] + dz[u] * h[u];
+      }
+      if (tr && threadIdx.x == 0) tr[6] = gclock();
+      st8_bf16(p.hx + ((size_t)((t + 1) & 1) * B + gb) * H + ju, h);
+    }
+    fence_proxy_async_global();  // h_{t+1} is read by peers' TMA (async proxy) after the barrier
+    if (tr && threadIdx.x == 0) tr[7] = gclock();
+    tc_fence_before();
+    cluster_arrive();            // publish h_{t+1}; what follows is needed only by backward
+    if (tr && threadIdx.x == 0) tr[4] = gclock();
+    if (row_ok) {
+      st8(p.hs + ((size_t)(t + 1) * B + gb) * H + ju, h);
+      float* gs = p.gates + ((size_t)t * B + gb) * 4 * H + ju;
+      st8(gs, dr);
+      st8(gs + H, dz);
+      st8(gs + 2 * H, gn);
+      st8(gs + 3 * H, dn);
+      if (t + 1 < T) {  // next step's input projections, in flight across the barrier
+        const float* g3 = p.gx + ((size_t)(t + 1) * B + gb) * H3 + ju;
+        ld8(g3, gr);
+        ld8(g3 + H, gz);
+        ld8(g3 + 2 * H, gn);
+      }
     }
   }
-  tc_fence_before();
-  cluster_sync_all();
+  cluster_wait();
   if (warp == 3) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
@@ -260,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
                                                                  const BwdArgs p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, RG = p.RG, CG = p.CG;
   const int CL = RG * CG;
   const int NC = H / CG;            // column-group width (MMA N)
@@ -305,82 +392,91 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
           tma_load_2d(&tmU, ufull, ub + nb * KR * 128 + (jj * 3 + g) * kUC * 128, gj * NC + nb * 64,
                       g * H + jj * NC + gi * kUC);
   }
+  // phase A runs on all eight warps: thread -> batch row gb = tid / 4, units [8 gq, 8 gq + 8) of this CTA;
+  // phase B's TMEM readers are warps 0,1,4,5 (accumulator rows = batch rows live in sub-partitions 0 and 1)
   const bool epi = (warp & 2) == 0;
   const int sp = warp & 1, hf = warp >> 2;
   const int b = sp * 32 + lane;
-  const bool row_ok = epi && b < B;
-  const int ju = j0 + hf * 16;   // first global unit of this thread (phase A)
-  const int uo = hf * 16;        // its offset inside the CTA's 32 units
-  float dhz[16];                 // dh_{t+1} * z_{t+1} carried to the next (earlier) step
+  const int gb = threadIdx.x >> 2, gq = threadIdx.x & 3;
+  const bool arow = gb < B;
+  const int ju = j0 + gq * 8;    // first global unit of this thread (phase A)
+  const int uo = gq * 8;         // its offset inside the CTA's 32 units
+  float dhz[8];                  // dh_{t+1} * z_{t+1} carried to the next (earlier) step
 #pragma unroll
-  for (int u = 0; u < 16; ++u) dhz[u] = 0.f;
+  for (int u = 0; u < 8; ++u) dhz[u] = 0.f;
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
   for (int t = T - 1; t >= 0; --t) {
     // ---- A: dh_t for own units, gate derivatives, dgh block ----
-    if (epi) {
-      if (row_ok) {
-        float dh[16], v[16];
-        ld16(p.dhs + ((size_t)t * B + b) * H + ju, dh);
-#pragma unroll
-        for (int u = 0; u < 16; ++u) dh[u] += dhz[u];
-        if (t < T - 1) {
-          const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + (size_t)b * kUC + uo;
-          for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
-            ld16(pp + (size_t)s * B * kUC, v);
-#pragma unroll
-            for (int u = 0; u < 16; ++u) dh[u] += v[u];
-          }
-        }
-        const float* gs = p.gates + ((size_t)t * B + b) * 4 * H + ju;
-        float r[16], z[16], n[16], a[16], hp[16];
-        ld16(gs, r);
-        ld16(gs + H, z);
-        ld16(gs + 2 * H, n);
-        ld16(gs + 3 * H, a);
-        ld16(p.hs + ((size_t)t * B + b) * H + ju, hp);
-        float drp[16], dzp[16], dnp[16], dnr[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const float dn = dh[u] * (1.f - z[u]);
-          const float dz = dh[u] * (hp[u] - n[u]);
-          dnp[u] = dn * (1.f - n[u] * n[u]);
-          drp[u] = dnp[u] * a[u] * r[u] * (1.f - r[u]);
-          dzp[u] = dz * z[u] * (1.f - z[u]);
-          dnr[u] = dnp[u] * r[u];
-          dhz[u] = dh[u] * z[u];
-        }
-        float* gxo = p.dgx + ((size_t)t * B + b) * H3 + ju;
-        float* gho = p.dgh + ((size_t)t * B + b) * H3 + ju;
-        st16(gxo, drp);
-        st16(gxo + H, dzp);
-        st16(gxo + 2 * H, dnp);
-        st16(gho, drp);
-        st16(gho + H, dzp);
-        st16(gho + 2 * H, dnr);
-        if (t == 0) {
-          // dh0 = dh_0 * z_0 + (dgh_0 U)[own units], the partials of step 0 are added after the last barrier
-          st16(p.dh0 + (size_t)b * H + ju, dhz);
-        }
-        __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + b) * KR + gj * 3 * kUC + uo;
-        st16_bf16(ge, drp);
-        st16_bf16(ge + kUC, dzp);
-        st16_bf16(ge + 2 * kUC, dnr);
-      }
-      fence_proxy_async_global();
+    if (t < T - 1) {
+      cluster_wait();  // partial products of step t+1 visible
+      tc_fence_after();
     }
+    float drp[8], dzp[8], dnp[8], dnr[8];
+    if (arow) {
+      float dh[8], v[8];
+      ld8(p.dhs + ((size_t)t * B + gb) * H + ju, dh);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) dh[u] += dhz[u];
+      if (t < T - 1) {
+        const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + (size_t)gb * kUC + uo;
+        for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
+          ld8(pp + (size_t)s * B * kUC, v);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) dh[u] += v[u];
+        }
+      }
+      const float* gs = p.gates + ((size_t)t * B + gb) * 4 * H + ju;
+      float r[8], z[8], n[8], a[8], hp[8];
+      ld8(gs, r);
+      ld8(gs + H, z);
+      ld8(gs + 2 * H, n);
+      ld8(gs + 3 * H, a);
+      ld8(p.hs + ((size_t)t * B + gb) * H + ju, hp);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const float dn = dh[u] * (1.f - z[u]);
+        const float dz = dh[u] * (hp[u] - n[u]);
+        dnp[u] = dn * (1.f - n[u] * n[u]);
+        drp[u] = dnp[u] * a[u] * r[u] * (1.f - r[u]);
+        dzp[u] = dz * z[u] * (1.f - z[u]);
+        dnr[u] = dnp[u] * r[u];
+        dhz[u] = dh[u] * z[u];
+      }
+      __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + gb) * KR + gj * 3 * kUC + uo;
+      st8_bf16(ge, drp);
+      st8_bf16(ge + kUC, dzp);
+      st8_bf16(ge + 2 * kUC, dnr);
+    }
+    fence_proxy_async_global();
     tc_fence_before();
-    cluster_sync_all();  // every dgh block of step t is in the ring
+    cluster_arrive();  // publish this step's dgh block; the fp32 copies below are only read after the kernel
+    if (arow) {
+      float* gxo = p.dgx + ((size_t)t * B + gb) * H3 + ju;
+      float* gho = p.dgh + ((size_t)t * B + gb) * H3 + ju;
+      st8(gxo, drp);
+      st8(gxo + H, dzp);
+      st8(gxo + 2 * H, dnp);
+      st8(gho, drp);
+      st8(gho + H, dzp);
+      st8(gho + 2 * H, dnr);
+      if (t == 0) {
+        // dh0 = dh_0 * z_0 + (dgh_0 U)[own units], the partials of step 0 are added after the last barrier
+        st8(p.dh0 + (size_t)gb * H + ju, dhz);
+      }
+    }
+    cluster_wait();  // every dgh block of step t is in the ring
     tc_fence_after();
     // ---- B: P = dgh(row group) . U(row group rows, column group cols), slices to the column group ----
     fence_proxy_async_global();
-    if (warp == 2) {
-      if (elect_one()) {
-        for (int c = 0; c < NKC; ++c) {
-          mbar_expect_tx(&gfull[c], (uint32_t)(B * 128));
-          tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B);
-        }
+    if ((warp & 2) && lane == 0) {  // four issuing threads (warps 2, 3, 6, 7)
+      const int w4 = (warp & 1) | ((warp >> 1) & 2);
+      for (int c = w4; c < NKC; c += 4) {
+        mbar_expect_tx(&gfull[c], (uint32_t)(B * 128));
+        tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B);
       }
-      __syncwarp();
+    }
+    __syncwarp();
+    if (warp == 2) {
     } else if (warp == 3) {
       if (t == T - 1) mbar_wait(ufull, 0);
       const uint32_t sg = smem_u32(gsm), su = smem_u32(ub);
@@ -410,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
         tmem_ld16(ta + s * kUC, v0);
         tmem_ld16(ta + s * kUC + 16, v1);
         tmem_ld_wait();
-        if (row_ok) {
+        if (b < B) {
           const int dest = s * CG + gj;
           float* po = p.pex + ((size_t)((t & 1) * CL + dest) * RG + gi) * B * kUC + (size_t)b * kUC;
           st16(po, v0);
@@ -419,20 +515,21 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
       }
     }
     tc_fence_before();
-    cluster_sync_all();  // partials of step t visible (read in A of step t-1)
-    tc_fence_after();
+    cluster_arrive();  // partials of step t published (read in A of step t-1)
   }
+  cluster_wait();
+  tc_fence_after();
   // dh0 += the step-0 partial products of this CTA's units
-  if (row_ok) {
-    float dh[16], v[16];
-    ld16(p.dh0 + (size_t)b * H + ju, dh);
-    const float* pp = p.pex + ((size_t)q * RG) * B * kUC + (size_t)b * kUC + uo;  // slot (0 & 1) = 0
+  if (arow) {
+    float dh[8], v[8];
+    ld8(p.dh0 + (size_t)gb * H + ju, dh);
+    const float* pp = p.pex + ((size_t)q * RG) * B * kUC + (size_t)gb * kUC + uo;  // slot (0 & 1) = 0
     for (int s = 0; s < RG; ++s) {
-      ld16(pp + (size_t)s * B * kUC, v);
+      ld8(pp + (size_t)s * B * kUC, v);
 #pragma unroll
-      for (int u = 0; u < 16; ++u) dh[u] += v[u];
+      for (int u = 0; u < 8; ++u) dh[u] += v[u];
     }
-    st16(p.dh0 + (size_t)b * H + ju, dh);
+    st8(p.dh0 + (size_t)gb * H + ju, dh);
   }
   if (warp == 3) {
     tc_fence_after();
@@ -457,7 +554,7 @@ int bwd_groups(int H, int* rg, int* cg) {
   return 1;
 }
 
-size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * (12288 + 8192) + 8192 + 256; }
+size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * (12288 + 8192) + 8192 + 64 * kDP * 4 + 256; }
 size_t bwd_smem(int H, int rg, int cg) {
   const int NB = H / cg / 64, KR = 3 * kUC * cg;
   return 1024 + (size_t)NB * KR * 128 + (size_t)(KR / 64) * 8192 + 8192 + 256;
@@ -496,6 +593,14 @@ int tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 
 extern "C" {
 
+// diagnostics: copy the forward trace (16 globaltimer stamps per CTA and step) of the last traced launch
+int nsk_gru_trace(long long* out, int steps) {
+  if (!g_trace) return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: run with NSK_GRU_TRACE=1");
+  NSK_CUDA(cudaDeviceSynchronize());
+  NSK_CUDA(cudaMemcpy(out, g_trace, (size_t)16 * steps * sizeof(long long), cudaMemcpyDeviceToHost));  // steps: T x CTAs
+  return NSK_OK;
+}
+
 int nsk_gru_tc_supported(int B, int H) {
   int rg, cg;
   return B >= 1 && B <= kMaxB && H % 64 == 0 && H >= 128 && H <= 16 * kUC && bwd_groups(H, &rg, &cg);
@@ -521,7 +626,8 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
   if (rc) return rc;
   __nv_bfloat16* hx = (__nv_bfloat16*)ws;
   if ((rc = tmap_2d_bf16(&tmH, hx, (uint64_t)2 * B, (uint64_t)H, (uint32_t)B))) return rc;
-  FwdArgs a{gx, c, hs, gates, hx, T, B, H};
+  if (getenv("NSK_GRU_TRACE") && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
+  FwdArgs a{gx, c, hs, gates, hx, T, B, H, T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
   return launch_cluster((const void*)gru_fwd_tc_kernel, H / kUC, fwd_smem(H), args, (cudaStream_t)stream);
 }

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
   using T = KT<ESZ>;
   constexpr bool kGate = Launch<S>::kGate;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint64_t* full = (uint64_t*)(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(256, 1) wgrad_rr64_kernel(const __grid_constan
                                                             const WgrrProb p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint64_t* full = (uint64_t*)(smem + kWgrrStages * kWgrrStage);
   uint64_t* empty = full + kWgrrStages;
   uint64_t* tfull = empty + kWgrrStages;
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(256, 1) wgrad_rr128_kernel(const __grid_consta
                                                              const WgrrProb p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint64_t* full = (uint64_t*)(smem + kWg128Stages * kWg128Stage);
   uint64_t* empty = full + kWg128Stages;
   uint64_t* tfull = empty + kWg128Stages;
