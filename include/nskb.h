@@ -231,10 +231,13 @@ int nsk_gru_tc_supported(int B, int H);
 /* diagnostics: 16 globaltimer stamps per (CTA, step) of the last forward launched with NSK_GRU_TRACE=1 */
 int nsk_gru_trace(long long* out, int steps);
 uint64_t nsk_gru_tc_workspace(int B, int H);
-int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, float* gates,
-                   void* ws, uint64_t ws_bytes, void* stream);
+int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, void* hsb,
+                   float* gates, void* ws, uint64_t ws_bytes, void* stream);
+/* hsb [T+1, B, H] bf16 copy of hs; the backward emits dgx / dgh as bf16 (the weight-gradient GEMM operands) and the
+ * bias gradients itself: db (+)= sum_{t,b} dgx, dc (+)= sum_{t,b} dgh (fp32, fixed order; beta 0 or 1). */
 int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const float* gates, int T, int B, int H,
-                   float* dgx, float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream);
+                   void* dgx, void* dgh, float* dh0, float* db, float beta_b, float* dc, float beta_c, void* ws,
+                   uint64_t ws_bytes, void* stream);
 
 /* ---- communication (comm.cu): NCCL over NVLink / NVSwitch ---- */
 int nsk_comm_unique_id(uint8_t* out128);

@@ -112,8 +112,8 @@ SIGNATURES = {
     "nsk_gru_tc_supported": (i32, [i32, i32]),
     "nsk_gru_trace": (i32, [vp, i32]),
     "nsk_gru_tc_workspace": (u64, [i32, i32]),
-    "nsk_gru_fwd_tc": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp, u64, vp]),
-    "nsk_gru_bwd_tc": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
+    "nsk_gru_fwd_tc": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, u64, vp]),
+    "nsk_gru_bwd_tc": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, f32, vp, f32, vp, u64, vp]),
     "nsk_comm_unique_id": (i32, [vp]),
     "nsk_comm_init": (i32, [i32, i32, vp, C.POINTER(vp)]),
     "nsk_comm_destroy": (i32, [vp]),

@@ -143,6 +143,7 @@ struct FwdArgs {
   const float* c;    // [3H]
   float* hs;         // [T+1][B][H], hs[0] = h0 on entry
   float* gates;      // [T][B][4][H]  (r, z, n, a)
+  __nv_bfloat16* hsb;  // [T+1][B][H] bf16 copy of hs (operand of the recurrent weight gradient dU = dgh^T h)
   __nv_bfloat16* hx; // [2][B][H] exchange ring
   int T, B, H;
   long long* trace;  // optional per-step timestamps of CTA 0 (NSK_GRU_TRACE), 8 per step
@@ -154,6 +155,32 @@ __device__ __forceinline__ long long gclock() {
   return t;
 }
 
+// SW64 K-major shared-memory descriptor (sm_100 layout type 4): rows of 64 B (32 bf16), 8-row groups 512 B apart
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;             // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;    // SBO
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)4 << 61;
+  return d;
+}
+
+// one box of the h ring, multicast to every CTA of the cluster (same smem offset / mbarrier in each)
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+// Per step: every CTA writes its 32-unit slice of h_{t+1} (bf16) to the global ring and multicasts that slice --
+// one 64-row x 64-byte TMA box -- into all CTAs' h buffers, signalling their per-slice mbarriers; the MMA on
+// slice c starts as soon as it lands. The only cluster-wide barrier is split: each CTA arrives once its MMA has
+// finished reading h_t and waits right before its multicast overwrites the peers' h buffers, so its latency hides
+// behind the gate math.
 __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                  const __grid_constant__ CUtensorMap tmH,
                                                                  const FwdArgs p) {
@@ -161,26 +188,30 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   const int H = p.H, B = p.B, T = p.T, H3 = 3 * H;
-  const int NCH = H / 64;                  // K chunks
-  uint8_t* us = smem;                      // NCH x 12 KB
-  uint8_t* hsm = us + NCH * 12288;         // NCH x 8 KB (+8 KB slack)
-  float* dsm = (float*)(hsm + NCH * 8192 + 8192);   // [64][kDP] accumulator tile for the gate math
+  const int NCH = H / 64;                  // 64-wide K chunks of U
+  const int NS = H / kUC;                  // 32-wide h slices = CTAs of the cluster
+  uint8_t* us = smem;                      // NCH x 12 KB (SW128, B operand)
+  uint8_t* hsm = us + NCH * 12288;         // NS x 4 KB (SW64, A operand) + 4 KB slack (rows 64..127 of the last)
+  float* dsm = (float*)(hsm + NS * 4096 + 4096);   // [64][kDP] accumulator tile for the gate math
   uint64_t* bars = (uint64_t*)(dsm + 64 * kDP);
   uint64_t* ufull = bars;                  // 1
-  uint64_t* hfull = bars + 1;              // NCH (one per K chunk: the MMAs start on chunk 0 while the rest land)
-  uint64_t* mdone = hfull + NCH;           // 1
+  uint64_t* hfull = bars + 1;              // NS: one per slice (= per producing CTA)
+  uint64_t* mdone = hfull + NS;            // 1
   uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int q = (int)cluster_rank();
   const int j0 = q * kUC;
+  const uint16_t all = (uint16_t)((1u << NS) - 1u);
+  const uint32_t slice_bytes = (uint32_t)(B * 64);
   if (threadIdx.x == 0) {
     mbar_init(ufull, 1);
-    for (int c = 0; c < NCH; ++c) mbar_init(&hfull[c], 1);
+    for (int c = 0; c < NS; ++c) mbar_init(&hfull[c], 1);
     mbar_init(mdone, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmU);
     tma_prefetch_desc(&tmH);
+    for (int c = 0; c < NS; ++c) mbar_expect_tx(&hfull[c], slice_bytes);  // phase 0
   }
   if (warp == 3) {
     tmem_alloc(tmem_slot, 128);
@@ -199,13 +230,18 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   const int gb = threadIdx.x >> 2, gq = threadIdx.x & 3;
   const bool row_ok = gb < B;
   const int ju = j0 + gq * 8;  // first global unit of this thread
-  float h[8], cr[8], cz[8], cn[8];
+  float h[8], cr[8], cz[8], cn[8], gr[8], gz[8], gn[8];
   if (row_ok) {
     ld8(p.hs + (size_t)gb * H + ju, h);
     ld8(p.c + ju, cr);
     ld8(p.c + H + ju, cz);
     ld8(p.c + 2 * H + ju, cn);
     st8_bf16(p.hx + (size_t)gb * H + ju, h);  // ring slot 0 = bf16(h0)
+    st8_bf16(p.hsb + (size_t)gb * H + ju, h);
+    const float* g3 = p.gx + (size_t)gb * H3 + ju;  // step 0's input projections
+    ld8(g3, gr);
+    ld8(g3 + H, gz);
+    ld8(g3 + 2 * H, gn);
   }
   if (warp == 2 && elect_one()) {  // U rows of this CTA: 3 gates x NCH chunks of {64 k, 32 rows}
     mbar_expect_tx(ufull, (uint32_t)(NCH * 12288));
@@ -213,48 +249,26 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
       for (int g = 0; g < 3; ++g) tma_load_2d(&tmU, ufull, us + c * 12288 + g * 4096, c * 64, g * H + j0);
   }
   fence_proxy_async_global();
+  tc_fence_before();
+  cluster_sync_all();  // every CTA's mbarriers are initialised and its h0 slice is in the ring
+  if (threadIdx.x == 0) tma_load_2d_mc(&tmH, &hfull[q], hsm + q * 4096, j0, 0, all);
 
   const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
-  float gr[8], gz[8], gn[8];
-  if (row_ok) {  // step 0's input projections
-    const float* g3 = p.gx + (size_t)gb * H3 + ju;
-    ld8(g3, gr);
-    ld8(g3 + H, gz);
-    ld8(g3 + 2 * H, gn);
-  }
-  tc_fence_before();
-  cluster_arrive();  // h_0 published
   for (int t = 0; t < T; ++t) {
-    // h_t (ring slot t & 1) is complete in global memory once every CTA of the cluster has arrived
-    cluster_wait();
-    tc_fence_after();
-    fence_proxy_async_global();
     long long* tr = p.trace ? p.trace + ((size_t)q * T + t) * 16 : nullptr;
-    if (tr && threadIdx.x == 0) tr[0] = gclock();
-    if ((warp & 2) && lane == 0) {
-      // four issuing threads (warps 2, 3, 6, 7): a single thread sustains about one box per L2 round trip
-      const int w4 = (warp & 1) | ((warp >> 1) & 2);
-      for (int c = w4; c < NCH; c += 4) {
-        mbar_expect_tx(&hfull[c], (uint32_t)(B * 128));
-        tma_load_2d(&tmH, &hfull[c], hsm + c * 8192, c * 64, (t & 1) * B);
-      }
-    }
-    __syncwarp();
-    if (warp == 2) {
-    } else if (warp == 3) {
+    if (warp == 3) {
       if (t == 0) mbar_wait(ufull, 0);
       const uint32_t sh = smem_u32(hsm), su = smem_u32(us);
-      for (int c = 0; c < NCH; ++c) {
+      for (int c = 0; c < NS; ++c) {
         mbar_wait(&hfull[c], t & 1);
-        if (tr && lane == 0 && (c == 0 || c == NCH - 1)) tr[c == 0 ? 1 : 2] = gclock();
+        if (tr && lane == 0 && (c == 0 || c == NS - 1)) tr[c == 0 ? 1 : 2] = gclock();
         tc_fence_after();
-        const uint64_t ad = sdesc_sw128(sh + c * 8192, 16, 1024);
-        const uint64_t bd = sdesc_sw128(su + c * 12288, 16, 1024);
+        const uint64_t ad = sdesc_sw64(sh + c * 4096);
+        // U chunk c/2, the 64-byte half (c & 1) of its 128-byte rows
+        const uint64_t bd = sdesc_sw128(su + (c >> 1) * 12288, 16, 1024) + (uint64_t)((c & 1) * 4);
         if (elect_one()) {
           umma_off<0, 0, false>(tmem, ad, bd, idesc, c > 0 ? 1u : 0u);
           umma_off<2, 2, false>(tmem, ad, bd, idesc, 1u);
-          umma_off<4, 4, false>(tmem, ad, bd, idesc, 1u);
-          umma_off<6, 6, false>(tmem, ad, bd, idesc, 1u);
         }
         __syncwarp();
       }
@@ -265,6 +279,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     mbar_wait_backoff(mdone, t & 1);
     if (tr && threadIdx.x == 0) tr[3] = gclock();
     tc_fence_after();
+    if (threadIdx.x == 0 && t + 1 < T)  // next phase of every slice barrier (this step's phases are complete)
+      for (int c = 0; c < NS; ++c) mbar_expect_tx(&hfull[c], slice_bytes);
     if (rd) {  // D row (32 sp + lane), columns [16 hf, +16) of each gate -> dsm[row][g*32 + col]
       float d[16];
       const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16) + hf * 16;
@@ -277,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
       }
     }
     tc_fence_before();
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // done reading this step's h buffer
     named_sync(1, kThreads);
     if (tr && threadIdx.x == 0) tr[5] = gclock();
     float dr[8], dz[8], dn[8];
@@ -288,8 +305,6 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
       *(float4*)(dz + 4) = *(const float4*)(drow + 36);
       *(float4*)dn = *(const float4*)(drow + 64);
       *(float4*)(dn + 4) = *(const float4*)(drow + 68);
-      if (tr && threadIdx.x == 0) tr[8] = gclock() + (dr[0] + dz[7] + dn[3] == 12345.f);
-      if (tr && threadIdx.x == 0) tr[9] = gclock() + (gr[0] + gz[7] + gn[3] == 12345.f);
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         dr[u] = sigm(gr[u] + dr[u] + cr[u]);            // r
@@ -299,29 +314,33 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
         h[u] = gn[u] - dz[u] * gn[u] + dz[u] * h[u];
       }
       if (tr && threadIdx.x == 0) tr[6] = gclock();
-      st8_bf16(p.hx + ((size_t)((t + 1) & 1) * B + gb) * H + ju, h);
+      if (t + 1 < T) st8_bf16(p.hx + ((size_t)((t + 1) & 1) * B + gb) * H + ju, h);
     }
-    fence_proxy_async_global();  // h_{t+1} is read by peers' TMA (async proxy) after the barrier
+    fence_proxy_async_global();  // this slice of h_{t+1} is read by this CTA's multicast (async proxy)
+    named_sync(1, kThreads);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA is done with h_t: buffers are free
     if (tr && threadIdx.x == 0) tr[7] = gclock();
-    tc_fence_before();
-    cluster_arrive();            // publish h_{t+1}; what follows is needed only by backward
-    if (tr && threadIdx.x == 0) tr[4] = gclock();
-    if (row_ok) {
+    if (threadIdx.x == 0 && t + 1 < T)
+      tma_load_2d_mc(&tmH, &hfull[q], hsm + q * 4096, j0, ((t + 1) & 1) * B, all);
+    if (row_ok) {  // needed only by backward: off the critical path
       st8(p.hs + ((size_t)(t + 1) * B + gb) * H + ju, h);
+      st8_bf16(p.hsb + ((size_t)(t + 1) * B + gb) * H + ju, h);
       float* gs = p.gates + ((size_t)t * B + gb) * 4 * H + ju;
       st8(gs, dr);
       st8(gs + H, dz);
       st8(gs + 2 * H, gn);
       st8(gs + 3 * H, dn);
-      if (t + 1 < T) {  // next step's input projections, in flight across the barrier
+      if (t + 1 < T) {  // next step's input projections
         const float* g3 = p.gx + ((size_t)(t + 1) * B + gb) * H3 + ju;
         ld8(g3, gr);
         ld8(g3 + H, gz);
         ld8(g3 + 2 * H, gn);
       }
     }
+    if (tr && threadIdx.x == 0) tr[4] = gclock();
   }
-  cluster_wait();
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while a peer's multicast may still target it
   if (warp == 3) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
@@ -334,9 +353,12 @@ struct BwdArgs {
   const float* dhs;    // [T][B][H] external gradient of each h_{t+1}
   const float* hs;     // [T+1][B][H]
   const float* gates;  // [T][B][4][H]
-  float* dgx;          // [T][B][3H]
-  float* dgh;          // [T][B][3H]
+  __nv_bfloat16* dgx;  // [T][B][3H] bf16: operand of dW = dgx^T x and dx = dgx W
+  __nv_bfloat16* dgh;  // [T][B][3H] bf16: operand of dU = dgh^T h
   float* dh0;          // [B][H]
+  float* db;           // [3H]  sum over (t, b) of dgx (fp32, fixed order), accumulated with beta_b
+  float* dc;           // [3H]  sum over (t, b) of dgh, accumulated with beta_c
+  float beta_b, beta_c;
   __nv_bfloat16* gex;  // [2][RG][B][KR] dgh exchange ring (bf16)
   float* pex;          // [2][CL][RG][B][32] partial-product ring
   int T, B, H, RG, CG;
@@ -402,8 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   const int ju = j0 + gq * 8;    // first global unit of this thread (phase A)
   const int uo = gq * 8;         // its offset inside the CTA's 32 units
   float dhz[8];                  // dh_{t+1} * z_{t+1} carried to the next (earlier) step
+  float cs[4][8];                // running column sums of dr', dz', dn', dn'*r (bias gradients db, dc)
 #pragma unroll
-  for (int u = 0; u < 8; ++u) dhz[u] = 0.f;
+  for (int u = 0; u < 8; ++u) {
+    dhz[u] = 0.f;
+    cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
+  }
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
   for (int t = T - 1; t >= 0; --t) {
     // ---- A: dh_t for own units, gate derivatives, dgh block ----
@@ -441,6 +467,10 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
         dzp[u] = dz * z[u] * (1.f - z[u]);
         dnr[u] = dnp[u] * r[u];
         dhz[u] = dh[u] * z[u];
+        cs[0][u] += drp[u];
+        cs[1][u] += dzp[u];
+        cs[2][u] += dnp[u];
+        cs[3][u] += dnr[u];
       }
       __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + gb) * KR + gj * 3 * kUC + uo;
       st8_bf16(ge, drp);
@@ -451,14 +481,14 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     tc_fence_before();
     cluster_arrive();  // publish this step's dgh block; the fp32 copies below are only read after the kernel
     if (arow) {
-      float* gxo = p.dgx + ((size_t)t * B + gb) * H3 + ju;
-      float* gho = p.dgh + ((size_t)t * B + gb) * H3 + ju;
-      st8(gxo, drp);
-      st8(gxo + H, dzp);
-      st8(gxo + 2 * H, dnp);
-      st8(gho, drp);
-      st8(gho + H, dzp);
-      st8(gho + 2 * H, dnr);
+      __nv_bfloat16* gxo = p.dgx + ((size_t)t * B + gb) * H3 + ju;
+      __nv_bfloat16* gho = p.dgh + ((size_t)t * B + gb) * H3 + ju;
+      st8_bf16(gxo, drp);
+      st8_bf16(gxo + H, dzp);
+      st8_bf16(gxo + 2 * H, dnp);
+      st8_bf16(gho, drp);
+      st8_bf16(gho + H, dzp);
+      st8_bf16(gho + 2 * H, dnr);
       if (t == 0) {
         // dh0 = dh_0 * z_0 + (dgh_0 U)[own units], the partials of step 0 are added after the last barrier
         st8(p.dh0 + (size_t)gb * H + ju, dhz);
@@ -531,6 +561,32 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     }
     st8(p.dh0 + (size_t)gb * H + ju, dh);
   }
+  // bias gradients: the running column sums of the 64 batch rows, added in row order (deterministic); the
+  // dgh block ring in shared memory is free now
+  float* red = (float*)gsm;  // [64 rows][4 sums][32 units]
+  if (arow) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st8(red + ((size_t)gb * 4 + k) * kUC + uo, cs[k]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 * kUC) {
+    const int k = threadIdx.x / kUC, u = threadIdx.x % kUC;
+    float acc = 0.f;
+    for (int r = 0; r < B; ++r) acc += red[((size_t)r * 4 + k) * kUC + u];
+    const int j = j0 + u;
+    if (k < 2) {  // r and z parts: dgx and dgh agree
+      float* o1 = p.db + k * H + j;
+      float* o2 = p.dc + k * H + j;
+      *o1 = acc + p.beta_b * *o1;
+      *o2 = acc + p.beta_c * *o2;
+    } else if (k == 2) {
+      float* o = p.db + 2 * H + j;
+      *o = acc + p.beta_b * *o;
+    } else {
+      float* o = p.dc + 2 * H + j;
+      *o = acc + p.beta_c * *o;
+    }
+  }
   if (warp == 3) {
     tc_fence_after();
     tmem_dealloc(tmem, NC <= 32 ? 32 : (NC <= 64 ? 64 : (NC <= 128 ? 128 : 256)));
@@ -554,7 +610,7 @@ int bwd_groups(int H, int* rg, int* cg) {
   return 1;
 }
 
-size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * (12288 + 8192) + 8192 + 64 * kDP * 4 + 256; }
+size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * 12288 + (size_t)(H / kUC) * 4096 + 4096 + 64 * kDP * 4 + 256; }
 size_t bwd_smem(int H, int rg, int cg) {
   const int NB = H / cg / 64, KR = 3 * kUC * cg;
   return 1024 + (size_t)NB * KR * 128 + (size_t)(KR / 64) * 8192 + 8192 + 256;
@@ -616,8 +672,8 @@ uint64_t nsk_gru_tc_workspace(int B, int H) {
   return ((hx + 255) / 256 + (gex + 255) / 256) * 256 + pex;
 }
 
-int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, float* gates,
-                   void* ws, uint64_t ws_bytes, void* stream) {
+int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, void* hsb,
+                   float* gates, void* ws, uint64_t ws_bytes, void* stream) {
   if (!nsk_gru_tc_supported(B, H) || T < 1)
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: needs 1 <= B <= 64 and H in 128..512, H % 64 == 0");
   if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
@@ -625,15 +681,23 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
   __nv_bfloat16* hx = (__nv_bfloat16*)ws;
-  if ((rc = tmap_2d_bf16(&tmH, hx, (uint64_t)2 * B, (uint64_t)H, (uint32_t)B))) return rc;
+  {  // h ring as 32-column (64-byte) boxes, 64B-swizzled: one box = one CTA's slice
+    const uint64_t dims[2] = {(uint64_t)H, (uint64_t)2 * B};
+    const uint64_t str[1] = {(uint64_t)H * 2};
+    const uint32_t box[2] = {(uint32_t)kUC, (uint32_t)B};
+    if ((rc = nsk::encode_tmap(&tmH, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hx, dims, str, box, nullptr,
+                               CU_TENSOR_MAP_SWIZZLE_64B)))
+      return rc;
+  }
   if (getenv("NSK_GRU_TRACE") && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
-  FwdArgs a{gx, c, hs, gates, hx, T, B, H, T <= 4096 ? g_trace : nullptr};
+  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
   return launch_cluster((const void*)gru_fwd_tc_kernel, H / kUC, fwd_smem(H), args, (cudaStream_t)stream);
 }
 
 int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const float* gates, int T, int B, int H,
-                   float* dgx, float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream) {
+                   void* dgx, void* dgh, float* dh0, float* db, float beta_b, float* dc, float beta_c, void* ws,
+                   uint64_t ws_bytes, void* stream) {
   if (!nsk_gru_tc_supported(B, H) || T < 1)
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: needs 1 <= B <= 64 and H in 128..512, H % 64 == 0");
   if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
@@ -648,7 +712,8 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
   if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)B))) return rc;
-  BwdArgs a{dhs, hs, gates, dgx, dgh, dh0, gex, pex, T, B, H, rg, cg};
+  BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
+            T, B, H, rg, cg};
   void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
   return launch_cluster((const void*)gru_bwd_tc_kernel, H / kUC, bwd_smem(H, rg, cg), args, (cudaStream_t)stream);
 }

@@ -472,17 +472,19 @@ def gru(x: Tensor, w: Tensor, b: Tensor, u: Tensor, c: Tensor, steps: int, pool:
     check(lib.nsk_fill_f32(hs.ptr, bsz * h, 0.0, st))
     gates = _internal_tensor(empty_tensor(pool, (tb, 4 * h), F32))
     tc = _gru_tc(bsz, h)
-    if tc:  # tensor-core recurrence: one cluster, U resident as bf16 (gru_tc.cu)
+    hsb = None
+    if tc:  # tensor-core recurrence: one cluster, U resident as bf16 (gru_tc.cu); also a bf16 copy of h for dU
+        hsb = _internal_tensor(empty_tensor(pool, ((steps + 1) * bsz, h), BF16))
         ws = GRU_WS.get(lib.nsk_gru_tc_workspace(bsz, h))
-        check(lib.nsk_gru_fwd_tc(gx.ptr, u.bf16_ptr(), c.ptr, steps, bsz, h, hs.ptr, gates.ptr, ws.ptr, ws.nbytes,
-                                 st))
+        check(lib.nsk_gru_fwd_tc(gx.ptr, u.bf16_ptr(), c.ptr, steps, bsz, h, hs.ptr, hsb.ptr, gates.ptr, ws.ptr,
+                                 ws.nbytes, st))
     else:  # shapes the cluster kernel does not tile: fp32 cooperative kernel (gru.cu)
         check(lib.nsk_gru_fwd(gx.ptr, u.ptr, c.ptr, steps, bsz, h, hs.ptr, gates.ptr, st))
     release_tensor(pool, gx)
     out = empty_tensor(pool, (bsz, h), F32)
     check(lib.nsk_memcpy_d2d(out.ptr, hs.ptr + 4 * steps * bsz * h, 4 * bsz * h, st))
-    record("gru", out, x, w, b, u, c, saved=(x, hs, gates, w, u),
-           attrs={"T": steps, "B": bsz, "H": h, "E": e, "tc": tc})
+    saved = (x, hs, gates, w, u) + ((hsb,) if tc else ())
+    record("gru", out, x, w, b, u, c, saved=saved, attrs={"T": steps, "B": bsz, "H": h, "E": e, "tc": tc})
     return out
 
 
@@ -495,6 +497,90 @@ def _gru_tc(bsz: int, h: int) -> bool:
 
 
 @rule("gru")
+def _r_gru(node, g, pool, sinks):
+    from .tensor import _gemm, _Operands
+
+    tc = node.attrs.get("tc")
+    x, hs, gates, w, u = node.saved[:5]
+    T, B, H, E = (node.attrs[k] for k in ("T", "B", "H", "E"))
+    H3, TB = 3 * H, T * B
+    lib, st = _lib.lib(), _lib.stream()
+    outs = [None] * 5
+
+    def target(i, shape):
+        if sinks[i] is not None:
+            return sinks[i].ptr, 1.0, SUNK
+        t = empty_tensor(pool, shape, F32)
+        return t.ptr, 0.0, t
+
+    dhs = empty_tensor(pool, (TB, H), F32)
+    check(lib.nsk_fill_f32(dhs.ptr, (T - 1) * B * H, 0.0, st))
+    check(lib.nsk_memcpy_d2d(dhs.ptr + 4 * (T - 1) * B * H, g.ptr, 4 * B * H, st))
+    dh0 = empty_tensor(pool, (B, H), F32)
+    if tc:
+        # the cluster kernel emits dgx / dgh as bf16 GEMM operands and reduces the bias gradients itself
+        hsb = node.saved[5]
+        dgx = empty_tensor(pool, (TB, H3), BF16)
+        dgh = empty_tensor(pool, (TB, H3), BF16)
+        scratch = []
+        bias = []
+        for i in (2, 4):
+            if node.inputs[i].requires_grad:
+                ptr, beta, outs[i] = target(i, (H3,))
+            else:
+                tmp = empty_tensor(pool, (H3,), F32)
+                scratch.append(tmp)
+                ptr, beta = tmp.ptr, 0.0
+            bias.append((ptr, beta))
+        ws = GRU_WS.get(lib.nsk_gru_tc_workspace(B, H))
+        check(lib.nsk_gru_bwd_tc(dhs.ptr, u.bf16_ptr(), hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr,
+                                 bias[0][0], bias[0][1], bias[1][0], bias[1][1], ws.ptr, ws.nbytes, st))
+        for tmp in scratch:
+            release_tensor(pool, tmp)
+        hprev = Tensor((TB, H), Buffer(TB * H, BF16, base=hsb.buffer, offset=0))
+    else:
+        dgx = empty_tensor(pool, (TB, H3), F32)
+        dgh = empty_tensor(pool, (TB, H3), F32)
+        ws = GRU_WS.get(lib.nsk_gru_bwd_workspace(T, B, H))
+        check(lib.nsk_gru_bwd(dhs.ptr, u.ptr, hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr,
+                              ws.nbytes, st))
+        hprev = Tensor((TB, H), Buffer(TB * H, F32, base=hs.buffer, offset=0))
+    release_tensor(pool, dhs)
+    release_tensor(pool, dh0)
+
+    # bf16 operands, fp32 accumulation for the batched weight / input gradients (K = T*B steps)
+    with _Operands(pool, BF16, dgx, dgh, x, w, hprev) as (pgx, pgh, px, pw, ph):
+        if node.inputs[0].requires_grad:
+            xdt = node.inputs[0].tensor.dtype  # the gradient takes the input's dtype
+            dx = empty_tensor(pool, (TB, E), xdt)
+            _gemm(pgx, 0, H3, pw, 1, E, TB, E, H3, dx.ptr, E, dtype=BF16, out_f32=xdt == F32)  # dx = dgx . W
+            outs[0] = dx
+        if node.inputs[1].requires_grad:
+            ptr, beta, outs[1] = target(1, (H3, E))
+            _gemm(pgx, 1, H3, px, 1, E, H3, E, TB, ptr, E, dtype=BF16, beta=beta)  # dW = dgx^T . x
+        if node.inputs[3].requires_grad:
+            ptr, beta, outs[3] = target(3, (H3, H))
+            _gemm(pgh, 1, H3, ph, 1, H, H3, H, TB, ptr, H, dtype=BF16, beta=beta)  # dU = dgh^T . h_{t-1}
+    if not tc:
+        if node.inputs[2].requires_grad:
+            ptr, beta, outs[2] = target(2, (H3,))
+            check(lib.nsk_colsum(F32, dgx.ptr, ptr, TB, H3, beta, st))
+        if node.inputs[4].requires_grad:
+            ptr, beta, outs[4] = target(4, (H3,))
+            check(lib.nsk_colsum(F32, dgh.ptr, ptr, TB, H3, beta, st))
+    release_tensor(pool, dgx)
+    release_tensor(pool, dgh)
+    return outs
+
+
+def _gru_tc(bsz: int, h: int) -> bool:
+    """The tcgen05 cluster recurrence covers 1 <= B <= 64, H in 128..512 (H % 64 == 0); NSK_GRU_TC=0 forces the
+    fp32 cooperative kernel (A/B and precision studies)."""
+    import os
+
+    return os.environ.get("NSK_GRU_TC", "1") != "0" and bool(_lib.lib().nsk_gru_tc_supported(bsz, h))
+
+
 def _r_gru(node, g, pool, sinks):
     from .tensor import _gemm, _Operands
 

@@ -1,7 +1,7 @@
 """Per-step phase timeline of the tcgen05 GRU forward, every CTA, from globaltimer stamps (NSK_GRU_TRACE=1).
 
-Stamps per (CTA, step): 0 after the cluster wait, 1 / 2 first / last h chunk landed (MMA warp), 3 accumulator ready,
-5 accumulator tile in shared memory, 6 gate math done, 7 h_{t+1} stored + proxy fence, 4 after the cluster arrive."""
+Stamps per (CTA, step): 1 / 2 first / last h slice landed (MMA warp), 3 accumulator ready, 5 accumulator tile in
+shared memory, 6 gate math done, 7 cluster barrier passed (peers done with h_t), 4 end of the step's work."""
 import ctypes as C
 import os
 import sys
@@ -26,10 +26,10 @@ for _ in range(3):
     s.tape().clear(s.pool)
 buf = np.zeros((CL, T, 16), np.int64)
 _lib.check(lib.nsk_gru_trace(buf.ctypes.data, T * CL))
-t0 = buf[:, :, 0].min(axis=0)  # per step: earliest wait exit
+t0 = buf[:, :, 1].min(axis=0)  # per step: earliest first-slice arrival
 rel = buf - t0[None, :, None]
-order = [0, 1, 2, 3, 5, 8, 9, 6, 7, 4]
-names = ["wait", "chunk0", "chunkN", "acc", "tile", "lds", "gx", "math", "hx", "arrive"]
+order = [1, 2, 3, 5, 6, 7, 4]
+names = ["slice0", "sliceN", "acc", "tile", "math", "bar_wait", "step_end"]
 print("median over steps 2.., per stamp: min / median / max over CTAs (ns from the step's first wait exit)")
 for k, nm in zip(order, names):
     v = np.median(rel[:, 2:, k], axis=1)
