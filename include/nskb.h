@@ -95,6 +95,14 @@ int nsk_conv2d_fprop_stats(const NskConvDesc* d, const void* x, const void* w, v
 int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, void* stream);
 /* dx = dgrad + beta * dx (bf16, in place): accumulates a second gradient contribution in the epilogue */
 int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, void* stream);
+/* dgrad producing the (complete) gradient of a BatchNorm's output -- the backward of BatchNorm+ReLU fused into
+ * the dgrad epilogue: stores dz = relu_mask * (dgrad + beta * dx) (beta 0 or 1; relu_mask may be NULL) and
+ * per-CTA partials [nparts][2][C] of sum dz and sum dz * bn_x (bn_x = the BatchNorm's saved bf16 input) for
+ * nsk_bn_bwd_partials. Replaces the reduction pass of the reference-restated BatchNorm backward
+ * (oracle/restated.py batchnorm_bwd; the reference has no BatchNorm). partials: 2*SMs x 2 x C. */
+int nsk_conv2d_dgrad_bnstats(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta,
+                             const void* bn_x, const void* relu_mask, float* partials, uint64_t partial_floats,
+                             int* nparts, void* stream);
 /* CTAs per weight-gradient launch (0 = default two per SM); see side.py */
 int nsk_wgrad_grid_cap(int ctas);
 uint64_t nsk_conv2d_wgrad_workspace(const NskConvDesc* d);
@@ -180,6 +188,10 @@ int nsk_bn_fwd_eval(const void* x, const float* gamma_beta, const float* running
 int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float* gamma_beta, const float* mean,
                const float* invstd, void* dx, void* dres, float* dgamma_beta, float beta_acc, uint64_t rows, int C,
                float* ws, void* stream);
+/* nsk_bn_bwd with dz already ReLU-masked and its statistics taken from dgrad partials (nsk_conv2d_dgrad_bnstats) */
+int nsk_bn_bwd_partials(const float* partials, int nparts, const void* dz, const void* x, const float* gamma_beta,
+                        const float* mean, const float* invstd, void* dx, void* dres, float* dgamma_beta,
+                        float beta_acc, uint64_t rows, int C, float* ws, void* stream);
 int nsk_avgpool_fwd(int dtype_in, const void* x, float* y, int N, int HW, int C, void* stream);
 int nsk_avgpool_bwd(const float* dy, int dtype_out, void* dx, int N, int HW, int C, void* stream);
 /* argmax: one byte per output element (window position r*k+s of the first maximum), written by the forward */

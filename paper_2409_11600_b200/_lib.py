@@ -64,6 +64,7 @@ SIGNATURES = {
     "nsk_wgrad_grid_cap": (i32, [i32]),
     "nsk_conv2d_dgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, vp]),
     "nsk_conv2d_dgrad_acc": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp]),
+    "nsk_conv2d_dgrad_bnstats": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp, vp, vp, u64, C.POINTER(i32), vp]),
     "nsk_conv2d_wgrad_workspace": (u64, [C.POINTER(ConvDesc)]),
     "nsk_conv2d_wgrad": (i32, [C.POINTER(ConvDesc), vp, vp, vp, f32, vp, u64, vp]),
     "nsk_gemm_simt": (i32, [i32, i32, i32, i32, i32, vp, i64, vp, i64, vp, i64, vp, f32, vp]),
@@ -92,6 +93,7 @@ SIGNATURES = {
     "nsk_bn_fwd": (i32, [vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, f32, vp, vp]),
     "nsk_bn_fwd_partials": (i32, [vp, i32, vp, vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp, f32, vp, vp]),
     "nsk_bn_bwd": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, f32, u64, i32, vp, vp]),
+    "nsk_bn_bwd_partials": (i32, [vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, f32, u64, i32, vp, vp]),
     "nsk_bn_running_update": (i32, [vp, vp, vp, u64, i32, f32, f32, vp]),
     "nsk_bn_fwd_eval": (i32, [vp, vp, vp, vp, u64, i32, f32, i32, vp, vp, vp]),
     "nsk_avgpool_fwd": (i32, [i32, vp, vp, i32, i32, i32, vp]),

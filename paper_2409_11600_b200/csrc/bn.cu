@@ -614,6 +614,10 @@ int check(uint64_t rows, int C, const void* a, const void* b) {
 // device address of the forward fold count, zeroed by the conv statistics epilogue (umma_gemm.cu) that feeds
 // nsk_bn_fwd_partials
 unsigned* nsk::bn_fold_counter_fwd(cudaStream_t st) { return fold_counters(st); }
+unsigned* nsk::bn_fold_counter_bwd(cudaStream_t st) {
+  unsigned* fc = fold_counters(st);
+  return fc ? fc + 2 : nullptr;
+}
 
 extern "C" {
 
@@ -737,6 +741,34 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
                   (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres,
                   fold_blocks(C), fold_counters(st) + 2);
   NSK_LAUNCH_CHECK("bn_bwd");
+  return NSK_OK;
+}
+
+// backward from channel partials produced by the dgrad that wrote dz (nsk_conv2d_dgrad_bnstats: dz is already
+// ReLU-masked): finalize + apply, no reduction pass over dz and x
+int nsk_bn_bwd_partials(const float* partials, int nparts, const void* dz, const void* x, const float* gamma_beta,
+                        const float* mean, const float* invstd, void* dx, void* dres, float* dgamma_beta,
+                        float beta_acc, uint64_t rows, int C, float* ws, void* stream) {
+  int rc = check(rows, C, dz, x);
+  if (rc) return rc;
+  if (nparts < 1) return nsk::set_error(NSK_ERR_SHAPE, "batchnorm backward: no statistics partials");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* coef = ws + (size_t)MAXBLK * 2 * C;
+  const uint64_t nv = rows * (uint64_t)C / 8;
+  if (!fold_in_apply(rows, C, st)) {
+    nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, partials, nparts, rows, C, gamma_beta, mean, invstd, dgamma_beta,
+                    beta_acc, coef);
+    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 3 * C * sizeof(float), st,
+                    (const __nv_bfloat16*)dz, (const __nv_bfloat16*)x, (const uint8_t*)nullptr, (const float*)coef,
+                    (__nv_bfloat16*)dx, (__nv_bfloat16*)dres, rows, C);
+    NSK_LAUNCH_CHECK("bn_bwd_partials");
+    return NSK_OK;
+  }
+  nsk::launch_pdl(bn_bwd_apply_fold_kernel, fold_grid(nv, C), AT, 3 * C * sizeof(float), st, partials, nparts, rows,
+                  C, gamma_beta, mean, invstd, dgamma_beta, beta_acc, coef, (const __nv_bfloat16*)dz,
+                  (const __nv_bfloat16*)x, (const uint8_t*)nullptr, (__nv_bfloat16*)dx, (__nv_bfloat16*)dres,
+                  fold_blocks(C), fold_counters(st) + 2);
+  NSK_LAUNCH_CHECK("bn_bwd_partials");
   return NSK_OK;
 }
 

@@ -56,6 +56,8 @@ int encode_tmap_im2col(CUtensorMap* map, const void* gaddr, int N, int H, int W,
 bool pdl_enabled();
 // device word counting the channels folded by a fused BatchNorm apply (bn.cu); producers of its partials zero it
 unsigned* bn_fold_counter_fwd(cudaStream_t st);
+// backward fold count, zeroed by the dgrad statistics epilogue that feeds nsk_bn_bwd_partials
+unsigned* bn_fold_counter_bwd(cudaStream_t st);
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
@@ -314,6 +316,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+// 16-byte asynchronous global -> shared copy (zero-fill when bytes == 0), per-thread commit groups
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, 128-byte swizzle, sm_100 (version 1).
@@ -343,6 +351,21 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+// column sums of a 32 x 32 tile held one row per lane (v[col]): butterfly reduce-scatter, lane L returns the sum of
+// column L over the warp's 32 rows (31 shuffles, no shared memory)
+__device__ __forceinline__ float warp_colsum32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < off; ++i) {
+      const float lo_v = v[i], hi_v = v[i + off];
+      const float send = hi ? lo_v : hi_v;
+      v[i] = (hi ? hi_v : lo_v) + __shfl_xor_sync(0xffffffffu, send, off);
+    }
+  }
+  return v[0];
 }
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll

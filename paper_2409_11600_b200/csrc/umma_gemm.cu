@@ -80,6 +80,13 @@ struct UmmaProb {
   int rr_fast;  // row-reuse 3x3 on 32-wide rows, taps t = 0..2 at row offsets t (1: fprop, 2: dgrad) or 2 - t
                 // (4: fprop, 3: dgrad): the MMA issuer uses immediate descriptor offsets
   int asplit;  // WRES: each stage's A box is asplit row bands, one per producer warp (more boxes in flight)
+  // dgrad feeding a BatchNorm's backward (nsk_conv2d_dgrad_bnstats): the output is the gradient dz of that
+  // BatchNorm's output, stored ReLU-masked (bmask bits; dz = g * [y > 0]); `stats` then receives per-CTA partials
+  // [gridDim.x][2][N] of sum dz and sum dz * x (bx = the BatchNorm's input) so the backward needs no reduction
+  // pass. bacc: dz = mask * bf16(old + dgrad), the pending gradient accumulated before masking and statistics.
+  const __nv_bfloat16* bx;
+  const uint8_t* bmask;
+  int bacc;
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
@@ -106,12 +113,16 @@ struct Smem {
   static constexpr int W_OFF = STAGES * STAGE_BYTES;                      // resident filter taps (WRES)
   static constexpr int BAR_OFF = W_OFF + (WRES ? 9 * B1_BYTES : 0);
   // TMA-store source; 512-byte aligned: the SWIZZLE_64B pattern is taken from address bits 7-8
-  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 5) + 16 + 511) / 512 * 512;
+  static constexpr int STG_OFF = (BAR_OFF + 8 * (2 * STAGES + 9) + 16 + 511) / 512 * 512;
   // staging buffers per epilogue warp: double-buffered with 8 warps (one CTA per SM anyway); single with 4 so
   // the 64/128-wide tiles keep two CTAs per SM
   static constexpr int NSTG = EPI == 8 ? 2 : 1;
   static constexpr int TOTAL = STG_OFF + EPI * NSTG * kStgBytes + 1024;  // + epilogue staging
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
+  // TMEM accumulator buffers: four when they fit the 512 columns beside the co-resident CTA (the epilogue of a tile
+  // may then lag the MMAs by up to three tiles), else two
+  static constexpr bool kTwoPerSM = 2 * TOTAL + 8192 <= 227 * 1024;
+  static constexpr int NACC = (kTwoPerSM ? 256 : 512) / BN >= 4 ? 4 : 2;
+  static constexpr int TMEM_COLS = NACC * BN < 32 ? 32 : NACC * BN;
 };
 
 // bf16x8 beta*old + v (fp32 math, one rounding): the same value the axpy kernel would produce
@@ -220,7 +231,11 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 // overlap the MMAs of unit j+1.
 // EPI epilogue warps (4 or 8): with 8, two warpgroups take alternate 32-column chunks of each tile, doubling the
 // TMEM-drain / store parallelism for the wide (BN = 256) tiles whose epilogue is the bottleneck.
-template <int BN, int ESZ, int STAGES, bool RR, int EPI, bool WRES>
+// BST: the output is the gradient of a BatchNorm's output (dgrad feeding nsk_bn_bwd_partials): the epilogue
+// masks it with the BatchNorm's ReLU bits, adds the pending gradient (bacc) and emits per-CTA column sums of dz and
+// dz * x (p.bx = the BatchNorm input) into p.stats -- a separate instantiation, so the other passes keep their
+// register budget
+template <int BN, int ESZ, int STAGES, bool RR, int EPI, bool WRES, bool BST>
 __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::template threads<EPI>(),
                                   Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::kTwoPerSM ? 2 : 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -234,10 +249,11 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
   uint64_t* full = (uint64_t*)(smem + S::BAR_OFF);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2] accumulator ready for the epilogue
-  uint64_t* tempty = tfull + 2;      // [2] accumulator drained by the epilogue
-  uint64_t* wfull = tempty + 2;      // resident filter taps landed (WRES)
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 3);
+  constexpr int NACC = S::NACC;
+  uint64_t* tfull = empty + STAGES;  // [NACC] accumulator ready for the epilogue
+  uint64_t* tempty = tfull + NACC;   // [NACC] accumulator drained by the epilogue
+  uint64_t* wfull = tempty + NACC;   // resident filter taps landed (WRES)
+  uint32_t* tmem_slot = (uint32_t*)(wfull + 1);
   uint8_t* stage_base = smem + S::STG_OFF;
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform role index
@@ -249,7 +265,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       mbar_init(&full[s], WRES ? p.asplit : 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI);  // one arrival per epilogue warp
     }
@@ -438,12 +454,12 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         } else {
           w = decode_unit(p, u, BN);
         }
-        const int acc = j & 1;
-        if (j >= 2) {
+        const int acc = j % NACC;
+        if (j >= NACC) {
           if constexpr (kGate)
             gate_sync(kBarAcc + acc);
           else
-            mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+            mbar_wait(&tempty[acc], (j / NACC - 1) & 1);
         }
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -532,9 +548,9 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
       const Unit w = decode_unit(p, u, BN);
-      const int acc = j & 1;
-      if (j >= 2) {
-        mbar_wait(&tempty[acc], ((j >> 1) - 1) & 1);
+      const int acc = j % NACC;
+      if (j >= NACC) {
+        mbar_wait(&tempty[acc], (j / NACC - 1) & 1);
         gate_arrive(kBarAcc + acc);
       }
       for (int k = 0; k < w.nk; ++k) {
@@ -555,24 +571,16 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     float* st_acc = (float*)(stage_base + EPI * S::NSTG * kStgBytes);  // [2][N] CTA channel sums (stats mode)
     int sbuf = 0;  // staging double buffer (TMA stores of the previous chunk may still be reading the other)
     float* st_red = st_acc + 2 * p.N + eg * 256;                // per warpgroup: [4 warps][2][32]
-    if (p.stats) {
+    if (p.stats && !BST) {
       for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) st_acc[i] = 0.f;
       epi_bar_all(32 * EPI);
     }
-    int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const Unit w = decode_unit(p, u, BN);
-      const int acc = j & 1;
-      mbar_wait_backoff(&tfull[acc], (j >> 1) & 1);
-      tc_fence_after();
+    // output element offset of this thread's row of unit w
+    auto row_of = [&](const Unit& w) -> long long {
       const int m = w.m0 + r;
-      const bool row_ok = m < p.M;
-      long long row_off;
-      if (p.mode == MODE_WGRAD) {
-        row_off = (long long)w.z * p.N * p.Mpad + m;  // transposed partials: ws[split][n][m]
-      } else if (p.mode == MODE_CONV && p.k_per_split > 0) {
-        row_off = ((long long)w.z * p.M + m) * p.ldc;  // split-K conv: fp32 partials ws[z][M][N]
-      } else if (p.mode == MODE_CONV) {
+      if (p.mode == MODE_WGRAD) return (long long)w.z * p.N * p.Mpad + m;  // transposed partials: ws[split][n][m]
+      if (p.mode == MODE_CONV && p.k_per_split > 0) return ((long long)w.z * p.M + m) * p.ldc;  // split-K conv
+      if (p.mode == MODE_CONV) {
         const int hw = p.Ho * p.Wo;
         const int nn = m / hw;
         const int rem = m - nn * hw;
@@ -580,17 +588,43 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         const int jj = rem - ii * p.Wo;
         const int ph = p.cph[w.z], pw = p.cpw[w.z];
         const long long pix = ((long long)nn * p.Hd + ii * p.os + ph) * p.Wd + (jj * p.os + pw);
-        row_off = pix * p.ldc;
-      } else {
-        // split-K GEMM: fp32 partials of split z into ws[z][M][N] (p.out / p.ldc set up by the host)
-        row_off = ((long long)(p.k_per_split > 0 ? w.z : 0) * p.M + m) * p.ldc;
+        return pix * p.ldc;
       }
-      int nchunks = (p.N - w.n0 + 31) / 32;
-      if (nchunks > BN / 32) nchunks = BN / 32;
+      // split-K GEMM: fp32 partials of split z into ws[z][M][N] (p.out / p.ldc set up by the host)
+      return ((long long)(p.k_per_split > 0 ? w.z : 0) * p.M + m) * p.ldc;
+    };
+    auto chunks_of = [&](const Unit& w) {
+      const int n = (p.N - w.n0 + 31) / 32;
+      return n > BN / 32 ? BN / 32 : n;
+    };
+    // BatchNorm-backward statistics (BST): per-warp column sums of dz and dz * x, [EPI warps][2][N / G] floats
+    // (G = EPI / 4 warpgroups; warp (q, eg) owns the 32-column chunks gc = eg mod G of the output)
+    constexpr int G = EPI / 4;
+    float* st_col = (float*)(stage_base + EPI * S::NSTG * kStgBytes);
+    const int ncol_w = (p.N / 32 + G - 1) / G * 32;  // columns per warp
+    if constexpr (BST) {
+      for (int i = lane; i < 2 * ncol_w; i += 32) st_col[(warp - 4) * 2 * ncol_w + i] = 0.f;
+      __syncwarp();
+    }
+    int j = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      const Unit w = decode_unit(p, u, BN);
+      const int acc = j % NACC;
+      mbar_wait_backoff(&tfull[acc], (j / NACC) & 1);
+      tc_fence_after();
+      const int m = w.m0 + r;
+      const bool row_ok = m < p.M;
+      const long long row_off = row_of(w);
+      const int nchunks = chunks_of(w);
 #pragma unroll 1
       for (int c = eg; c < nchunks; c += EPI / 4) {
         uint32_t v[32];
         if (p.probe & 32) continue;  // diagnostics: accumulator never read
+        // BST: this row's ReLU-mask word, requested before the TMEM load
+        uint32_t bmw = 0xffffffffu;
+        if constexpr (BST) {
+          if (row_ok && p.bmask) bmw = __ldg((const uint32_t*)(p.bmask + ((row_off + w.n0 + c * 32) >> 3)));
+        }
         if (w.nk > 0) {
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, v);
           tmem_ld_wait();
@@ -653,6 +687,22 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             u4[t].z = pack_bf16x2(f[8 * t + 4], f[8 * t + 5]);
             u4[t].w = pack_bf16x2(f[8 * t + 6], f[8 * t + 7]);
           }
+          if constexpr (BST) {
+            // dz = [y > 0] * bf16(pending + bf16(dgrad)) -- the pending gradient added as the TMA reduce-add / axpby
+            // accumulation paths add it; masking commutes with the rounding
+            const uint4* o4 = (const uint4*)((const __nv_bfloat16*)p.out + row_off + col0);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              uint4 v4 = u4[c4];
+              if (p.bacc && row_ok) v4 = bf16x8_axpby(o4[c4], 1.f, v4);
+              const uint32_t m8 = bmw >> (8 * c4);
+              uint32_t* v32 = (uint32_t*)&v4;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                v32[i] &= (((m8 >> (2 * i)) & 1u) ? 0x0000ffffu : 0u) | (((m8 >> (2 * i + 1)) & 1u) ? 0xffff0000u : 0u);
+              u4[c4] = v4;
+            }
+          }
           // 64-byte-swizzled staging (the TMA store map uses SWIZZLE_64B): 16-byte chunk c of row r sits at chunk
           // c ^ ((r >> 1) & 3). Each quarter-warp store then covers all 32 banks exactly once, and the chunk index
           // of the register operand stays static (a lane-dependent register index spilled u4 to local memory)
@@ -660,7 +710,39 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
           for (int c4 = 0; c4 < 4; ++c4) *(uint4*)(stg + stg_off(lane, c4)) = u4[c4];
           if (p.tma_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (p.stats) {
+          if constexpr (BST) {
+            // column sums over this warp's 32 rows (thread = row) by a butterfly reduce-scatter: lane ends with column
+            // col0 + lane; no shared-memory traffic beside the MMAs' operand reads, no cross-warp barrier per chunk
+            float red[32];
+            const uint4* x4 = (const uint4*)(p.bx + row_off + col0);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {  // dz * x
+              const uint4 xv = row_ok ? __ldg(x4 + c4) : make_uint4(0u, 0u, 0u, 0u);
+              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
+              const __nv_bfloat162* hx = (const __nv_bfloat162*)&xv;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 z = __bfloat1622float2(hz[i]), xx = __bfloat1622float2(hx[i]);
+                red[8 * c4 + 2 * i] = z.x * xx.x;
+                red[8 * c4 + 2 * i + 1] = z.y * xx.y;
+              }
+            }
+            const float s2 = warp_colsum32(red, lane);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {  // dz
+              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 z = __bfloat1622float2(hz[i]);
+                red[8 * c4 + 2 * i] = z.x;
+                red[8 * c4 + 2 * i + 1] = z.y;
+              }
+            }
+            const float s1 = warp_colsum32(red, lane);
+            float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
+            col[0] += s1;
+            col[ncol_w] += s2;
+          } else if (p.stats) {
             // column sums of the staged (bf16-rounded) tile: lane = column, rows of this warp
             const unsigned okm = __ballot_sync(0xffffffffu, row_ok);
             float s1 = 0.f, s2 = 0.f;
@@ -726,7 +808,19 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    if (p.stats) {
+    if constexpr (BST) {
+      // CTA partials [2][N]: the four lane-quarter warps of the owning warpgroup, in fixed order
+      epi_bar_all(32 * EPI);
+      float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
+      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) {
+        const int k = i / p.N, n = i - k * p.N;
+        const int gc = n / 32, e = gc % G, li = (gc / G) * 32 + (n & 31);
+        float t = 0.f;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) t += st_col[(e * 4 + qq) * 2 * ncol_w + k * ncol_w + li];
+        out[i] = t;
+      }
+    } else if (p.stats) {
       epi_bar_all(32 * EPI);
       float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
       for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) out[i] = st_acc[i];
@@ -1102,7 +1196,9 @@ __global__ void __launch_bounds__(256, 1) wgrad_rr128_kernel(const __grid_consta
 // for the BatchNorm consuming y (nsk_bn_fwd_partials), as the conv epilogue would have written them.
 constexpr int kFoldThreads = 256;
 __global__ void __launch_bounds__(kFoldThreads) conv_split_fold_kernel(const float* __restrict__ ws, int splits, int M,
-                                                                       int N, __nv_bfloat16* y, float beta, float* stats) {
+                                                                       int N, __nv_bfloat16* y, float beta, float* stats,
+                                                                       const __nv_bfloat16* __restrict__ bx,
+                                                                       const uint8_t* __restrict__ bmask) {
   pdl_wait();
   extern __shared__ float fold_red[];  // [RPB][N] (stats)
   const int CV = N / 8;
@@ -1126,8 +1222,34 @@ __global__ void __launch_bounds__(kFoldThreads) conv_split_fold_kernel(const flo
       v.x = pack_bf16x2(a[0], a[1]); v.y = pack_bf16x2(a[2], a[3]);
       v.z = pack_bf16x2(a[4], a[5]); v.w = pack_bf16x2(a[6], a[7]);
       if (beta != 0.f) v = bf16x8_axpby(*dst, beta, v);
+      if (bmask) {  // BatchNorm-backward mode: dz = [y > 0] * g
+        const unsigned m = bmask[(r * N + cv * 8) >> 3];
+        uint32_t* v32 = (uint32_t*)&v;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          v32[i] &= (((m >> (2 * i)) & 1u) ? 0x0000ffffu : 0u) | (((m >> (2 * i + 1)) & 1u) ? 0xffff0000u : 0u);
+      }
       *dst = v;
-      if (stats) {
+      if (stats && bx) {  // sum dz, sum dz * x (x = the BatchNorm input)
+        float xv[8];
+        {
+          const uint4 xu = __ldg((const uint4*)(bx + r * N + cv * 8));
+          const __nv_bfloat162* xh = (const __nv_bfloat162*)&xu;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 t = __bfloat1622float2(xh[i]);
+            xv[2 * i] = t.x;
+            xv[2 * i + 1] = t.y;
+          }
+        }
+        const __nv_bfloat162* h = (const __nv_bfloat162*)&v;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __bfloat1622float2(h[i]);
+          s1[2 * i] += f.x; s2[2 * i] += f.x * xv[2 * i];
+          s1[2 * i + 1] += f.y; s2[2 * i + 1] += f.y * xv[2 * i + 1];
+        }
+      } else if (stats) {
         const __nv_bfloat162* h = (const __nv_bfloat162*)&v;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -1208,12 +1330,23 @@ int gemm_scratch(size_t floats, cudaStream_t st, float** out) {
 
 int g_wgrad_grid_cap = 0;  // CTAs per wgrad launch (0: two per SM as usual)
 
-template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false>
+// dynamic shared memory past Smem::TOTAL: statistics accumulators [2][N] + per-warpgroup reduction slots, and
+// for the BatchNorm-backward statistics a staging block of the BatchNorm input per epilogue warp
+int epi_extra_smem(const UmmaProb& p, int epi) {
+  if (!p.stats) return 0;
+  if (p.bx) {  // BatchNorm-backward column sums: [epi warps][2][columns per warp]
+    const int g = epi / 4;
+    return epi * 2 * ((p.N / 32 + g - 1) / g * 32) * (int)sizeof(float);
+  }
+  return (2 * p.N + epi * 64) * (int)sizeof(float);
+}
+
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false, bool BST = false>
 int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, UmmaProb p, cudaStream_t st,
                 int* grid_out) {
   using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
-  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES>;
-  const int smem = S::TOTAL + (p.stats ? (2 * p.N + EPI * 64) * (int)sizeof(float) : 0);
+  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES, BST>;
+  const int smem = S::TOTAL + epi_extra_smem(p, EPI);
   if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
   static int configured = 0;
   if (smem > configured) {
@@ -1236,7 +1369,7 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   return NSK_OK;
 }
 
-template <int ESZ>
+template <int ESZ, bool BST = false>
 int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
                 cudaStream_t st, int* grid_out = nullptr, const CUtensorMap* cmap = nullptr) {
   static CUtensorMap dummy{};
@@ -1251,28 +1384,28 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
         case 64: {
           // one 64-channel chunk, N = 64, 3x3 in strided tap boxes: keep all 9 taps resident (the ring then
           // moves only A; re-fetching the 72 KB filter per tile was half the L2->smem traffic)
-          if (p.wres && nt == 1 && nz == 1) return launch_umma<64, 2, 4, true, 8, true>(a, b, c, p, st, grid_out);
+          if (p.wres && nt == 1 && nz == 1) return launch_umma<64, 2, 4, true, 8, true, BST>(a, b, c, p, st, grid_out);
           if (p.wres) return nsk::set_error(NSK_ERR_UNSUPPORTED, "weight-resident conv needs a single 64-wide tile");
-          return launch_umma<64, 2, 2, true>(a, b, c, p, st, grid_out);
+          return launch_umma<64, 2, 2, true, 4, false, BST>(a, b, c, p, st, grid_out);
         }
         case 128:
-          return launch_umma<128, 2, 2, true>(a, b, c, p, st, grid_out);
+          return launch_umma<128, 2, 2, true, 4, false, BST>(a, b, c, p, st, grid_out);
       }
     }
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "row-reuse conv needs bf16 and N <= 128");
   }
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 4>(a, b, c, p, st, grid_out);
+      return launch_umma<64, ESZ, 4, false, 4, false, BST>(a, b, c, p, st, grid_out);
     case 128:
-      return launch_umma<128, ESZ, 3>(a, b, c, p, st, grid_out);
+      return launch_umma<128, ESZ, 3, false, 4, false, BST>(a, b, c, p, st, grid_out);
     case 256: {
       // 8 epilogue warps unless the statistics buffers would not fit beside them
       using S8 = Smem<256, ESZ, 4, false, 8>;
-      const int need = S8::TOTAL + (p.stats ? (2 * p.N + 8 * 64) * (int)sizeof(float) : 0);
+      const int need = S8::TOTAL + epi_extra_smem(p, 8);
       if (need <= 227 * 1024 && !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0'))
-        return launch_umma<256, ESZ, 4, false, 8>(a, b, c, p, st, grid_out);
-      return launch_umma<256, ESZ, 4>(a, b, c, p, st, grid_out);
+        return launch_umma<256, ESZ, 4, false, 8, false, BST>(a, b, c, p, st, grid_out);
+      return launch_umma<256, ESZ, 4, false, 4, false, BST>(a, b, c, p, st, grid_out);
     }
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
@@ -1481,6 +1614,11 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   p.tma_store = 0;
   p.stats = nullptr;
   p.rr = 0;
+  const __nv_bfloat16* bx = p.bx;
+  const uint8_t* bmask = p.bmask;
+  p.bx = nullptr;
+  p.bmask = nullptr;
+  p.bacc = 0;
   if ((rc = dispatch_bn<2>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st))) return rc;
   const int CV = N / 8, RPB = kFoldThreads / CV;
   unsigned grid = (unsigned)((M + RPB - 1) / RPB);
@@ -1488,7 +1626,7 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   if (!stats && grid > (unsigned)(16 * nsk::sm_count())) grid = 16 * nsk::sm_count();
   const size_t smem = stats ? (size_t)RPB * N * sizeof(float) : 0;
   nsk::launch_pdl(conv_split_fold_kernel, grid, kFoldThreads, smem, st, (const float*)ws, splits, M, N,
-                  (__nv_bfloat16*)out, beta, stats);
+                  (__nv_bfloat16*)out, beta, stats, bx, bmask);
   NSK_LAUNCH_CHECK("conv_split_fold_kernel");
   if (nparts) *nparts = (int)grid;
   return NSK_OK;
@@ -1666,6 +1804,9 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
                         ts ? &mc : nullptr);
 }
 
+int conv_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, const __nv_bfloat16* bx,
+               const uint8_t* bmask, float* stats, uint64_t stats_floats, int* nparts, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -1690,6 +1831,31 @@ int nsk_conv2d_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* 
 
 // dx = dgrad + beta * dx (bf16 in place): a second gradient contribution accumulated in the epilogue
 int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, void* stream) {
+  return conv_dgrad(d, dy, w, dx, beta, nullptr, nullptr, nullptr, 0, nullptr, stream);
+}
+
+// dgrad whose result is the gradient of a BatchNorm's output (the last contribution to it): stores
+// dz = relu_mask * (dgrad + beta * dx) and per-CTA partials [nparts][2][C] of sum dz and sum dz * bn_x for
+// nsk_bn_bwd_partials (no reduction pass over dz and x)
+int nsk_conv2d_dgrad_bnstats(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta,
+                             const void* bn_x, const void* relu_mask, float* partials, uint64_t partial_floats,
+                             int* nparts, void* stream) {
+  if (!bn_x || !partials || !nparts) return nsk::set_error(NSK_ERR_SHAPE, "conv2d dgrad_bnstats: null argument");
+  if (beta != 0.f && beta != 1.f) return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad_bnstats: beta 0 or 1");
+  if (partial_floats < (uint64_t)2 * nsk::sm_count() * 2 * d->C)
+    return nsk::set_error(NSK_ERR_SHAPE, "conv2d dgrad_bnstats: partials buffer smaller than 2*SMs x 2 x C floats");
+  if (((uintptr_t)bn_x & 15) || ((uintptr_t)relu_mask & 3))
+    return nsk::set_error(NSK_ERR_UNSUPPORTED, "conv2d dgrad_bnstats: misaligned BatchNorm input or mask");
+  return conv_dgrad(d, dy, w, dx, beta, (const __nv_bfloat16*)bn_x, (const uint8_t*)relu_mask, partials,
+                    partial_floats, nparts, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+int conv_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, float beta, const __nv_bfloat16* bx,
+               const uint8_t* bmask, float* stats, uint64_t stats_floats, int* nparts, void* stream) {
   int rc = check_desc(d);
   if (rc) return rc;
   const int P = d->P, Q = d->Q, st = d->stride;
@@ -1753,7 +1919,7 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
   // accumulating into an existing gradient: a parity class without taps (1x1 stride 2: three of four) adds
   // nothing, so its work units are dropped instead of re-writing dx unchanged
   int ncls_run = ncls;
-  if (beta == 1.f && ncls > 1) {
+  if (beta == 1.f && ncls > 1 && !bx) {  // (statistics need every pixel through the epilogue)
     ncls_run = 0;
     for (int c = 0; c < ncls; ++c) {
       if (p.ntaps[c] == 0) continue;
@@ -1784,16 +1950,43 @@ int nsk_conv2d_dgrad_acc(const NskConvDesc* d, const void* dy, const void* w, vo
       try_wres(p, &ma, dy, d->N, P, Q, d->K, d->C);
     }
   }
-  if (splits > 1) return conv_split_run(p, ma, mb, splits, dsteps, dx, beta, nullptr, nullptr, (cudaStream_t)stream);
+  if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
+  if (bx) {
+    p.bx = bx;
+    p.bmask = bmask;
+    p.stats = stats;
+    p.fold_reset = nsk::bn_fold_counter_bwd((cudaStream_t)stream);
+  }
+  if (splits > 1)
+    return conv_split_run(p, ma, mb, splits, dsteps, dx, beta, stats, nparts, (cudaStream_t)stream);
   CUtensorMap mc;
   const char* red = getenv("NSK_TMA_REDUCE");
-  const bool ts = ncls == 1 && (beta == 0.f || (beta == 1.f && !(red && red[0] == '0'))) &&
+  const bool ts = ncls == 1 && (beta == 0.f || (beta == 1.f && (bx || !(red && red[0] == '0')))) &&
                   out_map(&mc, dx, p.M, d->C, d->C);
-  p.tma_store = ts ? (beta == 1.f ? 2 : 1) : 0;
-  if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
+  if (bx) {  // the epilogue adds the pending gradient itself (it needs the sum for the statistics)
+    p.bacc = beta == 1.f;
+    p.beta = 0.f;
+    p.tma_store = ts ? 1 : 0;
+  } else {
+    p.tma_store = ts ? (beta == 1.f ? 2 : 1) : 0;
+    if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
+  }
+  if (bx) {
+    rc = dispatch_bn<2, true>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run,
+                              (cudaStream_t)stream, nparts, ts ? &mc : nullptr);
+    if (rc != NSK_ERR_UNSUPPORTED) return rc;
+    // the statistics buffers do not fit beside this tile configuration: plain (accumulating) dgrad, no partials --
+    // the caller then runs the BatchNorm backward's own reduction over the unmasked gradient
+    *nparts = 0;
+    return conv_dgrad(d, dy, w, dx, beta, nullptr, nullptr, nullptr, 0, nullptr, stream);
+  }
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run, (cudaStream_t)stream,
-                        nullptr, ts ? &mc : nullptr);
+                        nparts, ts ? &mc : nullptr);
 }
+
+}  // namespace
+
+extern "C" {
 
 // Grid cap for the weight-gradient kernels. side.py sets it to one CTA per SM while wgrads run on a side stream
 // next to the rest of backward: two persistent CTAs per SM starve the compute stream (2.41 -> 2.35 ms/step).

@@ -13,6 +13,7 @@ optimizer). Gradients always take the dtype of the tensor they belong to.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 
 import numpy as np
@@ -171,6 +172,21 @@ def _r_conv2d(node, g, pool, sinks):
                                  desc.pad, desc.P, desc.Q, kp, st))
             release_tensor(pool, dcols)
             release_tensor(pool, wpk)
+        elif _BNB_FUSE and (node.bnb_sinks or {}).get(0) is not None:
+            # this dgrad completes the gradient of a BatchNorm(+ReLU) output: the epilogue stores it ReLU-masked
+            # and emits the BatchNorm-backward channel sums, so _r_batchnorm skips its reduction pass
+            bn = node.bnb_sinks[0]
+            target = acc if acc is not None else dx
+            mask = bn.saved[4] if bn.attrs["relu"] else None
+            parts = empty_tensor(pool, (2 * _lib.ctx.sm_count, 2, desc.C))
+            nparts = C.c_int(0)
+            check(lib.nsk_conv2d_dgrad_bnstats(C.byref(desc), gp, wb, target.ptr, 1.0 if acc is not None else 0.0,
+                                               bn.saved[0].ptr, None if mask is None else mask.ptr, parts.ptr,
+                                               parts.numel, C.byref(nparts), st))
+            if nparts.value > 0:
+                target.bnb_partials = (parts, nparts.value)
+            else:  # tile configuration without room for the statistics: plain dgrad ran, BN reduces itself
+                release_tensor(pool, parts)
         elif acc is not None:  # second contribution: accumulate into the pending gradient in the epilogue
             check(lib.nsk_conv2d_dgrad_acc(C.byref(desc), gp, wb, acc.ptr, 1.0, st))
         else:
@@ -202,6 +218,13 @@ def _r_conv2d(node, g, pool, sinks):
     if gtmp is not None:
         release_tensor(pool, gtmp)
     return [dx, dw]
+
+
+# BatchNorm backward statistics fused into the dgrad that completes the BatchNorm output's gradient
+# (nsk_conv2d_dgrad_bnstats). Off by default: measured on B200 the statistics epilogue lengthens the
+# latency-bound epilogue of the weight-resident 64-channel dgrad by more than the separate reduction pass costs
+# (2.08 -> 2.13 ms/step); NSK_BNB_FUSE=1 enables it (tests/test_gpu_parity_c2.py checks it either way)
+_BNB_FUSE = os.environ.get("NSK_BNB_FUSE", "0") == "1"
 
 
 # --- batchnorm (+ residual, + relu) ---------------------------------------------------------------
@@ -297,9 +320,17 @@ def _r_batchnorm(node, g, pool, sinks):
     if dx is None:
         scratch_dx = empty_tensor(pool, x.shape, BF16)
     ws = BN_WS.get(lib.nsk_bn_workspace(rows, c))
-    check(lib.nsk_bn_bwd(g.ptr, x.ptr, None if mask is None else mask.ptr, gb.ptr, mean.ptr, invstd.ptr,
-                         (dx or scratch_dx).ptr, None if dres is None else dres.ptr, dgb_ptr, beta, rows, c,
-                         ws.ptr, st))
+    parts = g.bnb_partials
+    if parts is not None:  # g arrives ReLU-masked with its channel sums (the dgrad that completed it)
+        g.bnb_partials = None
+        check(lib.nsk_bn_bwd_partials(parts[0].ptr, parts[1], g.ptr, x.ptr, gb.ptr, mean.ptr, invstd.ptr,
+                                      (dx or scratch_dx).ptr, None if dres is None else dres.ptr, dgb_ptr, beta,
+                                      rows, c, ws.ptr, st))
+        release_tensor(pool, parts[0])
+    else:
+        check(lib.nsk_bn_bwd(g.ptr, x.ptr, None if mask is None else mask.ptr, gb.ptr, mean.ptr, invstd.ptr,
+                             (dx or scratch_dx).ptr, None if dres is None else dres.ptr, dgb_ptr, beta, rows, c,
+                             ws.ptr, st))
     if scratch_dx is not None:
         release_tensor(pool, scratch_dx)
     if not node.inputs[1].requires_grad:
@@ -491,8 +522,6 @@ def gru(x: Tensor, w: Tensor, b: Tensor, u: Tensor, c: Tensor, steps: int, pool:
 def _gru_tc(bsz: int, h: int) -> bool:
     """The tcgen05 cluster recurrence covers 1 <= B <= 64, H in 128..512 (H % 64 == 0); NSK_GRU_TC=0 forces the
     fp32 cooperative kernel (A/B and precision studies)."""
-    import os
-
     return os.environ.get("NSK_GRU_TC", "1") != "0" and bool(_lib.lib().nsk_gru_tc_supported(bsz, h))
 
 
@@ -568,70 +597,6 @@ def _r_gru(node, g, pool, sinks):
         if node.inputs[4].requires_grad:
             ptr, beta, outs[4] = target(4, (H3,))
             check(lib.nsk_colsum(F32, dgh.ptr, ptr, TB, H3, beta, st))
-    release_tensor(pool, dgx)
-    release_tensor(pool, dgh)
-    return outs
-
-
-def _gru_tc(bsz: int, h: int) -> bool:
-    """The tcgen05 cluster recurrence covers 1 <= B <= 64, H in 128..512 (H % 64 == 0); NSK_GRU_TC=0 forces the
-    fp32 cooperative kernel (A/B and precision studies)."""
-    import os
-
-    return os.environ.get("NSK_GRU_TC", "1") != "0" and bool(_lib.lib().nsk_gru_tc_supported(bsz, h))
-
-
-def _r_gru(node, g, pool, sinks):
-    from .tensor import _gemm, _Operands
-
-    x, hs, gates, w, u = node.saved
-    T, B, H, E = (node.attrs[k] for k in ("T", "B", "H", "E"))
-    H3, TB = 3 * H, T * B
-    lib, st = _lib.lib(), _lib.stream()
-    dhs = empty_tensor(pool, (TB, H), F32)
-    check(lib.nsk_fill_f32(dhs.ptr, (T - 1) * B * H, 0.0, st))
-    check(lib.nsk_memcpy_d2d(dhs.ptr + 4 * (T - 1) * B * H, g.ptr, 4 * B * H, st))
-    dgx = empty_tensor(pool, (TB, H3), F32)
-    dgh = empty_tensor(pool, (TB, H3), F32)
-    dh0 = empty_tensor(pool, (B, H), F32)
-    if node.attrs.get("tc"):
-        ws = GRU_WS.get(lib.nsk_gru_tc_workspace(B, H))
-        check(lib.nsk_gru_bwd_tc(dhs.ptr, u.bf16_ptr(), hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr,
-                                 ws.nbytes, st))
-    else:
-        ws = GRU_WS.get(lib.nsk_gru_bwd_workspace(T, B, H))
-        check(lib.nsk_gru_bwd(dhs.ptr, u.ptr, hs.ptr, gates.ptr, T, B, H, dgx.ptr, dgh.ptr, dh0.ptr, ws.ptr,
-                              ws.nbytes, st))
-    release_tensor(pool, dhs)
-    release_tensor(pool, dh0)
-    outs = [None] * 5
-
-    def target(i, shape):
-        if sinks[i] is not None:
-            return sinks[i].ptr, 1.0, SUNK
-        t = empty_tensor(pool, shape, F32)
-        return t.ptr, 0.0, t
-
-    # bf16 operands, fp32 accumulation for the batched weight / input gradients (K = T*B steps)
-    hprev = Tensor((TB, H), Buffer(TB * H, F32, base=hs.buffer, offset=0))
-    with _Operands(pool, BF16, dgx, dgh, x, w, hprev) as (pgx, pgh, px, pw, ph):
-        if node.inputs[0].requires_grad:
-            xdt = node.inputs[0].tensor.dtype  # the gradient takes the input's dtype
-            dx = empty_tensor(pool, (TB, E), xdt)
-            _gemm(pgx, 0, H3, pw, 1, E, TB, E, H3, dx.ptr, E, dtype=BF16, out_f32=xdt == F32)  # dx = dgx . W
-            outs[0] = dx
-        if node.inputs[1].requires_grad:
-            ptr, beta, outs[1] = target(1, (H3, E))
-            _gemm(pgx, 1, H3, px, 1, E, H3, E, TB, ptr, E, dtype=BF16, beta=beta)  # dW = dgx^T . x
-        if node.inputs[3].requires_grad:
-            ptr, beta, outs[3] = target(3, (H3, H))
-            _gemm(pgh, 1, H3, ph, 1, H, H3, H, TB, ptr, H, dtype=BF16, beta=beta)  # dU = dgh^T . h_{t-1}
-    if node.inputs[2].requires_grad:
-        ptr, beta, outs[2] = target(2, (H3,))
-        check(lib.nsk_colsum(F32, dgx.ptr, ptr, TB, H3, beta, st))
-    if node.inputs[4].requires_grad:
-        ptr, beta, outs[4] = target(4, (H3,))
-        check(lib.nsk_colsum(F32, dgh.ptr, ptr, TB, H3, beta, st))
     release_tensor(pool, dgx)
     release_tensor(pool, dgh)
     return outs

@@ -352,12 +352,13 @@ class Tensor:
     Extra slots: ``dtype`` (F32 or BF16), ``host_src`` (the host array a data
     tensor was made from, so host-side index checks need no sync), ``shadow``
     (bf16 copy of a float32 parameter read by tensor-core kernels),
-    ``version`` (bumped whenever a parameter's values change) and ``bn_partials``
-    (channel statistics a conv emitted for the BatchNorm that consumes it).
+    ``version`` (bumped whenever a parameter's values change), ``bn_partials``
+    (channel statistics a conv emitted for the BatchNorm that consumes it) and ``bnb_partials`` (on a
+    gradient: the BatchNorm-backward statistics the dgrad that completed it emitted, see layers._r_conv2d).
     """
 
     __slots__ = ("shape", "buffer", "param_name", "node", "grad", "refs", "_scalar", "dtype", "host_src",
-                 "shadow", "shadow_version", "version", "bn_partials", "__weakref__")
+                 "shadow", "shadow_version", "version", "bn_partials", "bnb_partials", "__weakref__")
 
     def __init__(self, shape: tuple[int, ...], buffer: Buffer, param_name: str | None = None):
         numel = 1
@@ -380,6 +381,7 @@ class Tensor:
         self.shadow_version = -1
         self.version = 0
         self.bn_partials = None
+        self.bnb_partials = None  # (gradient tensors) BatchNorm-backward partials a dgrad emitted with it
 
     @property
     def numel(self) -> int:

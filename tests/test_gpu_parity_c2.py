@@ -146,3 +146,64 @@ def test_stem_at_batch_256(session):
     autodiff.backward(tape, session.grad_cache, pool)
     dw_ref = X.conv2d_wgrad(xq, gy, wt.shape, 1, 1)
     assert rel(session.grad_cache.get("w"), dw_ref) < TOL
+
+
+@pytest.mark.parametrize("acc", [False, True], ids=["single", "accumulated"])
+@pytest.mark.parametrize("case", C2_CONVS, ids=_ids)
+def test_bn_backward_fused_into_dgrad_at_batch_256(session, case, acc, monkeypatch):
+    """BatchNorm(+ReLU) -> conv at the bench batch, where the conv's dgrad completes the gradient of the BatchNorm
+    output, so the dgrad epilogue stores it ReLU-masked and emits the BatchNorm-backward channel sums
+    (nsk_conv2d_dgrad_bnstats -> nsk_bn_bwd_partials: no reduction pass). ``accumulated``: the BatchNorm output
+    has a second consumer whose gradient is already pending (the residual pattern), so the epilogue adds it
+    before masking. Checked against the float64 oracle at 1e-3, and against the unfused path (separate
+    reduction kernel) to bf16 rounding."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+    from paper_2409_11600_b200.runtime import Session
+
+    hw, k, co, r, st, pad = case  # the BatchNorm has k channels and feeds the conv k -> co
+    rng = np.random.default_rng(3000 + sum(case) + acc)
+    x = X.round_bf16(rng.standard_normal((B, hw, hw, k)) * 2.0 + 0.3)
+    gb = np.stack([rng.uniform(0.5, 1.5, k), rng.uniform(-0.5, 0.5, k)]).astype(np.float32)
+    wt = (rng.standard_normal((co, r, r, k)) * np.sqrt(2.0 / (k * r * r))).astype(np.float32)
+    p = (hw + 2 * pad - r) // st + 1
+    gy = X.round_bf16(rng.standard_normal((B, p, p, co)))
+    gy2 = X.round_bf16(rng.standard_normal((B, hw, hw, k)))
+
+    def run(fuse):
+        monkeypatch.setattr(layers, "_BNB_FUSE", fuse)
+        s = Session(seed=0)
+        pool = s.pool
+        xt = autodiff.make_param(pool, x, "x", dtype=BF16)
+        gbt = autodiff.make_param(pool, gb, "gb")
+        wp = autodiff.make_param(pool, wt, "w")
+        y = layers.batchnorm(xt, gbt, pool, relu=True)
+        tape = s.tape()
+        terms = []
+        if acc:  # delivered first: the pending gradient the dgrad then accumulates into
+            g2 = autodiff.make_data(pool, gy2, dtype=BF16)
+            autodiff.push_assignment(tape, "t.gy2", g2)
+            terms.append(autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", y, g2, pool), pool))
+        out = layers.conv2d(y, wp, st, pad, pool)
+        g1 = autodiff.make_data(pool, gy, dtype=BF16)
+        autodiff.push_assignment(tape, "t.gy", g1)
+        terms.append(autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", out, g1, pool), pool))
+        loss = terms[0] if len(terms) == 1 else autodiff.rec_sum_loss(
+            autodiff.rec_elementwise("add", terms[0], terms[1], pool), pool)
+        y_d = y.data
+        autodiff.push_assignment(tape, "t.loss", loss)
+        autodiff.backward(tape, s.grad_cache, pool)
+        return y_d, s.grad_cache.get("x").astype(np.float64), s.grad_cache.get("gb").astype(np.float64)
+
+    y_d, dx_f, dgb_f = run(True)
+    _, dx_u, dgb_u = run(False)
+    ref_y, cache = X.batchnorm_fwd(x, gb[0], gb[1], relu=True)
+    assert rel(y_d, X.round_bf16(ref_y)) < TOL
+    g = X.round_bf16(X.conv2d_dgrad(gy, X.round_bf16(wt), y_d.shape, st, pad))
+    if acc:
+        g = X.round_bf16(g.astype(np.float64) + gy2)
+    dxr, dgr, dbr, _ = X.batchnorm_bwd(g, cache, y_out=y_d, relu=True)
+    assert rel(dgb_f, np.stack([dgr, dbr])) < TOL, ("dgamma/dbeta", rel(dgb_f, np.stack([dgr, dbr])))
+    assert rel(dx_f, X.round_bf16(dxr)) < TOL, ("dx", rel(dx_f, X.round_bf16(dxr)))
+    # fused vs the separate reduction kernel: the same sums in another order
+    assert rel(dgb_f, dgb_u) < 1e-4 and rel(dx_f, dx_u) < 1e-3
