@@ -45,6 +45,11 @@ MODELS = {
                  "workload": "ImageNet-shape ResNet-50 v1.5 training step (fwd+bwd+SGD lr 0.1 m 0.9), config C4",
                  "model": "resnet50-v1.5 (25,557,032 params)",
                  "conv": (56, 64, 64, 3, 1, 1)},
+    # C3: sequences, not images (sub-line of the default run; --model gru prints it on its own)
+    "gru": {"tokens": 128, "vocab": 32768, "classes": 2, "batch": 64,
+            "workload": "GRU sequence classifier training step (embedding 32768x512 -> GRU H=512 T=128 -> linear 2, "
+                        "AdamW lr 1e-3 wd 1e-4, clip 5), config C3",
+            "model": "gru-classifier (V=32768, E=H=512, T=128)"},
 }
 
 
@@ -110,7 +115,10 @@ class Clocks:
 def synthetic_batch(seed: int, b: int = BATCH, model: str = "resnet18"):
     spec = MODELS[model]
     rng = np.random.default_rng(seed)
-    x = rng.standard_normal((b,) + spec["image"]).astype(np.float32)
+    if model == "gru":
+        x = rng.integers(0, spec["vocab"], (b, spec["tokens"])).astype(np.float32)
+    else:
+        x = rng.standard_normal((b,) + spec["image"]).astype(np.float32)
     y = rng.integers(0, spec["classes"], b).astype(np.float32)
     return x, y
 
@@ -169,6 +177,10 @@ def reference_arm(args, rank, world):
     no extrapolation), W warm-up + K timed steps on this host's cores; rank 0 only under torchrun."""
     if rank != 0:
         return
+    if args.model == "gru":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference arm is defined for the headline ResNet "
+                          "configs; the GRU composition's CPU cost is in DESIGN.md"}), flush=True)
+        return
     from oracle.refapi import cpu_model
 
     cores = cpu_cores()
@@ -196,10 +208,11 @@ def time_conv_kernel(lib, _lib, conv, iters=20):
     hw, c, k, r, st_, pad = conv
     p = (hw + 2 * pad - r) // st_ + 1
     d = ConvDesc(BATCH, hw, hw, c, k, r, r, st_, pad, p, p)
+    rng = np.random.default_rng(5)  # random operands: constant data understates the tensor pipe's power draw
     x = Buffer(BATCH * hw * hw * c, BF16)
-    x.fill(0.5)
+    x.upload(rng.standard_normal(BATCH * hw * hw * c).astype(np.float32))
     w = Buffer(k * r * r * c, BF16)
-    w.fill(0.01)
+    w.upload((rng.standard_normal(k * r * r * c) / np.sqrt(r * r * c)).astype(np.float32))
     y = Buffer(BATCH * p * p * k, BF16)
     st = _lib.stream()
     for _ in range(3):
@@ -219,6 +232,76 @@ def time_conv_kernel(lib, _lib, conv, iters=20):
     return flops, per_ms
 
 
+class ConvTimer:
+    """layers.KTIMER hook: CUDA events around every conv fprop launch of one geometry inside a training step."""
+
+    def __init__(self, lib, conv):
+        hw, c, k, r, st_, pad = conv
+        self.key = (BATCH, hw, hw, c, k, r, st_, pad)
+        self.lib = lib
+        self.pairs = []
+
+    def match(self, d):
+        return (d.N, d.H, d.W, d.C, d.K, d.R, d.stride, d.pad) == self.key
+
+    def _ev(self, stream):
+        ev = C.c_void_p()
+        self.lib.nsk_event_create(1, C.byref(ev))
+        self.lib.nsk_event_record(ev, stream)
+        return ev
+
+    def begin(self, stream):
+        self.pairs.append([self._ev(stream), None])
+
+    def end(self, stream):
+        self.pairs[-1][1] = self._ev(stream)
+
+    def mean_ms(self):
+        ts = []
+        for a, b in self.pairs:
+            self.lib.nsk_event_sync(b)
+            ms = C.c_float()
+            self.lib.nsk_event_elapsed_ms(a, b, C.byref(ms))
+            ts.append(ms.value)
+        return sum(ts) / len(ts) if ts else None, len(ts)
+
+
+def time_conv_in_step(tr, lib, conv, steps=3):
+    """The dominant conv's launch duration inside real (eager) training steps on the staged batch: events on the
+    compute stream right around each launch, with the rest of the step (side-stream weight gradients included)
+    running as in the bench."""
+    from paper_2409_11600_b200 import _lib, layers
+
+    timer = ConvTimer(lib, conv)
+    layers.KTIMER = timer
+    try:
+        for _ in range(steps):
+            tr._body()
+        _lib.sync()
+    finally:
+        layers.KTIMER = None
+    return timer.mean_ms()
+
+
+def sub_bench(model: str, steps: int, warmup: int):
+    """Another BASELINE config in a child process (own device memory): its JSON line as a dict, or an error."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--model", model, "--steps", str(steps), "--warmup",
+           str(warmup), "--no-sub"]
+    r = None
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        if not lines:
+            return {"error": f"exit {r.returncode}: " + " | ".join(r.stderr.strip().splitlines()[-4:])[:600]}
+        line = lines[-1]
+        d = json.loads(line)
+        keep = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "config", "e2e", "step_tflops_per_gpu",
+                "step_frac_of_peak", "final_loss", "clocks", "gpu_launches", "dtype")
+        return {k: d[k] for k in keep if k in d}
+    except Exception as e:  # noqa: BLE001 -- reported, never fatal for the headline line
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+
+
 def profiled_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "dominant_kernel_traffic.json")
@@ -231,7 +314,7 @@ def profiled_traffic():
 
 def ours_arm(args, rank, world, local_rank):
     from paper_2409_11600_b200 import _lib
-    from paper_2409_11600_b200 import models
+    from paper_2409_11600_b200 import models, nn
     from paper_2409_11600_b200.runtime import Session
     from paper_2409_11600_b200.tensor import Buffer
     from paper_2409_11600_b200.train import Trainer
@@ -241,17 +324,26 @@ def ours_arm(args, rank, world, local_rank):
     st = _lib.stream()
     dp = None
     spec = MODELS[args.model]
+    gru = args.model == "gru"
     s = Session(seed=0)
-    model = models.ResNet18(s) if args.model == "resnet18" else models.ResNet50(s)
-    flops_per_img = (models.resnet18_train_flops_per_image() if args.model == "resnet18"
-                     else models.resnet50_train_flops_per_image())
+    if gru:
+        model = models.GRUClassifier(s)
+        per_unit_flops = models.gru_train_flops_per_seq(spec["tokens"])
+        batch = spec["batch"]
+        opt = ("adamw", nn.Hyperparams(learning_rate=1e-3, weight_decay=1e-4), 5.0)
+    else:
+        model = models.ResNet18(s) if args.model == "resnet18" else models.ResNet50(s)
+        per_unit_flops = (models.resnet18_train_flops_per_image() if args.model == "resnet18"
+                          else models.resnet50_train_flops_per_image())
+        batch = BATCH
+        opt = ("sgd", 0.1, 0.9)
     if world > 1:
         from paper_2409_11600_b200.dp import DataParallel
 
         dp = DataParallel(s, rank, world)
         dp.broadcast_params()
-    x, y = synthetic_batch(1000 + rank, BATCH, args.model)
-    tr = Trainer(s, model, x.shape, spec["classes"], optimizer=("sgd", 0.1, 0.9), graph=True, warmup=2, dp=dp)
+    x, y = synthetic_batch(1000 + rank, batch, args.model)
+    tr = Trainer(s, model, x.shape, spec["classes"], optimizer=opt, graph=True, warmup=2, dp=dp)
 
     def barrier():
         _lib.sync()
@@ -294,13 +386,13 @@ def ours_arm(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t[0])
     ms_per_step = total_ms / args.steps
-    value = world * BATCH * args.steps / (total_ms / 1000.0)
+    value = world * batch * args.steps / (total_ms / 1000.0)
 
     # e2e through the public call: host batch in (pinned H2D on the copy stream, double-buffered input slots:
     # Trainer.step_async), loss out (async D2H into pinned host memory) every step
     from paper_2409_11600_b200.train import PinnedArray
 
-    xs = [x, synthetic_batch(2000 + rank, BATCH, args.model)[0]]
+    xs = [x, synthetic_batch(2000 + rank, batch, args.model)[0]]
     losses = PinnedArray((args.steps,))
     for i in range(2):  # capture the second input slot's graph outside the timed region
         tr.step_async(xs[i % 2], y)
@@ -312,33 +404,61 @@ def ours_arm(args, rank, world, local_rank):
     barrier()
     e2e_s = time.perf_counter() - t0
     loss = float(losses.array[-1])
-    e2e = world * BATCH * args.steps / e2e_s
+    e2e = world * batch * args.steps / e2e_s
 
     if rank != 0:
         return
     pk_burst, pk_sus, hbm, src = peaks()
-    flops, kms = time_conv_kernel(lib, _lib, spec["conv"])
-    achieved = flops / (kms / 1000.0) / 1e12
-    step_tflops = value * flops_per_img / 1e12 / world
+    unit = "sequences/s" if gru else "images/s"
+    step_tflops = value * per_unit_flops / 1e12 / world
+    cfg = bench_config(args.model, world) if not gru else {
+        "workload": spec["workload"], "model": spec["model"], "global_batch": batch * world, "per_gpu_batch": batch,
+        "seq_len": spec["tokens"], "parallelism": f"dp{world}",
+        "l2": "GPU arm: flushed between timed steps (256 MiB write outside the step events)"}
     line = {
-        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world, "steps": args.steps,
+        "metric": (METRIC if not gru else "train sequences/sec, GRU classifier H=512 T=128 (config C3)"),
+        "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (N(0,1) images, uniform labels, random init)",
-        "config": bench_config(args.model, world),
+        "vs_baseline": None, "dtype": "bf16",
+        "data": ("synthetic (uniform token ids, uniform labels, random init)" if gru
+                 else "synthetic (N(0,1) images, uniform labels, random init)"),
+        "config": cfg,
         "final_loss": loss,
-        "e2e": {"value": e2e, "unit": "images/s", "h2d_bytes_per_step": int(x.nbytes + y.nbytes),
+        "e2e": {"value": e2e, "unit": unit, "h2d_bytes_per_step": int(x.nbytes + y.nbytes),
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(tr.launches_per_step * args.steps),
         "step_tflops_per_gpu": step_tflops,
         "step_frac_of_peak": step_tflops / pk_sus,
-        "roofline": {"bound": "tensor",
-                     "kernel": "umma_kernel conv2d fprop {3}x{3} {1}->{2} s{4}, 256x{0}x{0}".format(*spec["conv"]),
-                     "achieved": achieved, "peak": pk_burst, "unit": "TFLOP/s", "frac": achieved / pk_burst,
-                     "traffic": profiled_traffic() if args.model == "resnet18" else None, "peak_source": f"{src} bf16_tflops (burst, kernel timed alone)",
-                     "algorithmic_flops_per_launch": flops, "launch_ms": kms},
         "clocks": clk.summary(),
     }
-    if world == 1:
+    if not gru:
+        # dominant tensor-core kernel: the heaviest conv geometry's fprop, (1) inside real training steps (eager
+        # replay of the step on the staged batch; CUDA events on the compute stream around each launch) against the
+        # sustained peak, (2) alone, back to back, random operands, against the burst peak
+        flops, kms_alone = time_conv_kernel(lib, _lib, spec["conv"])
+        kms_step, nlaunch = time_conv_in_step(tr, lib, spec["conv"]) if world == 1 else (None, 0)
+        hw_, c_, k_, r_, st_, _pd = spec["conv"]
+        name = f"umma_kernel conv2d fprop {r_}x{r_} {c_}->{k_} s{st_}, {BATCH}x{hw_}x{hw_}"
+        if kms_step:
+            achieved = flops / (kms_step / 1000.0) / 1e12
+            line["roofline"] = {
+                "bound": "tensor", "kernel": name, "achieved": achieved, "peak": pk_sus, "unit": "TFLOP/s",
+                "frac": achieved / pk_sus, "traffic": profiled_traffic() if args.model == "resnet18" else None,
+                "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside the training step)",
+                "algorithmic_flops_per_launch": flops, "launch_ms": kms_step,
+                "timing": f"mean of {nlaunch} launches inside 3 eager training steps (CUDA events on the compute "
+                          "stream around each launch; random-init weights, N(0,1) images)",
+                "alone": {"launch_ms": kms_alone, "achieved": flops / (kms_alone / 1000.0) / 1e12, "peak": pk_burst,
+                          "frac": flops / (kms_alone / 1000.0) / 1e12 / pk_burst,
+                          "timing": "20 back-to-back launches, random bf16 operands, burst peak"}}
+        else:
+            achieved = flops / (kms_alone / 1000.0) / 1e12
+            line["roofline"] = {
+                "bound": "tensor", "kernel": name, "achieved": achieved, "peak": pk_burst, "unit": "TFLOP/s",
+                "frac": achieved / pk_burst, "traffic": profiled_traffic() if args.model == "resnet18" else None,
+                "peak_source": f"{src} bf16_tflops (burst, kernel timed alone, random operands)",
+                "algorithmic_flops_per_launch": flops, "launch_ms": kms_alone}
+    if world == 1 and not gru:
         from oracle.refapi import cpu_model
 
         sample = 64 if args.model == "resnet18" else 2
@@ -347,6 +467,9 @@ def ours_arm(args, rank, world, local_rank):
                                 "cpu_model": cpu_model(),
                                 "sample": f"{sample} images/step x {len(times)} timed steps (1 warm-up) of the "
                                           f"B={BATCH} workload; {desc}"}
+    if world == 1 and args.model == "resnet18" and not args.no_sub:
+        # the other BASELINE configs measured in the same run, each in its own process (C4, C3)
+        line["other_configs"] = {"C4_resnet50": sub_bench("resnet50", 10, 3), "C3_gru": sub_bench("gru", 20, 3)}
     print(json.dumps(line), flush=True)
 
 
@@ -357,6 +480,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="resnet18", choices=sorted(MODELS))
+    ap.add_argument("--no-sub", action="store_true", help="skip the C3/C4 sub-runs of the default ResNet-18 line")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

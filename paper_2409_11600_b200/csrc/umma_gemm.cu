@@ -139,8 +139,7 @@ __device__ __forceinline__ uint4 bf16x8_axpby(uint4 old, float beta, uint4 v) {
   return r;
 }
 
-// named barriers: one per epilogue warpgroup (ids 1, 2; 128 threads), one over all epilogue warps (id 3)
-__device__ __forceinline__ void epi_bar(int group) { asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory"); }
+// named barrier over all epilogue warps (id 3)
 __device__ __forceinline__ void epi_bar_all(int threads) { asm volatile("bar.sync 3, %0;" ::"r"(threads) : "memory"); }
 // MMA gate: the gate warp waits on the mbarriers and releases the MMA warp through named barriers 4..4+STAGES-1
 // (stage s full) and 8, 9 (accumulator a drained), 64 threads each (gate warp arrives, MMA warp syncs)
@@ -231,11 +230,13 @@ __device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
 // overlap the MMAs of unit j+1.
 // EPI epilogue warps (4 or 8): with 8, two warpgroups take alternate 32-column chunks of each tile, doubling the
 // TMEM-drain / store parallelism for the wide (BN = 256) tiles whose epilogue is the bottleneck.
-// BST: the output is the gradient of a BatchNorm's output (dgrad feeding nsk_bn_bwd_partials): the epilogue
-// masks it with the BatchNorm's ReLU bits, adds the pending gradient (bacc) and emits per-CTA column sums of dz and
-// dz * x (p.bx = the BatchNorm input) into p.stats -- a separate instantiation, so the other passes keep their
-// register budget
-template <int BN, int ESZ, int STAGES, bool RR, int EPI, bool WRES, bool BST>
+// STATS (separate instantiations, so the passes without statistics keep their register budget):
+//   1: conv fprop feeding a BatchNorm -- per-CTA column sums of y and y^2 of the stored bf16 outputs into p.stats
+//   2: dgrad producing the gradient of a BatchNorm's output (feeding nsk_bn_bwd_partials) -- the epilogue masks it
+//      with the BatchNorm's ReLU bits, adds the pending gradient (bacc) and sums dz and dz * x (p.bx = BN input)
+// Column sums are warp butterflies over the thread-per-row registers into per-warp accumulators: no shared-memory
+// traffic beside the MMAs' operand reads (the 64-channel convs are shared-memory bound) and no per-chunk barrier.
+template <int BN, int ESZ, int STAGES, bool RR, int EPI, bool WRES, int STATS>
 __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::template threads<EPI>(),
                                   Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::kTwoPerSM ? 2 : 1)
     umma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -568,13 +569,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     const int eg = (warp - 4) >> 2;  // epilogue warpgroup: chunks eg, eg + EPI/4, ...
     const int r = q * 32 + lane;  // tile row == TMEM lane
     const bool vec_ok = ((p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0);
-    float* st_acc = (float*)(stage_base + EPI * S::NSTG * kStgBytes);  // [2][N] CTA channel sums (stats mode)
     int sbuf = 0;  // staging double buffer (TMA stores of the previous chunk may still be reading the other)
-    float* st_red = st_acc + 2 * p.N + eg * 256;                // per warpgroup: [4 warps][2][32]
-    if (p.stats && !BST) {
-      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) st_acc[i] = 0.f;
-      epi_bar_all(32 * EPI);
-    }
     // output element offset of this thread's row of unit w
     auto row_of = [&](const Unit& w) -> long long {
       const int m = w.m0 + r;
@@ -597,12 +592,12 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       const int n = (p.N - w.n0 + 31) / 32;
       return n > BN / 32 ? BN / 32 : n;
     };
-    // BatchNorm-backward statistics (BST): per-warp column sums of dz and dz * x, [EPI warps][2][N / G] floats
-    // (G = EPI / 4 warpgroups; warp (q, eg) owns the 32-column chunks gc = eg mod G of the output)
+    // statistics (STATS): per-warp column sums, [EPI warps][2][N / G] floats (G = EPI / 4 warpgroups; warp (q, eg)
+    // owns the 32-column chunks gc = eg mod G of the output)
     constexpr int G = EPI / 4;
     float* st_col = (float*)(stage_base + EPI * S::NSTG * kStgBytes);
     const int ncol_w = (p.N / 32 + G - 1) / G * 32;  // columns per warp
-    if constexpr (BST) {
+    if constexpr (STATS != 0) {
       for (int i = lane; i < 2 * ncol_w; i += 32) st_col[(warp - 4) * 2 * ncol_w + i] = 0.f;
       __syncwarp();
     }
@@ -620,9 +615,9 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       for (int c = eg; c < nchunks; c += EPI / 4) {
         uint32_t v[32];
         if (p.probe & 32) continue;  // diagnostics: accumulator never read
-        // BST: this row's ReLU-mask word, requested before the TMEM load
+        // STATS 2: this row's ReLU-mask word, requested before the TMEM load
         uint32_t bmw = 0xffffffffu;
-        if constexpr (BST) {
+        if constexpr (STATS == 2) {
           if (row_ok && p.bmask) bmw = __ldg((const uint32_t*)(p.bmask + ((row_off + w.n0 + c * 32) >> 3)));
         }
         if (w.nk > 0) {
@@ -687,7 +682,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             u4[t].z = pack_bf16x2(f[8 * t + 4], f[8 * t + 5]);
             u4[t].w = pack_bf16x2(f[8 * t + 6], f[8 * t + 7]);
           }
-          if constexpr (BST) {
+          if constexpr (STATS == 2) {
             // dz = [y > 0] * bf16(pending + bf16(dgrad)) -- the pending gradient added as the TMA reduce-add / axpby
             // accumulation paths add it; masking commutes with the rounding
             const uint4* o4 = (const uint4*)((const __nv_bfloat16*)p.out + row_off + col0);
@@ -710,40 +705,9 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
           for (int c4 = 0; c4 < 4; ++c4) *(uint4*)(stg + stg_off(lane, c4)) = u4[c4];
           if (p.tma_store) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if constexpr (BST) {
-            // column sums over this warp's 32 rows (thread = row) by a butterfly reduce-scatter: lane ends with column
-            // col0 + lane; no shared-memory traffic beside the MMAs' operand reads, no cross-warp barrier per chunk
-            float red[32];
-            const uint4* x4 = (const uint4*)(p.bx + row_off + col0);
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {  // dz * x
-              const uint4 xv = row_ok ? __ldg(x4 + c4) : make_uint4(0u, 0u, 0u, 0u);
-              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
-              const __nv_bfloat162* hx = (const __nv_bfloat162*)&xv;
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 z = __bfloat1622float2(hz[i]), xx = __bfloat1622float2(hx[i]);
-                red[8 * c4 + 2 * i] = z.x * xx.x;
-                red[8 * c4 + 2 * i + 1] = z.y * xx.y;
-              }
-            }
-            const float s2 = warp_colsum32(red, lane);
-#pragma unroll
-            for (int c4 = 0; c4 < 4; ++c4) {  // dz
-              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const float2 z = __bfloat1622float2(hz[i]);
-                red[8 * c4 + 2 * i] = z.x;
-                red[8 * c4 + 2 * i + 1] = z.y;
-              }
-            }
-            const float s1 = warp_colsum32(red, lane);
-            float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
-            col[0] += s1;
-            col[ncol_w] += s2;
-          } else if (p.stats) {
-            // column sums of the staged (bf16-rounded) tile: lane = column, rows of this warp
+          if constexpr (STATS == 1) {
+            // column sums of the staged (bf16-rounded) tile: lane = column, this warp's 32 rows, into the warp's own
+            // accumulators (no cross-warp barrier per chunk)
             const unsigned okm = __ballot_sync(0xffffffffu, row_ok);
             float s1 = 0.f, s2 = 0.f;
 #pragma unroll 8
@@ -755,15 +719,41 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
                 s2 += v * v;
               }
             }
-            st_red[q * 64 + lane] = s1;
-            st_red[q * 64 + 32 + lane] = s2;
-            epi_bar(eg);
-            if (q == 0) {  // fixed warp order: deterministic
-              st_acc[col0 + lane] += (st_red[lane] + st_red[64 + lane]) + (st_red[128 + lane] + st_red[192 + lane]);
-              st_acc[p.N + col0 + lane] +=
-                  (st_red[32 + lane] + st_red[96 + lane]) + (st_red[160 + lane] + st_red[224 + lane]);
+            float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
+            col[0] += s1;
+            col[ncol_w] += s2;
+          } else if constexpr (STATS == 2) {
+            // column sums over this warp's 32 rows (thread = row) by a butterfly reduce-scatter: lane ends with column
+            // col0 + lane (the BatchNorm input is read per row straight from global memory)
+            float red[32];
+            const uint4* x4 = (const uint4*)(p.bx + row_off + col0);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
+              const uint4 xv = row_ok ? __ldg(x4 + c4) : make_uint4(0u, 0u, 0u, 0u);
+              const __nv_bfloat162* hx = (const __nv_bfloat162*)&xv;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 z = __bfloat1622float2(hz[i]), xx = __bfloat1622float2(hx[i]);
+                red[8 * c4 + 2 * i] = z.x * xx.x;
+                red[8 * c4 + 2 * i + 1] = z.y * xx.y;
+              }
             }
-            epi_bar(eg);
+            const float s2 = warp_colsum32(red, lane);
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const __nv_bfloat162* hz = (const __nv_bfloat162*)&u4[c4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float2 z = __bfloat1622float2(hz[i]);
+                red[8 * c4 + 2 * i] = row_ok ? z.x : 0.f;
+                red[8 * c4 + 2 * i + 1] = row_ok ? z.y : 0.f;
+              }
+            }
+            const float s1 = warp_colsum32(red, lane);
+            float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
+            col[0] += s1;
+            col[ncol_w] += s2;
           }
           if (p.tma_store) {
             if (lane == 0) {
@@ -808,7 +798,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (p.tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    if constexpr (BST) {
+    if constexpr (STATS != 0) {
       // CTA partials [2][N]: the four lane-quarter warps of the owning warpgroup, in fixed order
       epi_bar_all(32 * EPI);
       float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
@@ -820,10 +810,6 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         for (int qq = 0; qq < 4; ++qq) t += st_col[(e * 4 + qq) * 2 * ncol_w + k * ncol_w + li];
         out[i] = t;
       }
-    } else if (p.stats) {
-      epi_bar_all(32 * EPI);
-      float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
-      for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) out[i] = st_acc[i];
     }
   }
   __syncthreads();
@@ -1332,20 +1318,18 @@ int g_wgrad_grid_cap = 0;  // CTAs per wgrad launch (0: two per SM as usual)
 
 // dynamic shared memory past Smem::TOTAL: statistics accumulators [2][N] + per-warpgroup reduction slots, and
 // for the BatchNorm-backward statistics a staging block of the BatchNorm input per epilogue warp
+// dynamic shared memory past Smem::TOTAL: the statistics' per-warp column sums [epi warps][2][columns per warp]
 int epi_extra_smem(const UmmaProb& p, int epi) {
   if (!p.stats) return 0;
-  if (p.bx) {  // BatchNorm-backward column sums: [epi warps][2][columns per warp]
-    const int g = epi / 4;
-    return epi * 2 * ((p.N / 32 + g - 1) / g * 32) * (int)sizeof(float);
-  }
-  return (2 * p.N + epi * 64) * (int)sizeof(float);
+  const int g = epi / 4;
+  return epi * 2 * ((p.N / 32 + g - 1) / g * 32) * (int)sizeof(float);
 }
 
-template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false, bool BST = false>
+template <int BN, int ESZ, int STAGES, bool RR = false, int EPI = 4, bool WRES = false, int STATS = 0>
 int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, UmmaProb p, cudaStream_t st,
                 int* grid_out) {
   using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
-  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES, BST>;
+  auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES, STATS>;
   const int smem = S::TOTAL + epi_extra_smem(p, EPI);
   if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
   static int configured = 0;
@@ -1369,7 +1353,7 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
   return NSK_OK;
 }
 
-template <int ESZ, bool BST = false>
+template <int ESZ, int STATS = 0>
 int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
                 cudaStream_t st, int* grid_out = nullptr, const CUtensorMap* cmap = nullptr) {
   static CUtensorMap dummy{};
@@ -1384,28 +1368,28 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
         case 64: {
           // one 64-channel chunk, N = 64, 3x3 in strided tap boxes: keep all 9 taps resident (the ring then
           // moves only A; re-fetching the 72 KB filter per tile was half the L2->smem traffic)
-          if (p.wres && nt == 1 && nz == 1) return launch_umma<64, 2, 4, true, 8, true, BST>(a, b, c, p, st, grid_out);
+          if (p.wres && nt == 1 && nz == 1) return launch_umma<64, 2, 4, true, 8, true, STATS>(a, b, c, p, st, grid_out);
           if (p.wres) return nsk::set_error(NSK_ERR_UNSUPPORTED, "weight-resident conv needs a single 64-wide tile");
-          return launch_umma<64, 2, 2, true, 4, false, BST>(a, b, c, p, st, grid_out);
+          return launch_umma<64, 2, 2, true, 4, false, STATS>(a, b, c, p, st, grid_out);
         }
         case 128:
-          return launch_umma<128, 2, 2, true, 4, false, BST>(a, b, c, p, st, grid_out);
+          return launch_umma<128, 2, 2, true, 4, false, STATS>(a, b, c, p, st, grid_out);
       }
     }
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "row-reuse conv needs bf16 and N <= 128");
   }
   switch (BN) {  // ~192 KB of smem ring per CTA, one persistent CTA per SM
     case 64:
-      return launch_umma<64, ESZ, 4, false, 4, false, BST>(a, b, c, p, st, grid_out);
+      return launch_umma<64, ESZ, 4, false, 4, false, STATS>(a, b, c, p, st, grid_out);
     case 128:
-      return launch_umma<128, ESZ, 3, false, 4, false, BST>(a, b, c, p, st, grid_out);
+      return launch_umma<128, ESZ, 3, false, 4, false, STATS>(a, b, c, p, st, grid_out);
     case 256: {
       // 8 epilogue warps unless the statistics buffers would not fit beside them
       using S8 = Smem<256, ESZ, 4, false, 8>;
       const int need = S8::TOTAL + epi_extra_smem(p, 8);
       if (need <= 227 * 1024 && !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0'))
-        return launch_umma<256, ESZ, 4, false, 8, false, BST>(a, b, c, p, st, grid_out);
-      return launch_umma<256, ESZ, 4, false, 4, false, BST>(a, b, c, p, st, grid_out);
+        return launch_umma<256, ESZ, 4, false, 8, false, STATS>(a, b, c, p, st, grid_out);
+      return launch_umma<256, ESZ, 4, false, 4, false, STATS>(a, b, c, p, st, grid_out);
     }
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
@@ -1800,6 +1784,9 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   CUtensorMap mc;
   const bool ts = !y_f32 && out_map(&mc, y, p.M, d->K, d->K);
   p.tma_store = ts;
+  if (stats)
+    return dispatch_bn<2, 1>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream, nparts,
+                             ts ? &mc : nullptr);
   return dispatch_bn<2>(BN, ma, mb, p, (p.M + 127) / 128, (d->K + BN - 1) / BN, 1, (cudaStream_t)stream, nparts,
                         ts ? &mc : nullptr);
 }
@@ -1972,7 +1959,7 @@ int conv_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, fl
     if (ts) p.beta = 0.f;  // the accumulation (if any) happens in the TMA reduce
   }
   if (bx) {
-    rc = dispatch_bn<2, true>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run,
+    rc = dispatch_bn<2, 2>(BN, ma, mb, p, (p.M + 127) / 128, (d->C + BN - 1) / BN, ncls_run,
                               (cudaStream_t)stream, nparts, ts ? &mc : nullptr);
     if (rc != NSK_ERR_UNSUPPORTED) return rc;
     // the statistics buffers do not fit beside this tile configuration: plain (accumulating) dgrad, no partials --

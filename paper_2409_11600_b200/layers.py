@@ -70,6 +70,11 @@ def _temp_bf16(t: Tensor, pool: Pool) -> tuple[int, Tensor | None]:
 
 # --- conv2d ---------------------------------------------------------------------------------
 
+# Measurement hook (bench.py): an object with match(desc) / begin(stream) / end(stream) that brackets the matching
+# conv fprop launches with CUDA events, so a kernel's duration is taken inside a real training step
+KTIMER = None
+
+
 def conv_out(h: int, k: int, stride: int, pad: int) -> int:
     return (h + 2 * pad - k) // stride + 1
 
@@ -104,6 +109,9 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str 
     xp, xtmp = (x.ptr, None) if nchw else _temp_bf16(x, pool)
     wp = w.bf16_ptr() if w.dtype == F32 else w.ptr
     if c % 64 == 0 and not nchw:
+        timer = KTIMER if KTIMER is not None and KTIMER.match(desc) else None
+        if timer is not None:
+            timer.begin(st)
         if bn_stats:
             # per-CTA channel partials for the BatchNorm consuming y (released by batchnorm)
             parts = empty_tensor(pool, (2 * _lib.ctx.sm_count, 2, k))
@@ -113,6 +121,8 @@ def conv2d(x: Tensor, w: Tensor, stride: int, pad: int, pool: Pool, layout: str 
             y.bn_partials = (parts, nparts.value)
         else:
             check(lib.nsk_conv2d_fprop(C.byref(desc), xp, wp, y.ptr, 0, st))
+        if timer is not None:
+            timer.end(st)
         saved = (x, w)
         attrs = {"desc": desc, "stem": False}
         if xtmp is not None:
