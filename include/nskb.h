@@ -67,6 +67,9 @@ int nsk_event_record(void* e, void* stream);
 int nsk_event_wait(void* stream, void* e);
 int nsk_event_sync(void* e);
 int nsk_event_elapsed_ms(void* start, void* stop, float* ms);
+/* measurement utility: occupies `stream` for ns nanoseconds of device time (bench.py enqueues a whole eager step
+ * behind it so in-step event brackets contain no host launch gaps) */
+int nsk_spin(uint64_t ns, void* stream);
 int nsk_graph_begin(void* stream);
 int nsk_graph_end(void* stream, void** exec_out, uint64_t* num_nodes);
 int nsk_graph_launch(void* exec, void* stream);

@@ -258,7 +258,26 @@ static Arena& arena() {
 
 using namespace nsk;
 
+namespace {
+// holds the stream for ns nanoseconds of device time (measurement: lets the host enqueue a whole eager step so its
+// kernels then run back to back, without host launch gaps inside event brackets)
+__global__ void spin_kernel(unsigned long long ns) {
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
+}  // namespace
+
 extern "C" {
+
+int nsk_spin(uint64_t ns, void* stream) {
+  spin_kernel<<<1, 32, 0, (cudaStream_t)stream>>>((unsigned long long)ns);
+  NSK_CUDA(cudaGetLastError());
+  return NSK_OK;
+}
 
 const char* nsk_last_error(void) { return g_last_error.c_str(); }
 

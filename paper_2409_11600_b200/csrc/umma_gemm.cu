@@ -87,6 +87,7 @@ struct UmmaProb {
   const __nv_bfloat16* bx;
   const uint8_t* bmask;
   int bacc;
+  int stats_shared;  // STATS 1 with wide N: one [2][N] CTA accumulator combined per chunk (per-warp ones do not fit)
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
@@ -139,7 +140,10 @@ __device__ __forceinline__ uint4 bf16x8_axpby(uint4 old, float beta, uint4 v) {
   return r;
 }
 
-// named barrier over all epilogue warps (id 3)
+// named barriers: one per epilogue warpgroup (ids 1, 2; 128 threads), one over all epilogue warps (id 3)
+__device__ __forceinline__ void epi_bar_group(int group) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + group) : "memory");
+}
 __device__ __forceinline__ void epi_bar_all(int threads) { asm volatile("bar.sync 3, %0;" ::"r"(threads) : "memory"); }
 // MMA gate: the gate warp waits on the mbarriers and releases the MMA warp through named barriers 4..4+STAGES-1
 // (stage s full) and 8, 9 (accumulator a drained), 64 threads each (gate warp arrives, MMA warp syncs)
@@ -598,8 +602,13 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     float* st_col = (float*)(stage_base + EPI * S::NSTG * kStgBytes);
     const int ncol_w = (p.N / 32 + G - 1) / G * 32;  // columns per warp
     if constexpr (STATS != 0) {
-      for (int i = lane; i < 2 * ncol_w; i += 32) st_col[(warp - 4) * 2 * ncol_w + i] = 0.f;
-      __syncwarp();
+      if (p.stats_shared) {
+        for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) st_col[i] = 0.f;
+        epi_bar_all(32 * EPI);
+      } else {
+        for (int i = lane; i < 2 * ncol_w; i += 32) st_col[(warp - 4) * 2 * ncol_w + i] = 0.f;
+        __syncwarp();
+      }
     }
     int j = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
@@ -719,9 +728,23 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
                 s2 += v * v;
               }
             }
-            float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
-            col[0] += s1;
-            col[ncol_w] += s2;
+            if (p.stats_shared) {
+              // [2][N] CTA accumulator: the four lane-quarter warps of this warpgroup combine in fixed order
+              float* st_red = st_col + 2 * p.N + eg * 256;  // per warpgroup: [4 warps][2][32]
+              st_red[q * 64 + lane] = s1;
+              st_red[q * 64 + 32 + lane] = s2;
+              epi_bar_group(eg);
+              if (q == 0) {
+                st_col[col0 + lane] += (st_red[lane] + st_red[64 + lane]) + (st_red[128 + lane] + st_red[192 + lane]);
+                st_col[p.N + col0 + lane] +=
+                    (st_red[32 + lane] + st_red[96 + lane]) + (st_red[160 + lane] + st_red[224 + lane]);
+              }
+              epi_bar_group(eg);
+            } else {
+              float* col = st_col + (warp - 4) * 2 * ncol_w + (col0 / 32 / G) * 32 + lane;
+              col[0] += s1;
+              col[ncol_w] += s2;
+            }
           } else if constexpr (STATS == 2) {
             // column sums over this warp's 32 rows (thread = row) by a butterfly reduce-scatter: lane ends with column
             // col0 + lane (the BatchNorm input is read per row straight from global memory)
@@ -803,6 +826,10 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       epi_bar_all(32 * EPI);
       float* out = p.stats + (size_t)blockIdx.x * 2 * p.N;
       for (int i = threadIdx.x - 128; i < 2 * p.N; i += 32 * EPI) {
+        if (p.stats_shared) {
+          out[i] = st_col[i];
+          continue;
+        }
         const int k = i / p.N, n = i - k * p.N;
         const int gc = n / 32, e = gc % G, li = (gc / G) * 32 + (n & 31);
         float t = 0.f;
@@ -1318,9 +1345,11 @@ int g_wgrad_grid_cap = 0;  // CTAs per wgrad launch (0: two per SM as usual)
 
 // dynamic shared memory past Smem::TOTAL: statistics accumulators [2][N] + per-warpgroup reduction slots, and
 // for the BatchNorm-backward statistics a staging block of the BatchNorm input per epilogue warp
-// dynamic shared memory past Smem::TOTAL: the statistics' per-warp column sums [epi warps][2][columns per warp]
+// dynamic shared memory past Smem::TOTAL: the statistics' per-warp column sums [epi warps][2][columns per warp], or
+// with stats_shared one [2][N] CTA accumulator + per-warpgroup combine slots [4][2][32]
 int epi_extra_smem(const UmmaProb& p, int epi) {
   if (!p.stats) return 0;
+  if (p.stats_shared) return (2 * p.N + epi * 64) * (int)sizeof(float);
   const int g = epi / 4;
   return epi * 2 * ((p.N / 32 + g - 1) / g * 32) * (int)sizeof(float);
 }
@@ -1779,6 +1808,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
       return nsk::set_error(NSK_ERR_SHAPE, "conv2d fprop: statistics buffer smaller than 2*SMs x 2 x K floats");
     p.stats = stats;
     p.fold_reset = nsk::bn_fold_counter_fwd((cudaStream_t)stream);
+    p.stats_shared = 32 * d->K > 8192;  // per-warp accumulators cost 32 B per channel: wide layers share one
   }
   if (splits > 1) return conv_split_run(p, ma, mb, splits, fsteps, y, 0.f, stats, nparts, (cudaStream_t)stream);
   CUtensorMap mc;

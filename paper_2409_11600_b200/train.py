@@ -298,6 +298,8 @@ class Trainer:
         captured graph; the returned loss is still a device scalar (read it when needed)."""
         if len(self._slots) < 2:
             self._slots.append(_InputSlot(self.x_shape, self.augment))
+            if self.input_classes is not None:  # token ids validated on the host at staging (as for slot 0)
+                self._slots[1].x_dev.host_src = self._slots[1].x_pin.array
             s = C.c_void_p()
             check(_lib.lib().nsk_stream_create(C.byref(s)))
             self._copy_stream = s.value

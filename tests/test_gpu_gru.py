@@ -70,3 +70,31 @@ def test_gru_trainer_graph_replay_with_adamw_clip(dev):
         if mode:
             assert tr.graph is not None
     np.testing.assert_allclose(losses[True], losses[False], rtol=1e-5)
+
+
+def test_gru_step_async_matches_step(dev):
+    """Token models through Trainer.step_async (two input slots, copy stream, two captured graphs): the second slot's
+    token ids are range-checked on the host at staging like the first (no device check inside a capture); losses
+    equal Trainer.step's."""
+    from paper_2409_11600_b200 import nn
+    from paper_2409_11600_b200.models import GRUClassifier
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    rng = np.random.default_rng(21)
+    V, B, T = 1000, 16, 12
+    xs = [rng.integers(0, V, (B, T)).astype(np.float32) for _ in range(6)]
+    ys = [rng.integers(0, 2, B).astype(np.float32) for _ in range(6)]
+    out = {}
+    for mode in ("step", "async"):
+        s = Session(seed=0)
+        opt = ("adamw", nn.Hyperparams(learning_rate=1e-3, weight_decay=1e-4), 5.0)
+        tr = Trainer(s, GRUClassifier(s, vocab=V, embed=128, hidden=128), (B, T), 2, optimizer=opt, graph=True,
+                     warmup=2)
+        fn = tr.step if mode == "step" else tr.step_async
+        out[mode] = [float(fn(x, y)) for x, y in zip(xs, ys)]
+    np.testing.assert_allclose(out["async"], out["step"], rtol=1e-5)
+    bad = xs[0].copy()
+    bad[3, 4] = V  # out of range: the reference's onehot message, raised at staging
+    with pytest.raises(Exception, match="onehot index"):
+        tr.step_async(bad, ys[0])

@@ -3,12 +3,15 @@
     python tools/conv_table.py [resnet18|resnet50] [batch]
 
 Prints one line per (shape, pass): count in the model, us per launch, TFLOP/s, and the model-weighted
-total, so the dominant passes are obvious. Not a bench number (kernels timed back to back, warm L2).
+total, so the dominant passes are obvious. Not a bench number (kernels timed back to back, warm L2). Random
+operands (CONST=1: the constant ones earlier tables used, which flatter the tensor pipe).
 """
 import collections
 import ctypes as C
 import os
 import sys
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -64,15 +67,21 @@ def main():
     grand = 0.0
     gflop = 0.0
     rows = []
+    rng = np.random.default_rng(0)
     for (n, hw, c, k, r, s, pad), cnt in sorted(convs.items()):
         p = (hw + 2 * pad - r) // s + 1
         d = ConvDesc(n, hw, hw, c, k, r, r, s, pad, p, p)
         x = Buffer(n * hw * hw * c, BF16)
-        x.fill(0.25)
         w = Buffer(k * r * r * c, BF16)
-        w.fill(0.01)
         y = Buffer(n * p * p * k, BF16)
-        y.fill(0.5)
+        if os.environ.get("CONST") == "1":  # constant operands (understate the tensor pipe's power draw)
+            x.fill(0.25)
+            w.fill(0.01)
+            y.fill(0.5)
+        else:
+            x.upload(rng.standard_normal(x.capacity).astype(np.float32))
+            w.upload((rng.standard_normal(w.capacity) / np.sqrt(r * r * c)).astype(np.float32))
+            y.upload(rng.standard_normal(y.capacity).astype(np.float32))
         dw = Buffer(k * r * r * c, F32)
         ws_b = lib.nsk_conv2d_wgrad_workspace(C.byref(d))
         ws = Buffer(ws_b // 4 + 1, F32)
