@@ -567,3 +567,50 @@ def test_conv_split_k_matches_unsplit(dev, case, monkeypatch):
     assert rel(ys, yu) < 1e-3 and rel(ss, su) < 1e-3
     assert rel(ds, X.round_bf16(X.conv2d_dgrad(yu.astype(np.float32), wt, x.shape, st, pad))) < 1e-3
     assert rel(ds, du) < 1e-3
+
+
+@pytest.mark.parametrize("case", [(2, 3, 40, 40, 7, 2, 3), (3, 3, 32, 32, 3, 1, 1), (2, 3, 17, 23, 5, 2, 2)])
+def test_im2col_nchw_matches_oracle(dev, case):
+    """The image stem's fused layout change + im2col (NCHW float32 -> [N*P*Q, Kp] bf16, K = R*S*C zero-padded to a
+    multiple of 8), row-tiled through shared memory: bit-exact against the oracle's im2col of the NHWC image, the
+    padding columns zero."""
+    import ctypes as C
+
+    from paper_2409_11600_b200 import _lib
+    from paper_2409_11600_b200._lib import BF16, F32
+    from paper_2409_11600_b200.tensor import Buffer
+
+    n, c, h, w, r, st, pad = case
+    p, q = (h + 2 * pad - r) // st + 1, (w + 2 * pad - r) // st + 1
+    kp = (r * r * c + 7) // 8 * 8
+    rng = np.random.default_rng(sum(case))
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    xb, ob = Buffer(x.size, F32), Buffer(n * p * q * kp, BF16)
+    xb.upload(x)
+    lib = _lib.lib()
+    _lib.check(lib.nsk_im2col_nchw(xb.ptr, ob.ptr, n, c, h, w, r, r, st, pad, p, q, kp, _lib.stream()))
+    got = ob.host().reshape(n * p * q, kp)
+    ref = X.round_bf16(X.im2col(x.transpose(0, 2, 3, 1), r, r, st, pad)).astype(np.float32)
+    np.testing.assert_array_equal(got[:, : r * r * c], ref)
+    assert not np.any(got[:, r * r * c:])
+
+
+@pytest.mark.parametrize("k,st,pad", [(3, 2, 1), (2, 2, 0), (3, 1, 1)])
+def test_maxpool_window_variants(session, k, st, pad):
+    """Max-pool forward (bit-exact, first-maximum ties) and backward for the compile-time 3x3/2 kernels and the
+    runtime-window fallback."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16
+
+    rng = np.random.default_rng(k * 10 + st)
+    pool = session.pool
+    x = np.maximum(X.round_bf16(rng.standard_normal((3, 9, 11, 16))), 0)  # ReLU'd: many ties
+    xt = autodiff.make_param(pool, x, "x", dtype=BF16)
+    m = layers.maxpool(xt, k, st, pad, pool)
+    np.testing.assert_array_equal(m.data, X.maxpool_fwd(x, k, st, pad).astype(np.float32))
+    gy = X.round_bf16(rng.standard_normal(m.shape))
+    loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", m, autodiff.make_data(pool, gy, dtype=BF16),
+                                                          pool), pool)
+    autodiff.push_assignment(session.tape(), "loss", loss)
+    autodiff.backward(session.tape(), session.grad_cache, pool)
+    assert rel(session.grad_cache.get("x"), X.round_bf16(X.maxpool_bwd(x, gy, k, st, pad))) < 1e-3
