@@ -9,7 +9,9 @@ shuffled per epoch exactly like the reference dataset (dataset.py:93-121 via
 oracle.ref_ops.epoch_permutation / batch_rows), SGD momentum 0.9, per-model (steps, lr, batch, rows) in SETTINGS.
 ``resnet18_c2`` is BASELINE config C2 itself: ResNet-18/CIFAR, batch 256, SGD lr 0.1 momentum 0.9, 100 steps over
 25,600 rows (one epoch: every step sees fresh images, so the loss cannot collapse to memorisation, where a relative
-1% bar would be meaningless).
+1% bar would be meaningless). At lr 0.1 the first ~20 steps are a loss blow-up whose details rounding alone reorders
+(the oracle's own bf16 and float64 runs part there) before it settles near ln 10; ``resnet18_c2_lr002`` is the same
+batch and data at lr 0.02, a trajectory that learns without blowing up.
 Writes tests/golden/trajectory_<model>.npz with the per-step losses of the float64 oracle (bf16=False, the
 reference's own arithmetic) and of the bf16-emulating oracle (bf16=True). The GPU test replays the same
 schedule through the device Trainer.
@@ -37,7 +39,7 @@ MOMENTUM = 0.9
 # lr 0.01), so that golden uses a gentler lr and 30 steps; the small CNN runs the full 100 steps; resnet18_c2
 # is the C2 configuration (batch 256, lr 0.1) for 100 steps.
 SETTINGS = {"smallcnn": (100, 0.01, TRAJ_BATCH, TRAJ_ROWS), "resnet18": (30, 0.002, TRAJ_BATCH, TRAJ_ROWS),
-            "resnet18_c2": (100, 0.1, 256, 25600)}
+            "resnet18_c2": (100, 0.1, 256, 25600), "resnet18_c2_lr002": (100, 0.02, 256, 25600)}
 
 
 def dataset(rows: int = TRAJ_ROWS):
