@@ -78,7 +78,21 @@ __global__ void __launch_bounds__(BT) bn_stats_kernel(const __nv_bfloat16* __res
   const int CV = C / 8;
   const int cv = threadIdx.x % CV, ro = threadIdx.x / CV, RPB = BT / CV;
   float s1[8] = {0}, s2[8] = {0};
-  for (uint64_t r = (uint64_t)blockIdx.x * RPB + ro; r < rows; r += (uint64_t)gridDim.x * RPB) {
+  const uint64_t stride = (uint64_t)gridDim.x * RPB;
+  uint64_t r = (uint64_t)blockIdx.x * RPB + ro;
+  for (; r + 3 * stride < rows; r += 4 * stride) {  // four rows in flight, same order as one at a time
+    float f[4][8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ld8(x + (r + k * stride) * C + cv * 8, f[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        s1[j] += f[k][j];
+        s2[j] += f[k][j] * f[k][j];
+      }
+  }
+  for (; r < rows; r += stride) {
     float f[8];
     ld8(x + r * C + cv * 8, f);
 #pragma unroll
