@@ -431,6 +431,20 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
   }
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
+  // step t's external gradient, saved gates and h_t do not depend on the recurrence: they are loaded during step
+  // t + 1's exchange and MMA phase, so only the partial products stay on the per-step critical path
+  float pdh[8], pr[8], pz[8], pn[8], pa[8], php[8];
+  auto prefetch = [&](int tt) {
+    if (!arow || tt < 0) return;
+    ld8(p.dhs + ((size_t)tt * B + gb) * H + ju, pdh);
+    const float* gs = p.gates + ((size_t)tt * B + gb) * 4 * H + ju;
+    ld8(gs, pr);
+    ld8(gs + H, pz);
+    ld8(gs + 2 * H, pn);
+    ld8(gs + 3 * H, pa);
+    ld8(p.hs + ((size_t)tt * B + gb) * H + ju, php);
+  };
+  prefetch(T - 1);
   for (int t = T - 1; t >= 0; --t) {
     // ---- A: dh_t for own units, gate derivatives, dgh block ----
     if (t < T - 1) {
@@ -440,9 +454,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     float drp[8], dzp[8], dnp[8], dnr[8];
     if (arow) {
       float dh[8], v[8];
-      ld8(p.dhs + ((size_t)t * B + gb) * H + ju, dh);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dh[u] += dhz[u];
+      for (int u = 0; u < 8; ++u) dh[u] = pdh[u] + dhz[u];
       if (t < T - 1) {
         const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + (size_t)gb * kUC + uo;
         for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
@@ -451,13 +464,15 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
           for (int u = 0; u < 8; ++u) dh[u] += v[u];
         }
       }
-      const float* gs = p.gates + ((size_t)t * B + gb) * 4 * H + ju;
       float r[8], z[8], n[8], a[8], hp[8];
-      ld8(gs, r);
-      ld8(gs + H, z);
-      ld8(gs + 2 * H, n);
-      ld8(gs + 3 * H, a);
-      ld8(p.hs + ((size_t)t * B + gb) * H + ju, hp);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        r[u] = pr[u];
+        z[u] = pz[u];
+        n[u] = pn[u];
+        a[u] = pa[u];
+        hp[u] = php[u];
+      }
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const float dn = dh[u] * (1.f - z[u]);
@@ -480,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     fence_proxy_async_global();
     tc_fence_before();
     cluster_arrive();  // publish this step's dgh block; the fp32 copies below are only read after the kernel
+    prefetch(t - 1);
     if (arow) {
       __nv_bfloat16* gxo = p.dgx + ((size_t)t * B + gb) * H3 + ju;
       __nv_bfloat16* gho = p.dgh + ((size_t)t * B + gb) * H3 + ju;
