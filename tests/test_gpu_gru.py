@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import models as om
+from oracle import restated as X
 
 pytestmark = pytest.mark.gpu
 
@@ -98,3 +99,36 @@ def test_gru_step_async_matches_step(dev):
     bad[3, 4] = V  # out of range: the reference's onehot message, raised at staging
     with pytest.raises(Exception, match="onehot index"):
         tr.step_async(bad, ys[0])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_embedding_gather_equals_reference_onehot_matmul(session, dtype):
+    """the embedding gather is the reference's onehot(tokens) @ E (tensor.py:299-317 then the
+    float64 matmul_t, tensor.py:213-229) -- a one-term float64 sum, so the float32 gather must match it bit for bit
+    (bf16 output: its rounding); the scatter-add backward equals onehot^T . dout to float32 rounding (repeated
+    tokens included), time-major rows (row t*B + b holds token [b, t])."""
+    from paper_2409_11600_b200 import autodiff, layers
+    from paper_2409_11600_b200._lib import BF16, F32
+
+    rng = np.random.default_rng(31)
+    V, E, B, T = 500, 64, 8, 24
+    tokens = rng.integers(0, V, (B, T)).astype(np.float32)
+    tokens[0, :5] = 7  # repeated ids: several rows accumulate into one table row
+    table = rng.standard_normal((V, E)).astype(np.float32)
+    pool = session.pool
+    tt = autodiff.make_param(pool, table, "E")
+    out = layers.embedding(autodiff.make_data(pool, tokens), tt, pool, dtype=BF16 if dtype == "bf16" else F32)
+    onehot = np.zeros((B * T, V))
+    tm = tokens.T.reshape(-1).astype(np.int64)  # time-major
+    onehot[np.arange(B * T), tm] = 1.0
+    ref = onehot @ table.astype(np.float64)  # the reference composition in float64
+    want = X.round_bf16(ref) if dtype == "bf16" else ref.astype(np.float32)
+    np.testing.assert_array_equal(out.data.reshape(B * T, E), want)
+    g = X.round_bf16(rng.standard_normal((B * T, E))) if dtype == "bf16" else rng.standard_normal((B * T, E)).astype(
+        np.float32)
+    gt = autodiff.make_data(pool, g, dtype=BF16 if dtype == "bf16" else F32)
+    loss = autodiff.rec_sum_loss(autodiff.rec_elementwise("hadamard", out, gt, pool), pool)
+    autodiff.push_assignment(session.tape(), "loss", loss)
+    autodiff.backward(session.tape(), session.grad_cache, pool)
+    dref = onehot.T @ g.astype(np.float64)
+    np.testing.assert_allclose(session.grad_cache.get("E"), dref, rtol=1e-6, atol=1e-6)
