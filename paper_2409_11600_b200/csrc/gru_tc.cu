@@ -46,9 +46,6 @@ constexpr int kMaxB = 64;       // batch rows (A operand rows that are read back
 constexpr int kDP = 100;        // row pitch (floats) of the forward's accumulator tile: conflict-free float4 rows
 long long* g_trace = nullptr;   // NSK_GRU_TRACE: per-step timestamps of the forward (diagnostics)
 
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // split cluster barrier: the arrive publishes (release) what the peers need, work that only this CTA needs runs
 // between arrive and wait, off the critical path
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }

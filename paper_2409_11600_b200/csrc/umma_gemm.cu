@@ -88,6 +88,11 @@ struct UmmaProb {
   const uint8_t* bmask;
   int bacc;
   int stats_shared;  // STATS 1 with wide N: one [2][N] CTA accumulator combined per chunk (per-warp ones do not fit)
+  // CTA-pair multicast of the B operand (conv passes with 256-wide tiles, whose few-tile grids are L2-bound: every
+  // CTA streams the same filter): launched as 2-CTA clusters, the pair takes adjacent M tiles of one (N tile,
+  // class / split) unit, each CTA loads half of every B stage and multicasts it into both; a stage is free again
+  // once BOTH CTAs' MMAs are done with it (the MMA commit arrives on both CTAs' empty barriers). mt counts pairs.
+  int mc;
 };
 
 constexpr int kRRMaxA = 6 * 32 * 128;  // largest rr A box: (4 + 2) rows x 32 pixels x 128 B
@@ -177,6 +182,23 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* ba
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(const CUtensorMap* map, uint64_t* bar, void* dst, int c0, int c1,
+                                               int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
 // One 64-element K slab (4 UMMA k-steps) with compile-time descriptor steps: the offsets fold into immediates
 // of the uniform-register descriptor adds, so the issuing warp runs ~2 instructions per MMA.
 template <int AOFF0, int BOFF0, int AST, int BST, bool TF32>
@@ -207,13 +229,13 @@ struct Unit {
   int kb, nk;     // first k-step and number of k-steps
 };
 
-__device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN) {
+__device__ __forceinline__ Unit decode_unit(const UmmaProb& p, int u, int BN, int crank) {
   Unit w;
   const int mn = p.mt * p.nt;
   w.z = u / mn;
   const int r = u - w.z * mn;
   const int mi = r / p.nt;
-  w.m0 = mi * 128;
+  w.m0 = (p.mc ? 2 * mi + crank : mi) * 128;  // pair multicast: adjacent M tiles (past M: all rows masked)
   w.n0 = (r - mi * p.nt) * BN;
   if (p.mode == MODE_WGRAD || p.k_per_split > 0) {  // wgrad, or a split-K GEMM
     w.kb = w.z * p.k_per_split;
@@ -264,11 +286,15 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform role index
   const int lane = threadIdx.x & 31;
   const int units = p.units;
+  // pair multicast (p.mc): the 2-CTA cluster walks the pair units together; rank = the M tile within the pair
+  const int crank = p.mc ? (int)(blockIdx.x & 1) : 0;
+  const int u0 = p.mc ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ustep = p.mc ? (int)(gridDim.x >> 1) : (int)gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], WRES ? p.asplit : 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], p.mc ? 2 : 1);  // pair multicast: both CTAs' MMAs release the stage
     }
     for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
@@ -285,6 +311,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
   }
   tc_fence_before();
   __syncthreads();
+  if (p.mc) cluster_sync_all();  // the peer's barriers are initialised before any multicast targets them
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -303,8 +330,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         tma_load_3d(&tmB, wfull, smem + S::W_OFF + g * 3 * S::B1_BYTES, 0, 0, p.gw[0][g][0]);  // N = C = 64
       }
     }
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit w = decode_unit(p, u, BN);
+    for (int u = u0; u < units; u += ustep) {
+      const Unit w = decode_unit(p, u, BN, crank);
       int n_img = 0, h_img = 0, w_img = 0;
       if (p.mode == MODE_CONV) {
         const int hw = p.Ho * p.Wo;
@@ -416,7 +443,15 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
           const int tap = kk / p.cchunks;
           const int c0 = (kk - tap * p.cchunks) * 64;
           const int cls = p.k_per_split > 0 ? 0 : w.z;
-          if (p.bmode == BMODE_2D) {
+          if (p.mc) {  // this CTA's half of the B stage, into both CTAs of the pair (host map: BN/2-row boxes)
+            if (p.bmode == BMODE_2D) {
+              tma_load_2d_mc(&tmB, &full[s], sb + crank * (BN / 2) * 128, p.tw[cls][tap] * (p.cchunks * 64) + c0,
+                             w.n0 + crank * (BN / 2), (uint16_t)3);
+            } else {
+              for (int b = crank * (BN / 128); b < (crank + 1) * (BN / 128); ++b)
+                tma_load_3d_mc(&tmB, &full[s], sb + b * 8192, w.n0 + b * 64, p.tw[cls][tap], c0, (uint16_t)3);
+            }
+          } else if (p.bmode == BMODE_2D) {
             tma_load_2d(&tmB, &full[s], sb, p.tw[cls][tap] * (p.cchunks * 64) + c0, w.n0);
           } else {
 #pragma unroll
@@ -451,13 +486,13 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       int j = 0;
       // fixed-order row reuse: every unit has the same k-steps (single class, no split) -- no per-tile decode
       const int nk_fixed = (KIND >= 1 && KIND <= 4) ? rr_groups * p.cchunks : 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
+      for (int u = u0; u < units; u += ustep, ++j) {
         Unit w;
         if constexpr (KIND >= 1 && KIND <= 4) {
           w.z = 0;
           w.nk = nk_fixed;
         } else {
-          w = decode_unit(p, u, BN);
+          w = decode_unit(p, u, BN, crank);
         }
         const int acc = j % NACC;
         if (j >= NACC) {
@@ -510,7 +545,10 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             } else if constexpr (KIND == 13) {
               mma_slab<MNS, MNS, TF>(d_tmem, ad0, bd0, idesc, k > 0);
             }
-            umma_commit(&empty[s]);
+            if (p.mc)
+              umma_commit_mc(&empty[s], (uint16_t)3);
+            else
+              umma_commit(&empty[s]);
           }
           __syncwarp();
           if (RR && ++g == rr_groups) g = 0;
@@ -551,8 +589,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     int s = 0;
     uint32_t phase = 0;
     int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const Unit w = decode_unit(p, u, BN);
+    for (int u = u0; u < units; u += ustep, ++j) {
+      const Unit w = decode_unit(p, u, BN, crank);
       const int acc = j % NACC;
       if (j >= NACC) {
         mbar_wait(&tempty[acc], (j / NACC - 1) & 1);
@@ -611,8 +649,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
       }
     }
     int j = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++j) {
-      const Unit w = decode_unit(p, u, BN);
+    for (int u = u0; u < units; u += ustep, ++j) {
+      const Unit w = decode_unit(p, u, BN, crank);
       const int acc = j % NACC;
       mbar_wait_backoff(&tfull[acc], (j / NACC) & 1);
       tc_fence_after();
@@ -844,6 +882,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
     tc_fence_after();
     tmem_dealloc(tmem_base, S::TMEM_COLS);
   }
+  if (p.mc) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
 }
 
 // wgrad split-K reduction: ws[split][N][Mpad] (rows = cout, cols = (tap, cin)) -> dw[cout][tap][cin] (+= if beta).
@@ -1374,6 +1413,15 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
     if (const char* e = getenv("NSK_WGRAD_GRID")) cap = atoi(e);
     if (cap > 0 && cap < grid) grid = cap;
   }
+  if (p.mc) {  // CTA pairs (2-CTA clusters) walking pair units
+    if (grid > 2 * p.units) grid = 2 * p.units;
+    grid &= ~1;
+    if (grid < 2) grid = 2;
+    if (grid_out) *grid_out = grid;
+    nsk::launch_pdl_cluster(kern, grid, Launch<S>::template threads<EPI>(), smem, st, 2, a, b, c, p);
+    NSK_LAUNCH_CHECK("umma_kernel (pair multicast)");
+    return NSK_OK;
+  }
   if (grid > p.units) grid = p.units;
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
@@ -1388,9 +1436,9 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
   static CUtensorMap dummy{};
   const CUtensorMap& c = cmap ? *cmap : dummy;
   if (!cmap) p.tma_store = 0;
-  p.mt = mt;
+  p.mt = p.mc ? (mt + 1) / 2 : mt;  // pair multicast: units are pairs of M tiles
   p.nt = nt;
-  p.units = mt * nt * nz;
+  p.units = p.mt * nt * nz;
   if (p.rr) {
     if constexpr (ESZ == 2) {
       switch (BN) {  // rr stages carry 3 taps of B: one CTA per SM, ~190-220 KB of ring
@@ -1422,6 +1470,14 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
     }
   }
   return nsk::set_error(NSK_ERR_UNSUPPORTED, "unsupported BN");
+}
+
+// CTA-pair multicast of B for the 256-wide conv tiles: opt-in (NSK_MC=1). Measured on B200 it halves each CTA's
+// filter traffic but is 5 % slower on the 8x8 and 4x4 layers (19.5 -> 20.6 us, 26.7 -> 28.0 us): those passes are
+// not L2-bandwidth bound, and the pair's shared stage release couples the two CTAs' pipelines.
+bool mc_ok(int BN, int mt) {
+  const char* e = getenv("NSK_MC");
+  return e && e[0] == '1' && BN == 256 && mt >= 2;
 }
 
 int pick_bn(int N) {
@@ -1765,11 +1821,12 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   const int BN = splits > 1 ? 256 : pick_bn_units(d->K, (d->N * P * Q + 127) / 128, 1);
   CUtensorMap ma, mb;
   if (!i2c && (rc = nhwc_map(&ma, x, d->N, d->H, d->W, d->C, 64, Wt, Ht, Nt, d->stride))) return rc;
+  const bool pair_mc = !y_f32 && mc_ok(BN, (d->N * P * Q + 127) / 128);
   {
     const int RS = d->R * d->S;
     uint64_t dims[2] = {(uint64_t)RS * d->C, (uint64_t)d->K};
     uint64_t str[1] = {(uint64_t)RS * d->C * 2};
-    uint32_t box[2] = {64, (uint32_t)BN};
+    uint32_t box[2] = {64, (uint32_t)(pair_mc ? BN / 2 : BN)};  // pair multicast: each CTA loads half the rows
     if ((rc = nsk::encode_tmap(&mb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box, nullptr,
                                CU_TENSOR_MAP_SWIZZLE_128B)))
       return rc;
@@ -1795,6 +1852,7 @@ int conv_fprop(const NskConvDesc* d, const void* x, const void* w, void* y, int 
   p.out = y;
   p.ldc = d->K;
   p.out_f32 = y_f32;
+  p.mc = pair_mc;
   if (i2c) {
     if ((rc = i2c_map(p, &ma, x, d->N, d->H, d->W, d->C, P, Q, 1, 128))) return rc;
   } else if (splits == 1 && try_rowreuse(p, &ma, x, d->N, d->H, d->W, d->C, BN)) {
@@ -1967,6 +2025,7 @@ int conv_dgrad(const NskConvDesc* d, const void* dy, const void* w, void* dx, fl
       try_wres(p, &ma, dy, d->N, P, Q, d->K, d->C);
     }
   }
+  p.mc = !p.rr && mc_ok(BN, (p.M + 127) / 128);  // (the dgrad B boxes are per 64-channel slab: no map change)
   if (const char* pr = getenv("NSK_PROBE")) p.probe = atoi(pr);
   if (bx) {
     p.bx = bx;

@@ -92,10 +92,13 @@ def test_conv_bn_chain_at_batch_256(session, case):
 
 
 @pytest.mark.parametrize("case", C2_CONVS, ids=_ids)
-def test_conv_passes_at_batch_256(session, case):
+def test_conv_passes_at_batch_256(session, case, monkeypatch, pair_multicast=False):
     """The three conv passes alone (no BN between): fprop, dgrad, wgrad with a random bf16 output gradient."""
     from paper_2409_11600_b200 import autodiff, layers
     from paper_2409_11600_b200._lib import BF16
+
+    if pair_multicast:
+        monkeypatch.setenv("NSK_MC", "1")
 
     hw, c, k, r, st, pad = case
     rng = np.random.default_rng(2000 + sum(case))
@@ -207,3 +210,10 @@ def test_bn_backward_fused_into_dgrad_at_batch_256(session, case, acc, monkeypat
     assert rel(dx_f, X.round_bf16(dxr)) < TOL, ("dx", rel(dx_f, X.round_bf16(dxr)))
     # fused vs the separate reduction kernel: the same sums in another order
     assert rel(dgb_f, dgb_u) < 1e-4 and rel(dx_f, dx_u) < 1e-3
+
+
+@pytest.mark.parametrize("case", [c for c in C2_CONVS if c[2] >= 256 and c[3] == 3], ids=_ids)
+def test_conv_passes_pair_multicast(session, case, monkeypatch):
+    """The opt-in CTA-pair multicast of the filter operand (NSK_MC=1: 2-CTA clusters, each CTA loads half of every
+    B stage into both, stages released by both CTAs' MMAs) on the 256-wide layers, split-K included: same bar."""
+    test_conv_passes_at_batch_256(session, case, monkeypatch, pair_multicast=True)
