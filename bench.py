@@ -247,7 +247,7 @@ class ConvTimer:
     def _ev(self, stream):
         ev = C.c_void_p()
         self.lib.nsk_event_create(1, C.byref(ev))
-        self.lib.nsk_event_record(ev, stream)
+        self.lib.nsk_event_record_external(ev, stream)  # a real event node when the step is being captured
         return ev
 
     def begin(self, stream):
@@ -266,24 +266,28 @@ class ConvTimer:
         return sum(ts) / len(ts) if ts else None, len(ts)
 
 
-def time_conv_in_step(tr, lib, conv, steps=3):
-    """The dominant conv's launch duration inside real (eager) training steps on the staged batch: events on the
-    compute stream right around each launch, with the rest of the step (side-stream weight gradients included)
-    running as in the bench."""
+def time_conv_in_step(tr, lib, conv, replays=5):
+    """The dominant conv's launch duration inside the training step as it is timed: the step body captured once
+    more into a CUDA graph with event-record nodes around each launch of that conv (on the compute stream it is
+    launched on), replayed like the timed steps (side-stream weight gradients, PDL, the same pooled buffers)."""
     from paper_2409_11600_b200 import _lib, layers
+    from paper_2409_11600_b200.train import capture
 
     timer = ConvTimer(lib, conv)
     layers.KTIMER = timer
     try:
-        for _ in range(steps):
-            # the stream is held while the host enqueues the whole step, which then runs back to back: the event
-            # brackets contain the kernel, not host launch latency
-            _lib.check(lib.nsk_spin(300_000_000, _lib.stream()))
-            tr._body()
-            _lib.sync()
+        graph, _ = capture(tr._body)
     finally:
         layers.KTIMER = None
-    return timer.mean_ms()
+    ts = []
+    for _ in range(replays):
+        graph.launch()
+        _lib.sync()
+        for a, b in timer.pairs:
+            ms = C.c_float()
+            _lib.check(lib.nsk_event_elapsed_ms(a, b, C.byref(ms)))
+            ts.append(ms.value)
+    return (sum(ts) / len(ts) if ts else None), len(ts)
 
 
 def sub_bench(model: str, steps: int, warmup: int):
@@ -449,9 +453,9 @@ def ours_arm(args, rank, world, local_rank):
                 "frac": achieved / pk_sus, "traffic": profiled_traffic() if args.model == "resnet18" else None,
                 "peak_source": f"{src} bf16_tflops_sustained (kernel timed inside the training step)",
                 "algorithmic_flops_per_launch": flops, "launch_ms": kms_step,
-                "timing": f"mean of {nlaunch} launches inside 3 eager training steps, each enqueued whole behind a "
-                          "300 ms device spin so it runs back to back (CUDA events on the compute stream around each "
-                          "launch; random-init weights, N(0,1) images)",
+                "timing": f"mean of {nlaunch} launches inside replays of the captured training step (event-record "
+                          "nodes on the compute stream around each launch of this conv; random-init weights, N(0,1) "
+                          "images)",
                 "alone": {"launch_ms": kms_alone, "achieved": flops / (kms_alone / 1000.0) / 1e12, "peak": pk_burst,
                           "frac": flops / (kms_alone / 1000.0) / 1e12 / pk_burst,
                           "timing": "20 back-to-back launches, random bf16 operands, burst peak"}}

@@ -67,6 +67,8 @@ int nsk_event_record(void* e, void* stream);
 int nsk_event_wait(void* stream, void* e);
 int nsk_event_sync(void* e);
 int nsk_event_elapsed_ms(void* start, void* stop, float* ms);
+/* event record that becomes an event-record node of a graph under capture (timing inside a replayed step) */
+int nsk_event_record_external(void* e, void* stream);
 /* measurement utility: occupies `stream` for ns nanoseconds of device time (bench.py enqueues a whole eager step
  * behind it so in-step event brackets contain no host launch gaps) */
 int nsk_spin(uint64_t ns, void* stream);

@@ -54,6 +54,7 @@ SIGNATURES = {
     "nsk_event_sync": (i32, [vp]),
     "nsk_event_elapsed_ms": (i32, [vp, vp, C.POINTER(f32)]),
     "nsk_spin": (i32, [u64, vp]),
+    "nsk_event_record_external": (i32, [vp, vp]),
     "nsk_graph_begin": (i32, [vp]),
     "nsk_graph_end": (i32, [vp, C.POINTER(vp), C.POINTER(u64)]),
     "nsk_graph_launch": (i32, [vp, vp]),

@@ -373,6 +373,12 @@ int nsk_event_record(void* e, void* stream) {
   NSK_CUDA(cudaEventRecord((cudaEvent_t)e, (cudaStream_t)stream));
   return NSK_OK;
 }
+// a record that stays a real event-record node when the stream is being captured (cudaEventRecordExternal):
+// timing a kernel inside a replayed step graph
+int nsk_event_record_external(void* e, void* stream) {
+  NSK_CUDA(cudaEventRecordWithFlags((cudaEvent_t)e, (cudaStream_t)stream, cudaEventRecordExternal));
+  return NSK_OK;
+}
 int nsk_event_wait(void* stream, void* e) {
   NSK_CUDA(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)e, 0));
   return NSK_OK;
