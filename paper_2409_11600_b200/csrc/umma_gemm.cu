@@ -1329,6 +1329,50 @@ __global__ void __launch_bounds__(kFoldThreads) conv_split_fold_kernel(const flo
 }
 
 // split-K GEMM fold: C[m, n] = sum_z ws[z][m][n] (+ bias[n]) (+ beta * C[m, n]), fp32 or bf16 out
+// 16-byte variant (N, ldc multiples of 4, aligned buffers): four columns per thread, the splits' loads all in
+// flight, the same per-element summation order (split 0, 1, ...) -- bit-identical to the scalar fold
+__global__ void splitk_fold4_kernel(const float* __restrict__ ws, int splits, int M, int N, void* C, long long ldc,
+                                    int c_f32, const float* __restrict__ bias, float beta) {
+  pdl_wait();
+  const long long total = (long long)M * N, total4 = total / 4;
+  const int N4 = N / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int m = (int)(i / N4), n = (int)(i - (long long)m * N4) * 4;
+    float4 acc = __ldg((const float4*)ws + i);
+    for (int z = 1; z < splits; ++z) {
+      const float4 v = __ldg((const float4*)(ws + (long long)z * total) + i);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    if (bias) {
+      const float4 b4 = __ldg((const float4*)(bias + n));
+      acc.x += b4.x;
+      acc.y += b4.y;
+      acc.z += b4.z;
+      acc.w += b4.w;
+    }
+    if (c_f32) {
+      float4* o = (float4*)((float*)C + (long long)m * ldc + n);
+      if (beta != 0.f) {
+        const float4 old = *o;
+        acc.x += beta * old.x;
+        acc.y += beta * old.y;
+        acc.z += beta * old.z;
+        acc.w += beta * old.w;
+      }
+      *o = acc;
+    } else {
+      uint2 u;
+      u.x = pack_bf16x2(acc.x, acc.y);
+      u.y = pack_bf16x2(acc.z, acc.w);
+      *(uint2*)((__nv_bfloat16*)C + (long long)m * ldc + n) = u;
+    }
+  }
+}
+
 __global__ void splitk_fold_kernel(const float* __restrict__ ws, int splits, int M, int N, void* C, long long ldc,
                                    int c_f32, const float* __restrict__ bias, float beta) {
   pdl_wait();
@@ -1794,7 +1838,13 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
     rc = esz == 2 ? dispatch_bn<2>(BN, ma, mb, p, mt, nt, splits, st) : dispatch_bn<4>(BN, ma, mb, p, mt, nt, splits, st);
     if (rc) return rc;
     const long long total = (long long)M * N;
-    nsk::launch_pdl(splitk_fold_kernel, nsk::grid_for(total, 256), 256, 0, st, ws, splits, M, N, C, ldc, c_f32, bias, beta);
+    const bool vec = N % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)C & 15) == 0 && (!bias || ((uintptr_t)bias & 15) == 0);
+    if (vec)
+      nsk::launch_pdl(splitk_fold4_kernel, nsk::grid_for(total / 4, 256), 256, 0, st, ws, splits, M, N, C, ldc, c_f32,
+                      bias, beta);
+    else
+      nsk::launch_pdl(splitk_fold_kernel, nsk::grid_for(total, 256), 256, 0, st, ws, splits, M, N, C, ldc, c_f32,
+                      bias, beta);
     NSK_LAUNCH_CHECK("splitk_fold_kernel");
     return NSK_OK;
   }
