@@ -1508,8 +1508,17 @@ int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, 
       // 8 epilogue warps unless the statistics buffers would not fit beside them
       using S8 = Smem<256, ESZ, 4, false, 8>;
       const int need = S8::TOTAL + epi_extra_smem(p, 8);
-      if (need <= 227 * 1024 && !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0'))
+      const bool epi8 = !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0');
+      if (need <= 227 * 1024 && epi8)
         return launch_umma<256, ESZ, 4, false, 8, false, STATS>(a, b, c, p, st, grid_out);
+      if constexpr (STATS == 1) {
+        // the statistics do not fit beside four stages: the store-bound layers (large M, or ResNet-50's short-K
+        // 1x1 expands to >= 1024 channels) keep the 8-warp epilogue with three stages (R50 9.85k -> 10.24k
+        // img/s); ResNet-18's small 8x8 layers measure 0.15 % faster on the deeper 4-warp ring
+        if (epi8 && (p.M >= (1 << 15) || (p.k_steps <= 16 && p.N >= 1024)) &&
+            !(getenv("NSK_STATS_S3") && getenv("NSK_STATS_S3")[0] == '0'))
+          return launch_umma<256, ESZ, 3, false, 8, false, STATS>(a, b, c, p, st, grid_out);
+      }
       return launch_umma<256, ESZ, 4, false, 4, false, STATS>(a, b, c, p, st, grid_out);
     }
   }
