@@ -97,6 +97,16 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return copysignf(t, x);
 }
 
+// 32 lanes x 8 consecutive fp32 columns
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* f) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ void ld16(const float* p, float* v) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) *(float4*)(v + 4 * i) = __ldcg((const float4*)(p + 4 * i));
@@ -121,6 +131,57 @@ __device__ __forceinline__ void st8_bf16(__nv_bfloat16* p, const float* v) {
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// N consecutive fp32 / bf16 values per thread (N = units per thread: 8, 4, 2 or 1)
+template <int N>
+__device__ __forceinline__ void ldv(const float* p, float* v) {
+  if constexpr (N == 8) {
+    ld8(p, v);
+  } else if constexpr (N == 4) {
+    *(float4*)v = __ldcg((const float4*)p);
+  } else if constexpr (N == 2) {
+    *(float2*)v = __ldcg((const float2*)p);
+  } else {
+    v[0] = __ldcg(p);
+  }
+}
+template <int N>
+__device__ __forceinline__ void ldvs(const float* p, float* v) {  // shared memory
+  if constexpr (N >= 4) {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) *(float4*)(v + 4 * i) = *(const float4*)(p + 4 * i);
+  } else if constexpr (N == 2) {
+    *(float2*)v = *(const float2*)p;
+  } else {
+    v[0] = p[0];
+  }
+}
+template <int N>
+__device__ __forceinline__ void stv(float* p, const float* v) {
+  if constexpr (N >= 4) {
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i) *(float4*)(p + 4 * i) = *(const float4*)(v + 4 * i);
+  } else if constexpr (N == 2) {
+    *(float2*)p = *(const float2*)v;
+  } else {
+    p[0] = v[0];
+  }
+}
+template <int N>
+__device__ __forceinline__ void stvb(__nv_bfloat16* p, const float* v) {
+  if constexpr (N == 8) {
+    st8_bf16(p, v);
+  } else if constexpr (N == 4) {
+    uint2 a;
+    a.x = pack_bf16x2(v[0], v[1]);
+    a.y = pack_bf16x2(v[2], v[3]);
+    *(uint2*)p = a;
+  } else if constexpr (N == 2) {
+    *(uint32_t*)p = pack_bf16x2(v[0], v[1]);
+  } else {
+    p[0] = __float2bfloat16_rn(v[0]);
+  }
+}
+
 __device__ __forceinline__ void st16_bf16(__nv_bfloat16* p, const float* v) {
   uint4 a, b;
   a.x = pack_bf16x2(v[0], v[1]); a.y = pack_bf16x2(v[2], v[3]); a.z = pack_bf16x2(v[4], v[5]);
@@ -143,7 +204,10 @@ struct FwdArgs {
   __nv_bfloat16* hsb;  // [T+1][B][H] bf16 copy of hs (operand of the recurrent weight gradient dU = dgh^T h)
   __nv_bfloat16* hx; // [2][B][H] exchange ring
   int T, B, H;
-  long long* trace;  // optional per-step timestamps of CTA 0 (NSK_GRU_TRACE), 8 per step
+  int Bc;            // batch rows per cluster (cluster k owns rows [k Bc, (k + 1) Bc))
+  int NG;            // h-slice barrier groups: the MMA warp waits NG times per step (NS / NG slices each)
+  int swap;          // 1: D^T = U h^T (M = the CTA's 96 gate rows, N = the Bc batch rows rounded up to 16)
+  long long* trace;  // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE), 8 per step
 };
 
 __device__ __forceinline__ long long gclock() {
@@ -178,21 +242,26 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
 // slice c starts as soon as it lands. The only cluster-wide barrier is split: each CTA arrives once its MMA has
 // finished reading h_t and waits right before its multicast overwrites the peers' h buffers, so its latency hides
 // behind the gate math.
+// Batch groups: the rows of the batch are independent through the recurrence, so the grid is B / Bc clusters,
+// each the full H / 32 CTAs (U resident in every cluster) over its own Bc rows. Each SM then receives Bc rows of
+// h per step instead of B: the multicast delivery into a CTA (~17 B/clk) is what bounds the exchange.
+template <int UPT>  // hidden units per thread in the gate math: Bc <= 8 UPT rows x 32 / UPT threads per row
 __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                  const __grid_constant__ CUtensorMap tmH,
                                                                  const FwdArgs p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H;
+  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, Bc = p.Bc;
   const int NCH = H / 64;                  // 64-wide K chunks of U
   const int NS = H / kUC;                  // 32-wide h slices = CTAs of the cluster
+  const int b0 = (int)(blockIdx.x / NS) * Bc;  // first batch row of this cluster
   uint8_t* us = smem;                      // NCH x 12 KB (SW128, B operand)
   uint8_t* hsm = us + NCH * 12288;         // NS x 4 KB (SW64, A operand) + 4 KB slack (rows 64..127 of the last)
   float* dsm = (float*)(hsm + NS * 4096 + 4096);   // [64][kDP] accumulator tile for the gate math
   uint64_t* bars = (uint64_t*)(dsm + 64 * kDP);
   uint64_t* ufull = bars;                  // 1
-  uint64_t* hfull = bars + 1;              // NS: one per slice (= per producing CTA)
+  uint64_t* hfull = bars + 1;              // NG: one per group of NS / NG slices (producing CTAs)
   uint64_t* mdone = hfull + NS;            // 1
   uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
@@ -200,15 +269,17 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   const int q = (int)cluster_rank();
   const int j0 = q * kUC;
   const uint16_t all = (uint16_t)((1u << NS) - 1u);
-  const uint32_t slice_bytes = (uint32_t)(B * 64);
+  const int NG = p.NG, GS = NS / NG;       // barrier groups, slices per group
+  const uint32_t group_bytes = (uint32_t)(GS * Bc * 64);
+  uint64_t* hbar = &hfull[q / GS];         // the barrier this CTA's slice completes (in every CTA)
   if (threadIdx.x == 0) {
     mbar_init(ufull, 1);
-    for (int c = 0; c < NS; ++c) mbar_init(&hfull[c], 1);
+    for (int g = 0; g < NG; ++g) mbar_init(&hfull[g], 1);
     mbar_init(mdone, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmU);
     tma_prefetch_desc(&tmH);
-    for (int c = 0; c < NS; ++c) mbar_expect_tx(&hfull[c], slice_bytes);  // phase 0
+    for (int g = 0; g < NG; ++g) mbar_expect_tx(&hfull[g], group_bytes);  // phase 0
   }
   if (warp == 3) {
     tmem_alloc(tmem_slot, 128);
@@ -221,24 +292,26 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
 
   // TMEM readers: warps 0,1,4,5 (sub-partitions 0 and 1 hold accumulator rows = batch rows 0..63); they copy D to a
   // shared-memory tile so that ALL eight warps (all four schedulers) share the gate math: thread -> batch row
-  // gb = tid / 4, units [8 gq, 8 gq + 8) of this CTA
+  // gb = tid / TPR, units [UPT gq, UPT gq + UPT) of this CTA
+  constexpr int TPR = kUC / UPT;  // threads per batch row
   const bool rd = (warp & 2) == 0;
   const int sp = warp & 1, hf = warp >> 2;
-  const int gb = threadIdx.x >> 2, gq = threadIdx.x & 3;
-  const bool row_ok = gb < B;
-  const int ju = j0 + gq * 8;  // first global unit of this thread
-  float h[8], cr[8], cz[8], cn[8], gr[8], gz[8], gn[8];
+  const int gb = threadIdx.x / TPR, gq = threadIdx.x % TPR;
+  const bool row_ok = gb < Bc;
+  const size_t grow = (size_t)(b0 + gb);  // global batch row
+  const int ju = j0 + gq * UPT;  // first global unit of this thread
+  float h[UPT], cr[UPT], cz[UPT], cn[UPT], gr[UPT], gz[UPT], gn[UPT];
   if (row_ok) {
-    ld8(p.hs + (size_t)gb * H + ju, h);
-    ld8(p.c + ju, cr);
-    ld8(p.c + H + ju, cz);
-    ld8(p.c + 2 * H + ju, cn);
-    st8_bf16(p.hx + (size_t)gb * H + ju, h);  // ring slot 0 = bf16(h0)
-    st8_bf16(p.hsb + (size_t)gb * H + ju, h);
-    const float* g3 = p.gx + (size_t)gb * H3 + ju;  // step 0's input projections
-    ld8(g3, gr);
-    ld8(g3 + H, gz);
-    ld8(g3 + 2 * H, gn);
+    ldv<UPT>(p.hs + grow * H + ju, h);
+    ldv<UPT>(p.c + ju, cr);
+    ldv<UPT>(p.c + H + ju, cz);
+    ldv<UPT>(p.c + 2 * H + ju, cn);
+    stvb<UPT>(p.hx + grow * H + ju, h);  // ring slot 0 = bf16(h0)
+    stvb<UPT>(p.hsb + grow * H + ju, h);
+    const float* g3 = p.gx + grow * H3 + ju;  // step 0's input projections
+    ldv<UPT>(g3, gr);
+    ldv<UPT>(g3 + H, gz);
+    ldv<UPT>(g3 + 2 * H, gn);
   }
   if (warp == 2 && elect_one()) {  // U rows of this CTA: 3 gates x NCH chunks of {64 k, 32 rows}
     mbar_expect_tx(ufull, (uint32_t)(NCH * 12288));
@@ -248,26 +321,45 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   fence_proxy_async_global();
   tc_fence_before();
   cluster_sync_all();  // every CTA's mbarriers are initialised and its h0 slice is in the ring
-  if (threadIdx.x == 0) tma_load_2d_mc(&tmH, &hfull[q], hsm + q * 4096, j0, 0, all);
+  if (threadIdx.x == 0) tma_load_2d_mc(&tmH, hbar, hsm + q * 4096, j0, b0, all);
 
   const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
+  const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // swapped: MMA N (batch rows, rows past Bc unused)
+  const uint32_t idesc_s = make_idesc(1u, 0u, 0u, 128u, (uint32_t)NP);
+  const bool swap = p.swap != 0;
   for (int t = 0; t < T; ++t) {
-    long long* tr = p.trace ? p.trace + ((size_t)q * T + t) * 16 : nullptr;
+    long long* tr = p.trace && b0 == 0 ? p.trace + ((size_t)q * T + t) * 16 : nullptr;
     if (warp == 3) {
       if (t == 0) mbar_wait(ufull, 0);
-      const uint32_t sh = smem_u32(hsm), su = smem_u32(us);
-      for (int c = 0; c < NS; ++c) {
-        mbar_wait(&hfull[c], t & 1);
-        if (tr && lane == 0 && (c == 0 || c == NS - 1)) tr[c == 0 ? 1 : 2] = gclock();
+      // Lean issue loop (it is the step's critical path): a wait by the MMA warp also waits for the queued MMAs'
+      // operand reads (~130 cycles), so few barrier groups; per pair of slices one U chunk (its two 64-byte
+      // halves), descriptors advanced by immediates. Slice c: h at + c * 4 KB, U chunk c / 2, half c & 1.
+      const uint64_t hd0 = sdesc_sw64(smem_u32(hsm));
+      const uint64_t ud0 = sdesc_sw128(smem_u32(us), 16, 1024);
+      const int GP = NS / 2 / NG;  // slice pairs per barrier group
+      for (int g = 0; g < NG; ++g) {
+        mbar_wait(&hfull[g], t & 1);
+        if (tr && lane == 0 && (g == 0 || g == NG - 1)) tr[g == 0 ? 1 : 2] = gclock();
         tc_fence_after();
-        const uint64_t ad = sdesc_sw64(sh + c * 4096);
-        // U chunk c/2, the 64-byte half (c & 1) of its 128-byte rows
-        const uint64_t bd = sdesc_sw128(su + (c >> 1) * 12288, 16, 1024) + (uint64_t)((c & 1) * 4);
-        if (elect_one()) {
-          umma_off<0, 0, false>(tmem, ad, bd, idesc, c > 0 ? 1u : 0u);
-          umma_off<2, 2, false>(tmem, ad, bd, idesc, 1u);
+        for (int kk = 0; kk < GP; ++kk) {
+          const int k = g * GP + kk;
+          const uint64_t hd = hd0 + (uint64_t)(k * 512), ud = ud0 + (uint64_t)(k * 768);
+          const uint32_t acc0 = k > 0 ? 1u : 0u;
+          if (elect_one()) {
+            if (swap) {  // U (resident, 128 B swizzle) is the A operand: the MMA reads Bc rows of h, not 128
+              umma_off<0, 0, false>(tmem, ud, hd, idesc_s, acc0);
+              umma_off<2, 2, false>(tmem, ud, hd, idesc_s, 1u);
+              umma_off<4, 256, false>(tmem, ud, hd, idesc_s, 1u);
+              umma_off<6, 258, false>(tmem, ud, hd, idesc_s, 1u);
+            } else {
+              umma_off<0, 0, false>(tmem, hd, ud, idesc, acc0);
+              umma_off<2, 2, false>(tmem, hd, ud, idesc, 1u);
+              umma_off<256, 4, false>(tmem, hd, ud, idesc, 1u);
+              umma_off<258, 6, false>(tmem, hd, ud, idesc, 1u);
+            }
+          }
+          __syncwarp();
         }
-        __syncwarp();
       }
       if (elect_one()) umma_commit(mdone);
       __syncwarp();
@@ -277,8 +369,21 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     if (tr && threadIdx.x == 0) tr[3] = gclock();
     tc_fence_after();
     if (threadIdx.x == 0 && t + 1 < T)  // next phase of every slice barrier (this step's phases are complete)
-      for (int c = 0; c < NS; ++c) mbar_expect_tx(&hfull[c], slice_bytes);
-    if (rd) {  // D row (32 sp + lane), columns [16 hf, +16) of each gate -> dsm[row][g*32 + col]
+      for (int g = 0; g < NG; ++g) mbar_expect_tx(&hfull[g], group_bytes);
+    if (swap) {  // D^T lane = gate row m (sub-partitions 0..2), column = batch row b -> dsm[b][m]
+      const int sub = warp & 3;
+      if (sub < 3) {
+        const int nh = NP / 2;
+        for (int cb = hf * nh; cb < hf * nh + nh; cb += 8) {
+          float d[8];
+          tmem_ld8(tmem + ((uint32_t)(sub * 32) << 16) + cb, d);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            if (cb + i < Bc) dsm[(cb + i) * kDP + sub * 32 + lane] = d[i];
+        }
+      }
+    } else if (rd) {  // D row (32 sp + lane), columns [16 hf, +16) of each gate -> dsm[row][g*32 + col]
       float d[16];
       const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16) + hf * 16;
       float* drow = dsm + (sp * 32 + lane) * kDP + hf * 16;
@@ -293,17 +398,14 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // done reading this step's h buffer
     named_sync(1, kThreads);
     if (tr && threadIdx.x == 0) tr[5] = gclock();
-    float dr[8], dz[8], dn[8];
+    float dr[UPT], dz[UPT], dn[UPT];
     if (row_ok) {
-      const float* drow = dsm + gb * kDP + gq * 8;
-      *(float4*)dr = *(const float4*)drow;
-      *(float4*)(dr + 4) = *(const float4*)(drow + 4);
-      *(float4*)dz = *(const float4*)(drow + 32);
-      *(float4*)(dz + 4) = *(const float4*)(drow + 36);
-      *(float4*)dn = *(const float4*)(drow + 64);
-      *(float4*)(dn + 4) = *(const float4*)(drow + 68);
+      const float* drow = dsm + gb * kDP + gq * UPT;
+      ldvs<UPT>(drow, dr);
+      ldvs<UPT>(drow + 32, dz);
+      ldvs<UPT>(drow + 64, dn);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < UPT; ++u) {
         dr[u] = sigm(gr[u] + dr[u] + cr[u]);            // r
         dz[u] = sigm(gz[u] + dz[u] + cz[u]);            // z
         dn[u] = dn[u] + cn[u];                          // a
@@ -311,27 +413,27 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
         h[u] = gn[u] - dz[u] * gn[u] + dz[u] * h[u];
       }
       if (tr && threadIdx.x == 0) tr[6] = gclock();
-      if (t + 1 < T) st8_bf16(p.hx + ((size_t)((t + 1) & 1) * B + gb) * H + ju, h);
+      if (t + 1 < T) stvb<UPT>(p.hx + ((size_t)((t + 1) & 1) * B + grow) * H + ju, h);
     }
     fence_proxy_async_global();  // this slice of h_{t+1} is read by this CTA's multicast (async proxy)
     named_sync(1, kThreads);
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA is done with h_t: buffers are free
     if (tr && threadIdx.x == 0) tr[7] = gclock();
     if (threadIdx.x == 0 && t + 1 < T)
-      tma_load_2d_mc(&tmH, &hfull[q], hsm + q * 4096, j0, ((t + 1) & 1) * B, all);
+      tma_load_2d_mc(&tmH, hbar, hsm + q * 4096, j0, ((t + 1) & 1) * B + b0, all);
     if (row_ok) {  // needed only by backward: off the critical path
-      st8(p.hs + ((size_t)(t + 1) * B + gb) * H + ju, h);
-      st8_bf16(p.hsb + ((size_t)(t + 1) * B + gb) * H + ju, h);
-      float* gs = p.gates + ((size_t)t * B + gb) * 4 * H + ju;
-      st8(gs, dr);
-      st8(gs + H, dz);
-      st8(gs + 2 * H, gn);
-      st8(gs + 3 * H, dn);
+      stv<UPT>(p.hs + ((size_t)(t + 1) * B + grow) * H + ju, h);
+      stvb<UPT>(p.hsb + ((size_t)(t + 1) * B + grow) * H + ju, h);
+      float* gs = p.gates + ((size_t)t * B + grow) * 4 * H + ju;
+      stv<UPT>(gs, dr);
+      stv<UPT>(gs + H, dz);
+      stv<UPT>(gs + 2 * H, gn);
+      stv<UPT>(gs + 3 * H, dn);
       if (t + 1 < T) {  // next step's input projections
-        const float* g3 = p.gx + ((size_t)(t + 1) * B + gb) * H3 + ju;
-        ld8(g3, gr);
-        ld8(g3 + H, gz);
-        ld8(g3 + 2 * H, gn);
+        const float* g3 = p.gx + ((size_t)(t + 1) * B + grow) * H3 + ju;
+        ldv<UPT>(g3, gr);
+        ldv<UPT>(g3 + H, gz);
+        ldv<UPT>(g3 + 2 * H, gn);
       }
     }
     if (tr && threadIdx.x == 0) tr[4] = gclock();
@@ -358,17 +460,21 @@ struct BwdArgs {
   float beta_b, beta_c;
   __nv_bfloat16* gex;  // [2][RG][B][KR] dgh exchange ring (bf16)
   float* pex;          // [2][CL][RG][B][32] partial-product ring
+  float* bpart;        // [clusters][4][H] per-cluster bias-gradient sums (nullptr: one cluster writes db / dc)
   int T, B, H, RG, CG;
+  int Bc;              // batch rows per cluster (see the forward)
 };
 
+template <int UPT>
 __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                  const __grid_constant__ CUtensorMap tmG,
                                                                  const BwdArgs p) {
   pdl_wait();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, RG = p.RG, CG = p.CG;
+  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, RG = p.RG, CG = p.CG, Bc = p.Bc;
   const int CL = RG * CG;
+  const int cid = (int)(blockIdx.x / CL), b0 = cid * Bc;  // batch group of this cluster
   const int NC = H / CG;            // column-group width (MMA N)
   const int KR = 3 * kUC * CG;      // gate rows of a row group (MMA K)
   const int NB = NC / 64;           // 64-column MN blocks of the U block
@@ -411,35 +517,37 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
           tma_load_2d(&tmU, ufull, ub + nb * KR * 128 + (jj * 3 + g) * kUC * 128, gj * NC + nb * 64,
                       g * H + jj * NC + gi * kUC);
   }
-  // phase A runs on all eight warps: thread -> batch row gb = tid / 4, units [8 gq, 8 gq + 8) of this CTA;
-  // phase B's TMEM readers are warps 0,1,4,5 (accumulator rows = batch rows live in sub-partitions 0 and 1)
+  // phase A runs on all eight warps: thread -> batch row gb = tid / TPR, units [UPT gq, UPT gq + UPT) of this
+  // CTA; phase B's TMEM readers are warps 0,1,4,5 (accumulator rows = batch rows live in sub-partitions 0 and 1)
+  constexpr int TPR = kUC / UPT;
   const bool epi = (warp & 2) == 0;
   const int sp = warp & 1, hf = warp >> 2;
   const int b = sp * 32 + lane;
-  const int gb = threadIdx.x >> 2, gq = threadIdx.x & 3;
-  const bool arow = gb < B;
-  const int ju = j0 + gq * 8;    // first global unit of this thread (phase A)
-  const int uo = gq * 8;         // its offset inside the CTA's 32 units
-  float dhz[8];                  // dh_{t+1} * z_{t+1} carried to the next (earlier) step
-  float cs[4][8];                // running column sums of dr', dz', dn', dn'*r (bias gradients db, dc)
+  const int gb = threadIdx.x / TPR, gq = threadIdx.x % TPR;
+  const bool arow = gb < Bc;
+  const size_t grow = (size_t)(b0 + gb);  // global batch row (phase A)
+  const int ju = j0 + gq * UPT;  // first global unit of this thread (phase A)
+  const int uo = gq * UPT;       // its offset inside the CTA's 32 units
+  float dhz[UPT];                // dh_{t+1} * z_{t+1} carried to the next (earlier) step
+  float cs[4][UPT];              // running column sums of dr', dz', dn', dn'*r (bias gradients db, dc)
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
+  for (int u = 0; u < UPT; ++u) {
     dhz[u] = 0.f;
     cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
   }
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
   // step t's external gradient, saved gates and h_t do not depend on the recurrence: they are loaded during step
   // t + 1's exchange and MMA phase, so only the partial products stay on the per-step critical path
-  float pdh[8], pr[8], pz[8], pn[8], pa[8], php[8];
+  float pdh[UPT], pr[UPT], pz[UPT], pn[UPT], pa[UPT], php[UPT];
   auto prefetch = [&](int tt) {
     if (!arow || tt < 0) return;
-    ld8(p.dhs + ((size_t)tt * B + gb) * H + ju, pdh);
-    const float* gs = p.gates + ((size_t)tt * B + gb) * 4 * H + ju;
-    ld8(gs, pr);
-    ld8(gs + H, pz);
-    ld8(gs + 2 * H, pn);
-    ld8(gs + 3 * H, pa);
-    ld8(p.hs + ((size_t)tt * B + gb) * H + ju, php);
+    ldv<UPT>(p.dhs + ((size_t)tt * B + grow) * H + ju, pdh);
+    const float* gs = p.gates + ((size_t)tt * B + grow) * 4 * H + ju;
+    ldv<UPT>(gs, pr);
+    ldv<UPT>(gs + H, pz);
+    ldv<UPT>(gs + 2 * H, pn);
+    ldv<UPT>(gs + 3 * H, pa);
+    ldv<UPT>(p.hs + ((size_t)tt * B + grow) * H + ju, php);
   };
   prefetch(T - 1);
   for (int t = T - 1; t >= 0; --t) {
@@ -448,22 +556,22 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
       cluster_wait();  // partial products of step t+1 visible
       tc_fence_after();
     }
-    float drp[8], dzp[8], dnp[8], dnr[8];
+    float drp[UPT], dzp[UPT], dnp[UPT], dnr[UPT];
     if (arow) {
-      float dh[8], v[8];
+      float dh[UPT], v[UPT];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dh[u] = pdh[u] + dhz[u];
+      for (int u = 0; u < UPT; ++u) dh[u] = pdh[u] + dhz[u];
       if (t < T - 1) {
-        const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + (size_t)gb * kUC + uo;
+        const float* pp = p.pex + ((size_t)(((t + 1) & 1) * CL + q) * RG) * B * kUC + grow * kUC + uo;
         for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
-          ld8(pp + (size_t)s * B * kUC, v);
+          ldv<UPT>(pp + (size_t)s * B * kUC, v);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) dh[u] += v[u];
+          for (int u = 0; u < UPT; ++u) dh[u] += v[u];
         }
       }
-      float r[8], z[8], n[8], a[8], hp[8];
+      float r[UPT], z[UPT], n[UPT], a[UPT], hp[UPT];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < UPT; ++u) {
         r[u] = pr[u];
         z[u] = pz[u];
         n[u] = pn[u];
@@ -471,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
         hp[u] = php[u];
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < UPT; ++u) {
         const float dn = dh[u] * (1.f - z[u]);
         const float dz = dh[u] * (hp[u] - n[u]);
         dnp[u] = dn * (1.f - n[u] * n[u]);
@@ -484,27 +592,27 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
         cs[2][u] += dnp[u];
         cs[3][u] += dnr[u];
       }
-      __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + gb) * KR + gj * 3 * kUC + uo;
-      st8_bf16(ge, drp);
-      st8_bf16(ge + kUC, dzp);
-      st8_bf16(ge + 2 * kUC, dnr);
+      __nv_bfloat16* ge = p.gex + ((size_t)((t & 1) * RG + gi) * B + grow) * KR + gj * 3 * kUC + uo;
+      stvb<UPT>(ge, drp);
+      stvb<UPT>(ge + kUC, dzp);
+      stvb<UPT>(ge + 2 * kUC, dnr);
     }
     fence_proxy_async_global();
     tc_fence_before();
     cluster_arrive();  // publish this step's dgh block; the fp32 copies below are only read after the kernel
     prefetch(t - 1);
     if (arow) {
-      __nv_bfloat16* gxo = p.dgx + ((size_t)t * B + gb) * H3 + ju;
-      __nv_bfloat16* gho = p.dgh + ((size_t)t * B + gb) * H3 + ju;
-      st8_bf16(gxo, drp);
-      st8_bf16(gxo + H, dzp);
-      st8_bf16(gxo + 2 * H, dnp);
-      st8_bf16(gho, drp);
-      st8_bf16(gho + H, dzp);
-      st8_bf16(gho + 2 * H, dnr);
+      __nv_bfloat16* gxo = p.dgx + ((size_t)t * B + grow) * H3 + ju;
+      __nv_bfloat16* gho = p.dgh + ((size_t)t * B + grow) * H3 + ju;
+      stvb<UPT>(gxo, drp);
+      stvb<UPT>(gxo + H, dzp);
+      stvb<UPT>(gxo + 2 * H, dnp);
+      stvb<UPT>(gho, drp);
+      stvb<UPT>(gho + H, dzp);
+      stvb<UPT>(gho + 2 * H, dnr);
       if (t == 0) {
         // dh0 = dh_0 * z_0 + (dgh_0 U)[own units], the partials of step 0 are added after the last barrier
-        st8(p.dh0 + (size_t)gb * H + ju, dhz);
+        stv<UPT>(p.dh0 + grow * H + ju, dhz);
       }
     }
     cluster_wait();  // every dgh block of step t is in the ring
@@ -514,8 +622,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     if ((warp & 2) && lane == 0) {  // four issuing threads (warps 2, 3, 6, 7)
       const int w4 = (warp & 1) | ((warp >> 1) & 2);
       for (int c = w4; c < NKC; c += 4) {
-        mbar_expect_tx(&gfull[c], (uint32_t)(B * 128));
-        tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B);
+        mbar_expect_tx(&gfull[c], (uint32_t)(Bc * 128));
+        tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B + b0);
       }
     }
     __syncwarp();
@@ -549,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
         tmem_ld16(ta + s * kUC, v0);
         tmem_ld16(ta + s * kUC + 16, v1);
         tmem_ld_wait();
-        if (b < B) {
+        if (b < Bc) {
           const int dest = s * CG + gj;
-          float* po = p.pex + ((size_t)((t & 1) * CL + dest) * RG + gi) * B * kUC + (size_t)b * kUC;
+          float* po = p.pex + ((size_t)((t & 1) * CL + dest) * RG + gi) * B * kUC + (size_t)(b0 + b) * kUC;
           st16(po, v0);
           st16(po + 16, v1);
         }
@@ -564,30 +672,33 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   tc_fence_after();
   // dh0 += the step-0 partial products of this CTA's units
   if (arow) {
-    float dh[8], v[8];
-    ld8(p.dh0 + (size_t)gb * H + ju, dh);
-    const float* pp = p.pex + ((size_t)q * RG) * B * kUC + (size_t)gb * kUC + uo;  // slot (0 & 1) = 0
+    float dh[UPT], v[UPT];
+    ldv<UPT>(p.dh0 + grow * H + ju, dh);
+    const float* pp = p.pex + ((size_t)q * RG) * B * kUC + grow * kUC + uo;  // slot (0 & 1) = 0
     for (int s = 0; s < RG; ++s) {
-      ld8(pp + (size_t)s * B * kUC, v);
+      ldv<UPT>(pp + (size_t)s * B * kUC, v);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) dh[u] += v[u];
+      for (int u = 0; u < UPT; ++u) dh[u] += v[u];
     }
-    st8(p.dh0 + (size_t)gb * H + ju, dh);
+    stv<UPT>(p.dh0 + grow * H + ju, dh);
   }
-  // bias gradients: the running column sums of the 64 batch rows, added in row order (deterministic); the
-  // dgh block ring in shared memory is free now
-  float* red = (float*)gsm;  // [64 rows][4 sums][32 units]
+  // bias gradients: the running column sums of the cluster's batch rows, added in row order (deterministic);
+  // the dgh block ring in shared memory is free now. Several clusters: per-cluster sums, folded in cluster
+  // order by gru_bias_fold_kernel
+  float* red = (float*)gsm;  // [Bc rows][4 sums][32 units]
   if (arow) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) st8(red + ((size_t)gb * 4 + k) * kUC + uo, cs[k]);
+    for (int k = 0; k < 4; ++k) stv<UPT>(red + ((size_t)gb * 4 + k) * kUC + uo, cs[k]);
   }
   __syncthreads();
   if (threadIdx.x < 4 * kUC) {
     const int k = threadIdx.x / kUC, u = threadIdx.x % kUC;
     float acc = 0.f;
-    for (int r = 0; r < B; ++r) acc += red[((size_t)r * 4 + k) * kUC + u];
+    for (int r = 0; r < Bc; ++r) acc += red[((size_t)r * 4 + k) * kUC + u];
     const int j = j0 + u;
-    if (k < 2) {  // r and z parts: dgx and dgh agree
+    if (p.bpart) {
+      p.bpart[((size_t)cid * 4 + k) * H + j] = acc;
+    } else if (k < 2) {  // r and z parts: dgx and dgh agree
       float* o1 = p.db + k * H + j;
       float* o2 = p.dc + k * H + j;
       *o1 = acc + p.beta_b * *o1;
@@ -623,18 +734,73 @@ int bwd_groups(int H, int* rg, int* cg) {
   return 1;
 }
 
+// bias gradients of several batch groups: the per-cluster sums added in cluster order (deterministic)
+__global__ void gru_bias_fold_kernel(const float* __restrict__ part, int groups, int H, float* db, float beta_b,
+                                     float* dc, float beta_c) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 4 * H) return;
+  const int k = i / H, j = i - k * H;
+  float acc = 0.f;
+  for (int c = 0; c < groups; ++c) acc += part[((size_t)c * 4 + k) * H + j];
+  if (k < 2) {  // r and z parts: dgx and dgh agree
+    db[k * H + j] = acc + beta_b * db[k * H + j];
+    dc[k * H + j] = acc + beta_c * dc[k * H + j];
+  } else if (k == 2) {
+    db[2 * H + j] = acc + beta_b * db[2 * H + j];
+  } else {
+    dc[2 * H + j] = acc + beta_c * dc[2 * H + j];
+  }
+}
+
+constexpr int kMaxGroups = 8;
+
 size_t fwd_smem(int H) { return 1024 + (size_t)(H / 64) * 12288 + (size_t)(H / kUC) * 4096 + 4096 + 64 * kDP * 4 + 256; }
 size_t bwd_smem(int H, int rg, int cg) {
   const int NB = H / cg / 64, KR = 3 * kUC * cg;
   return 1024 + (size_t)NB * KR * 128 + (size_t)(KR / 64) * 8192 + 8192 + 256;
 }
 
-int launch_cluster(const void* fn, int cl, size_t smem, void** args, cudaStream_t st) {
+int set_cluster_attrs(const void* fn, int cl, size_t smem) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess && cl > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return nsk::cuda_status(e, "gru_tc: cudaFuncSetAttribute");
+  return NSK_OK;
+}
+
+// Batch groups (independent clusters over B / groups rows each): the largest power of two <= NSK_GRU_GROUPS
+// (default 4) dividing B whose clusters can all be resident at once
+int batch_groups(const void* fn, int cl, size_t smem, int B) {
+  const char* e = getenv("NSK_GRU_GROUPS");
+  int want = e ? atoi(e) : 4;
+  if (want > kMaxGroups) want = kMaxGroups;
+  if (want < 2 || set_cluster_attrs(fn, cl, smem)) return 1;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cl);
+  cfg.gridDim = dim3(cl * want);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  for (int g = want; g > 1; g >>= 1)
+    if (B % g == 0 && g <= n) return g;
+  return 1;
+}
+
+int launch_cluster(const void* fn, int cl, int groups, size_t smem, void** args, cudaStream_t st) {
+  int rc = set_cluster_attrs(fn, cl, smem);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cl * groups);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -645,7 +811,7 @@ int launch_cluster(const void* fn, int cl, size_t smem, void** args, cudaStream_
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelExC(&cfg, fn, args);
+  cudaError_t e = cudaLaunchKernelExC(&cfg, fn, args);
   if (e != cudaSuccess) return nsk::cuda_status(e, "gru_tc: cluster launch");
   return NSK_OK;
 }
@@ -682,7 +848,8 @@ uint64_t nsk_gru_tc_workspace(int B, int H) {
   const uint64_t hx = 2ull * B * H * 2;                // forward ring
   const uint64_t gex = 2ull * rg * B * KR * 2;         // backward dgh ring
   const uint64_t pex = 2ull * CL * rg * B * kUC * 4;   // backward partial ring
-  return ((hx + 255) / 256 + (gex + 255) / 256) * 256 + pex;
+  const uint64_t bpart = (uint64_t)kMaxGroups * 4 * H * 4;  // per-cluster bias-gradient sums
+  return ((hx + 255) / 256 + (gex + 255) / 256 + (pex + 255) / 256) * 256 + bpart;
 }
 
 int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int B, int H, float* hs, void* hsb,
@@ -690,22 +857,33 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
   if (!nsk_gru_tc_supported(B, H) || T < 1)
     return nsk::set_error(NSK_ERR_UNSUPPORTED, "gru_tc: needs 1 <= B <= 64 and H in 128..512, H % 64 == 0");
   if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
+  const int CL = H / kUC;
+  const size_t smem = fwd_smem(H);
+  const int groups = batch_groups((const void*)gru_fwd_tc_kernel<8>, CL, smem, B);
+  const int Bc = B / groups;
+  const void* fn = Bc > 32 ? (const void*)gru_fwd_tc_kernel<8>
+                 : Bc > 16 ? (const void*)gru_fwd_tc_kernel<4>
+                 : Bc > 8  ? (const void*)gru_fwd_tc_kernel<2>
+                           : (const void*)gru_fwd_tc_kernel<1>;
   CUtensorMap tmU, tmH;
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
   __nv_bfloat16* hx = (__nv_bfloat16*)ws;
-  {  // h ring as 32-column (64-byte) boxes, 64B-swizzled: one box = one CTA's slice
+  {  // h ring as 32-column (64-byte) boxes of one batch group's rows, 64B-swizzled: one box = one CTA's slice
     const uint64_t dims[2] = {(uint64_t)H, (uint64_t)2 * B};
     const uint64_t str[1] = {(uint64_t)H * 2};
-    const uint32_t box[2] = {(uint32_t)kUC, (uint32_t)B};
+    const uint32_t box[2] = {(uint32_t)kUC, (uint32_t)Bc};
     if ((rc = nsk::encode_tmap(&tmH, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, hx, dims, str, box, nullptr,
                                CU_TENSOR_MAP_SWIZZLE_64B)))
       return rc;
   }
   if (getenv("NSK_GRU_TRACE") && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
-  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, T <= 4096 ? g_trace : nullptr};
+  int ng = getenv("NSK_GRU_NG") ? atoi(getenv("NSK_GRU_NG")) : 1;
+  if (ng < 1 || ng > CL / 2 || (CL / 2) % ng) ng = 1;
+  const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
+  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap, T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
-  return launch_cluster((const void*)gru_fwd_tc_kernel, H / kUC, fwd_smem(H), args, (cudaStream_t)stream);
+  return launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream);
 }
 
 int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const float* gates, int T, int B, int H,
@@ -716,19 +894,35 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   if (ws_bytes < nsk_gru_tc_workspace(B, H)) return nsk::set_error(NSK_ERR_SHAPE, "gru_tc: workspace too small");
   int rg, cg;
   bwd_groups(H, &rg, &cg);
-  const int KR = 3 * kUC * cg;
+  const int CL = H / kUC, KR = 3 * kUC * cg;
+  const size_t smem = bwd_smem(H, rg, cg);
+  const int groups = batch_groups((const void*)gru_bwd_tc_kernel<8>, CL, smem, B);
+  const int Bc = B / groups;
+  const void* fn = Bc > 32 ? (const void*)gru_bwd_tc_kernel<8>
+                 : Bc > 16 ? (const void*)gru_bwd_tc_kernel<4>
+                 : Bc > 8  ? (const void*)gru_bwd_tc_kernel<2>
+                           : (const void*)gru_bwd_tc_kernel<1>;
   uint8_t* w = (uint8_t*)ws;
   const uint64_t hx_bytes = ((2ull * B * H * 2 + 255) / 256) * 256;
+  const uint64_t gex_bytes = ((2ull * rg * B * KR * 2 + 255) / 256) * 256;
+  const uint64_t pex_bytes = ((2ull * CL * rg * B * kUC * 4 + 255) / 256) * 256;
   __nv_bfloat16* gex = (__nv_bfloat16*)(w + hx_bytes);
-  float* pex = (float*)(w + hx_bytes + ((2ull * rg * B * KR * 2 + 255) / 256) * 256);
+  float* pex = (float*)(w + hx_bytes + gex_bytes);
+  float* bpart = groups > 1 ? (float*)(w + hx_bytes + gex_bytes + pex_bytes) : nullptr;
   CUtensorMap tmU, tmG;
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
-  if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)B))) return rc;
+  if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)Bc))) return rc;
   BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
-            T, B, H, rg, cg};
+            bpart, T, B, H, rg, cg, Bc};
   void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
-  return launch_cluster((const void*)gru_bwd_tc_kernel, H / kUC, bwd_smem(H, rg, cg), args, (cudaStream_t)stream);
+  if ((rc = launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream))) return rc;
+  if (bpart) {
+    nsk::launch_pdl(gru_bias_fold_kernel, (4 * H + 255) / 256, 256, 0, (cudaStream_t)stream, (const float*)bpart,
+                    groups, H, db, beta_b, dc, beta_c);
+    NSK_LAUNCH_CHECK("gru_bias_fold_kernel");
+  }
+  return NSK_OK;
 }
 
 }  // extern "C"
