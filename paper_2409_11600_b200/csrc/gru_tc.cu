@@ -463,6 +463,8 @@ struct BwdArgs {
   float* bpart;        // [clusters][4][H] per-cluster bias-gradient sums (nullptr: one cluster writes db / dc)
   int T, B, H, RG, CG;
   int Bc;              // batch rows per cluster (see the forward)
+  int swap;            // 1: P^T = U^T dgh^T (M = the 128 columns of the column group, N = the batch rows)
+  long long* trace;    // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE=2)
 };
 
 template <int UPT>
@@ -483,8 +485,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   uint8_t* gsm = ub + NB * KR * 128;               // NKC x 8 KB (+8 KB slack)
   uint64_t* bars = (uint64_t*)(gsm + NKC * 8192 + 8192);
   uint64_t* ufull = bars;
-  uint64_t* gfull = bars + 1;                      // NKC
-  uint64_t* mdone = gfull + NKC;
+  uint64_t* gfull = bars + 1;                      // 1: the step's dgh block (four issuers arrive)
+  uint64_t* mdone = gfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   const int j0 = gj * NC + gi * kUC;               // first owned unit
   if (threadIdx.x == 0) {
     mbar_init(ufull, 1);
-    for (int c = 0; c < NKC; ++c) mbar_init(&gfull[c], 1);
+    mbar_init(gfull, 4);
     mbar_init(mdone, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmU);
@@ -536,6 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
   }
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
+  const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // swapped: MMA N (batch rows, rows past Bc unused)
+  const bool swap = p.swap != 0 && NC == 128;
+  const uint32_t idesc_s = make_idesc(1u, 1u, 0u, 128u, (uint32_t)NP);
   // step t's external gradient, saved gates and h_t do not depend on the recurrence: they are loaded during step
   // t + 1's exchange and MMA phase, so only the partial products stay on the per-step critical path
   float pdh[UPT], pr[UPT], pz[UPT], pn[UPT], pa[UPT], php[UPT];
@@ -551,11 +556,13 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   };
   prefetch(T - 1);
   for (int t = T - 1; t >= 0; --t) {
+    long long* tr = p.trace && b0 == 0 ? p.trace + ((size_t)q * T + (T - 1 - t)) * 16 : nullptr;
     // ---- A: dh_t for own units, gate derivatives, dgh block ----
     if (t < T - 1) {
       cluster_wait();  // partial products of step t+1 visible
       tc_fence_after();
     }
+    if (tr && threadIdx.x == 0) tr[0] = gclock();
     float drp[UPT], dzp[UPT], dnp[UPT], dnr[UPT];
     if (arow) {
       float dh[UPT], v[UPT];
@@ -599,6 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     }
     fence_proxy_async_global();
     tc_fence_before();
+    if (tr && threadIdx.x == 0) tr[1] = gclock();
     cluster_arrive();  // publish this step's dgh block; the fp32 copies below are only read after the kernel
     prefetch(t - 1);
     if (arow) {
@@ -617,36 +625,57 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
     }
     cluster_wait();  // every dgh block of step t is in the ring
     tc_fence_after();
+    if (tr && threadIdx.x == 0) tr[2] = gclock();
     // ---- B: P = dgh(row group) . U(row group rows, column group cols), slices to the column group ----
     fence_proxy_async_global();
-    if ((warp & 2) && lane == 0) {  // four issuing threads (warps 2, 3, 6, 7)
+    if ((warp & 2) && lane == 0) {  // four issuing threads (warps 2, 3, 6, 7), one barrier for the whole block
       const int w4 = (warp & 1) | ((warp >> 1) & 2);
-      for (int c = w4; c < NKC; c += 4) {
-        mbar_expect_tx(&gfull[c], (uint32_t)(Bc * 128));
-        tma_load_2d(&tmG, &gfull[c], gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B + b0);
-      }
+      mbar_expect_tx(gfull, (uint32_t)(((NKC - w4 + 3) / 4) * Bc * 128));
+      for (int c = w4; c < NKC; c += 4)
+        tma_load_2d(&tmG, gfull, gsm + c * 8192, c * 64, ((t & 1) * RG + gi) * B + b0);
     }
     __syncwarp();
-    if (warp == 2) {
-    } else if (warp == 3) {
+    if (warp == 3) {
       if (t == T - 1) mbar_wait(ufull, 0);
-      const uint32_t sg = smem_u32(gsm), su = smem_u32(ub);
-      const uint64_t bd0 = sdesc_sw128(su, (uint32_t)(KR * 128), 1024);
-      for (int c = 0; c < NKC; ++c) {
-        mbar_wait(&gfull[c], (T - 1 - t) & 1);
-        tc_fence_after();
-        const uint64_t ad = sdesc_sw128(sg + c * 8192, 16, 1024);
-        const uint64_t bd = bd0 + (uint64_t)((c * 64 * 128) >> 4);  // 64 K rows further
+      const uint64_t gd0 = sdesc_sw128(smem_u32(gsm), 16, 1024);
+      const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(KR * 128), 1024);
+      mbar_wait(gfull, (T - 1 - t) & 1);
+      if (tr && lane == 0) tr[3] = gclock();
+      tc_fence_after();
+      for (int c = 0; c < NKC; ++c) {  // chunk c: dgh + 8 KB, U + 64 K rows
+        const uint64_t gd = gd0 + (uint64_t)(c * 512), ud = ud0 + (uint64_t)(c * 512);
         if (elect_one()) {
-          umma_off<0, 0, false>(tmem, ad, bd, idesc, c > 0 ? 1u : 0u);
-          umma_off<2, 128, false>(tmem, ad, bd, idesc, 1u);
-          umma_off<4, 256, false>(tmem, ad, bd, idesc, 1u);
-          umma_off<6, 384, false>(tmem, ad, bd, idesc, 1u);
+          if (swap) {  // U block (MN-major) as A: the MMA reads Bc rows of dgh, not 128
+            umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
+            umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
+            umma_off<256, 4, false>(tmem, ud, gd, idesc_s, 1u);
+            umma_off<384, 6, false>(tmem, ud, gd, idesc_s, 1u);
+          } else {
+            umma_off<0, 0, false>(tmem, gd, ud, idesc, c > 0 ? 1u : 0u);
+            umma_off<2, 128, false>(tmem, gd, ud, idesc, 1u);
+            umma_off<4, 256, false>(tmem, gd, ud, idesc, 1u);
+            umma_off<6, 384, false>(tmem, gd, ud, idesc, 1u);
+          }
         }
         __syncwarp();
       }
       if (elect_one()) umma_commit(mdone);
       __syncwarp();
+    }
+    if (swap) {  // P^T lane = column n = 32 s + u (sub-partition s = the slice of row group s), column = batch row
+      mbar_wait_backoff(mdone, (T - 1 - t) & 1);
+      tc_fence_after();
+      if (tr && threadIdx.x == 0) tr[4] = gclock();
+      const int s = warp & 3, nh = NP / 2;
+      float* po = p.pex + ((size_t)((t & 1) * CL + s * CG + gj) * RG + gi) * B * kUC + (size_t)b0 * kUC + lane;
+      for (int cb = hf * nh; cb < hf * nh + nh; cb += 8) {
+        float d[8];
+        tmem_ld8(tmem + ((uint32_t)(s * 32) << 16) + cb, d);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (cb + i < Bc) po[(size_t)(cb + i) * kUC] = d[i];
+      }
     } else if (epi) {
       mbar_wait_backoff(mdone, (T - 1 - t) & 1);
       tc_fence_after();
@@ -666,6 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
       }
     }
     tc_fence_before();
+    if (tr && threadIdx.x == 0) tr[5] = gclock();
     cluster_arrive();  // partials of step t published (read in A of step t-1)
   }
   cluster_wait();
@@ -881,7 +911,9 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
   int ng = getenv("NSK_GRU_NG") ? atoi(getenv("NSK_GRU_NG")) : 1;
   if (ng < 1 || ng > CL / 2 || (CL / 2) % ng) ng = 1;
   const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
-  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap, T <= 4096 ? g_trace : nullptr};
+  const bool trace_fwd = getenv("NSK_GRU_TRACE") && getenv("NSK_GRU_TRACE")[0] != '2';
+  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap,
+            trace_fwd && T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
   return launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream);
 }
@@ -913,8 +945,11 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
   if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)Bc))) return rc;
+  const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
+  const char* tre = getenv("NSK_GRU_TRACE");
+  if (tre && tre[0] == '2' && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
   BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
-            bpart, T, B, H, rg, cg, Bc};
+            bpart, T, B, H, rg, cg, Bc, swap, tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
   if ((rc = launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream))) return rc;
   if (bpart) {
