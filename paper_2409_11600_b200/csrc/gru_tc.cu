@@ -747,6 +747,293 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   }
 }
 
+// Backward with DSMEM pushes (batch groups of Bc <= 32 rows, 128-column column groups): no global rings and no
+// cluster barriers inside the sweep. Per step
+//   A) wait for the RG partial-product blocks of step t+1 (pushed into this CTA's shared memory), form dh_t and the
+//      gate derivatives, stage this CTA's dgh piece (its 3 x 32 gate rows) directly in the MMA operand layout
+//      (K-major, 64-byte swizzle, one 32-wide K chunk per gate) and push it with one bulk copy into the dgh
+//      buffer of every CTA of its row group;
+//   B) once the row group's CG pieces have landed, 6 CG tcgen05.mma (U block as the MN-major A operand, M = the 128
+//      columns of the column group, N = the batch rows) and push each 32-column slice of P^T to its owner.
+// Every buffer is double-buffered by step parity. A buffer of step t is rewritten at step t-2 only after its
+// reader has consumed it: the producer of step t-2's data transitively needs, through the alternating
+// row-group / column-group dependencies, data that every reader produced after consuming step t -- so no barrier
+// guards the rewrite, and every re-arm of a receive barrier precedes the pushes it counts.
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void bulk_s2c(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   dst),
+               "r"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+struct PushLayout {  // byte sizes of the push kernel's shared-memory regions
+  int NB, KR, NK32, NP, CP, GSZ, PSZ;
+  __host__ __device__ PushLayout(int H, int CG, int Bc) {
+    NB = H / CG / 64;
+    KR = 3 * kUC * CG;
+    NK32 = KR / 32;
+    NP = Bc <= 16 ? 16 : 32;
+    CP = NP * 64;
+    GSZ = NK32 * CP;
+    PSZ = (H / CG / kUC) * Bc * 128;
+  }
+  __host__ __device__ size_t bytes() const {
+    return (size_t)NB * KR * 128 + 2 * (size_t)GSZ + 6 * (size_t)CP + 4 * (size_t)PSZ + 64;
+  }
+};
+
+template <int UPT>
+__global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_constant__ CUtensorMap tmU,
+                                                                   const BwdArgs p) {
+  pdl_wait();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
+  const int H = p.H, B = p.B, T = p.T, H3 = 3 * H, RG = p.RG, CG = p.CG, Bc = p.Bc;
+  const int CL = RG * CG;
+  const int cid = (int)(blockIdx.x / CL), b0 = cid * Bc;
+  const int NC = H / CG;  // 128 = RG slices of 32
+  const PushLayout L(H, CG, Bc);
+  uint8_t* ub = smem;                         // NB x (KR x 128 B): U block, MN-major
+  uint8_t* gsm = ub + L.NB * L.KR * 128;      // [2][GSZ]: the row group's dgh, NK32 chunks of NP rows x 64 B
+  uint8_t* gst = gsm + 2 * L.GSZ;             // [2][3 CP]: this CTA's dgh piece, staged in operand layout
+  uint8_t* prx = gst + 6 * L.CP;              // [2][PSZ]: received partial products, RG blocks of [Bc][32] fp32
+  uint8_t* pst = prx + 2 * L.PSZ;             // [2][PSZ]: outgoing P^T slices, [RG][Bc][32] fp32
+  uint64_t* bars = (uint64_t*)(pst + 2 * L.PSZ);
+  uint64_t* ufull = bars;
+  uint64_t* gfull = bars + 1;  // [2]
+  uint64_t* pfull = bars + 3;  // [2]
+  uint64_t* mdone = bars + 5;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 6);
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
+  const int q = (int)cluster_rank();
+  const int gi = q / CG, gj = q % CG;
+  const int j0 = gj * NC + gi * kUC;
+  const uint32_t gbytes = (uint32_t)(CG * 3 * L.CP), pbytes = (uint32_t)L.PSZ;
+  if (threadIdx.x == 0) {
+    mbar_init(ufull, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&gfull[i], 1);
+      mbar_init(&pfull[i], 1);
+    }
+    mbar_init(mdone, 1);
+    fence_mbar_init();
+    tma_prefetch_desc(&tmU);
+    for (int i = 0; i < 2; ++i) {  // the first use of each buffer
+      mbar_expect_tx(&gfull[i], gbytes);
+      mbar_expect_tx(&pfull[i], pbytes);
+    }
+  }
+  if (warp == 3) {
+    tmem_alloc(tmem_slot, 32);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 2 && elect_one()) {
+    mbar_expect_tx(ufull, (uint32_t)(L.NB * L.KR * 128));
+    for (int nb = 0; nb < L.NB; ++nb)
+      for (int jj = 0; jj < CG; ++jj)
+        for (int g = 0; g < 3; ++g)
+          tma_load_2d(&tmU, ufull, ub + nb * L.KR * 128 + (jj * 3 + g) * kUC * 128, gj * NC + nb * 64,
+                      g * H + jj * NC + gi * kUC);
+  }
+  cluster_sync_all();  // every CTA's receive barriers are initialised and armed before the first push
+
+  constexpr int TPR = kUC / UPT;
+  const int hf = warp >> 2;
+  const int gb = threadIdx.x / TPR, gq = threadIdx.x % TPR;
+  const bool arow = gb < Bc;
+  const size_t grow = (size_t)(b0 + gb);
+  const int ju = j0 + gq * UPT;
+  const int uo = gq * UPT;
+  // this thread's dgh values in the SW64 K-major chunk: row gb (64 B), 16-byte granule uo / 8 XOR (gb / 2) % 4
+  const uint32_t soff = (uint32_t)(gb * 64 + ((((uo >> 3) ^ ((gb >> 1) & 3))) << 4) + (uo & 7) * 2);
+  float dhz[UPT], cs[4][UPT];
+#pragma unroll
+  for (int u = 0; u < UPT; ++u) {
+    dhz[u] = 0.f;
+    cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
+  }
+  const uint32_t idesc_s = make_idesc(1u, 1u, 0u, 128u, (uint32_t)L.NP);
+  float pdh[UPT], pr[UPT], pz[UPT], pn[UPT], pa[UPT], php[UPT];
+  auto prefetch = [&](int tt) {
+    if (!arow || tt < 0) return;
+    ldv<UPT>(p.dhs + ((size_t)tt * B + grow) * H + ju, pdh);
+    const float* gs = p.gates + ((size_t)tt * B + grow) * 4 * H + ju;
+    ldv<UPT>(gs, pr);
+    ldv<UPT>(gs + H, pz);
+    ldv<UPT>(gs + 2 * H, pn);
+    ldv<UPT>(gs + 3 * H, pa);
+    ldv<UPT>(p.hs + ((size_t)tt * B + grow) * H + ju, php);
+  };
+  prefetch(T - 1);
+  for (int t = T - 1; t >= 0; --t) {
+    const int par = t & 1;
+    long long* tr = p.trace && b0 == 0 ? p.trace + ((size_t)q * T + (T - 1 - t)) * 16 : nullptr;
+    // ---- A ----
+    float dh[UPT];
+#pragma unroll
+    for (int u = 0; u < UPT; ++u) dh[u] = pdh[u] + dhz[u];
+    if (t < T - 1) {
+      const int pp = (t + 1) & 1;
+      mbar_wait(&pfull[pp], (uint32_t)(((T - 2 - t) >> 1) & 1));
+      if (threadIdx.x == 0 && t >= 1) mbar_expect_tx(&pfull[pp], pbytes);  // next: the partials of step t-1
+      if (arow) {
+        const float* src = (const float*)(prx + pp * L.PSZ) + (size_t)gb * kUC + uo;
+        for (int s = 0; s < RG; ++s) {  // fixed order over the row groups
+          float v[UPT];
+          ldvs<UPT>(src + (size_t)s * Bc * kUC, v);
+#pragma unroll
+          for (int u = 0; u < UPT; ++u) dh[u] += v[u];
+        }
+      }
+    }
+    if (tr && threadIdx.x == 0) tr[0] = gclock();
+    float drp[UPT], dzp[UPT], dnp[UPT], dnr[UPT];
+    uint8_t* stg = gst + par * 3 * L.CP;
+    if (arow) {
+#pragma unroll
+      for (int u = 0; u < UPT; ++u) {
+        const float dn = dh[u] * (1.f - pz[u]);
+        const float dz = dh[u] * (php[u] - pn[u]);
+        dnp[u] = dn * (1.f - pn[u] * pn[u]);
+        drp[u] = dnp[u] * pa[u] * pr[u] * (1.f - pr[u]);
+        dzp[u] = dz * pz[u] * (1.f - pz[u]);
+        dnr[u] = dnp[u] * pr[u];
+        dhz[u] = dh[u] * pz[u];
+        cs[0][u] += drp[u];
+        cs[1][u] += dzp[u];
+        cs[2][u] += dnp[u];
+        cs[3][u] += dnr[u];
+      }
+      stvb<UPT>((__nv_bfloat16*)(stg + soff), drp);
+      stvb<UPT>((__nv_bfloat16*)(stg + L.CP + soff), dzp);
+      stvb<UPT>((__nv_bfloat16*)(stg + 2 * L.CP + soff), dnr);
+    }
+    fence_proxy_async_smem();
+    named_sync(1, kThreads);
+    if (threadIdx.x == 0) {  // the piece (3 chunks, rows past Bc unused) into every CTA of the row group
+      if (tr) tr[1] = gclock();
+      const uint32_t dst = smem_u32(gsm + par * L.GSZ + gj * 3 * L.CP), bar = smem_u32(&gfull[par]);
+      for (int j = 0; j < CG; ++j) {
+        const uint32_t r = (uint32_t)(gi * CG + j);
+        bulk_s2c(mapa_u32(dst, r), smem_u32(stg), (uint32_t)(3 * L.CP), mapa_u32(bar, r));
+      }
+    }
+    prefetch(t - 1);
+    if (arow) {  // bf16 operands of the weight-gradient GEMMs and dh0: off the critical path
+      __nv_bfloat16* gxo = p.dgx + ((size_t)t * B + grow) * H3 + ju;
+      __nv_bfloat16* gho = p.dgh + ((size_t)t * B + grow) * H3 + ju;
+      stvb<UPT>(gxo, drp);
+      stvb<UPT>(gxo + H, dzp);
+      stvb<UPT>(gxo + 2 * H, dnp);
+      stvb<UPT>(gho, drp);
+      stvb<UPT>(gho + H, dzp);
+      stvb<UPT>(gho + 2 * H, dnr);
+      if (t == 0) stv<UPT>(p.dh0 + grow * H + ju, dhz);
+    }
+    // ---- B ----
+    if (warp == 3) {
+      if (t == T - 1) mbar_wait(ufull, 0);
+      if (tr && lane == 0) tr[2] = gclock();
+      mbar_wait(&gfull[par], (uint32_t)(((T - 1 - t) >> 1) & 1));
+      if (t >= 2 && elect_one()) mbar_expect_tx(&gfull[par], gbytes);  // next: the dgh of step t-2
+      __syncwarp();
+      if (tr && lane == 0) tr[3] = gclock();
+      tc_fence_after();
+      const uint64_t gd0 = sdesc_sw64(smem_u32(gsm + par * L.GSZ));
+      const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(L.KR * 128), 1024);
+      for (int c = 0; c < L.NK32; ++c) {  // chunk c: 32 gate rows (dgh + CP, U + 4 KB)
+        const uint64_t gd = gd0 + (uint64_t)(c * (L.CP >> 4)), ud = ud0 + (uint64_t)(c * 256);
+        if (elect_one()) {
+          umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
+          umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) umma_commit(mdone);
+      __syncwarp();
+    }
+    mbar_wait_backoff(mdone, (uint32_t)((T - 1 - t) & 1));
+    tc_fence_after();
+    if (tr && threadIdx.x == 0) tr[4] = gclock();
+    {  // P^T lane 32 s + u = unit u of slice s (owner: row group s of this column group), column = batch row
+      const int s = warp & 3, nh = L.NP / 2;
+      float* ps = (float*)(pst + par * L.PSZ) + (size_t)s * Bc * kUC;
+      const int r0 = hf * nh, r1 = r0 + nh < Bc ? r0 + nh : Bc;
+      for (int cb = r0; cb < r0 + nh; cb += 8) {
+        float d[8];
+        tmem_ld8(tmem + ((uint32_t)(s * 32) << 16) + cb, d);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (cb + i < Bc) ps[(size_t)(cb + i) * kUC + lane] = d[i];
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0 && r1 > r0) {
+        const uint32_t r = (uint32_t)(s * CG + gj);
+        const uint32_t dst = smem_u32(prx + par * L.PSZ) + (uint32_t)((gi * Bc + r0) * 128);
+        bulk_s2c(mapa_u32(dst, r), smem_u32(ps + (size_t)r0 * kUC), (uint32_t)((r1 - r0) * 128),
+                 mapa_u32(smem_u32(&pfull[par]), r));
+      }
+    }
+    if (tr && threadIdx.x == 0) tr[5] = gclock();
+  }
+  // dh0 += the step-0 partial products of this CTA's units
+  mbar_wait(&pfull[0], (uint32_t)(((T - 1) >> 1) & 1));
+  if (arow) {
+    float dh[UPT], v[UPT];
+    ldv<UPT>(p.dh0 + grow * H + ju, dh);
+    const float* src = (const float*)prx + (size_t)gb * kUC + uo;
+    for (int s = 0; s < RG; ++s) {
+      ldvs<UPT>(src + (size_t)s * Bc * kUC, v);
+#pragma unroll
+      for (int u = 0; u < UPT; ++u) dh[u] += v[u];
+    }
+    stv<UPT>(p.dh0 + grow * H + ju, dh);
+  }
+  // bias gradients as in gru_bwd_tc_kernel (the dgh buffers are free: every push into them was consumed)
+  float* red = (float*)gsm;  // [Bc rows][4 sums][32 units]
+  if (arow) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) stv<UPT>(red + ((size_t)gb * 4 + k) * kUC + uo, cs[k]);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4 * kUC) {
+    const int k = threadIdx.x / kUC, u = threadIdx.x % kUC;
+    float acc = 0.f;
+    for (int r = 0; r < Bc; ++r) acc += red[((size_t)r * 4 + k) * kUC + u];
+    const int j = j0 + u;
+    if (p.bpart) {
+      p.bpart[((size_t)cid * 4 + k) * H + j] = acc;
+    } else if (k < 2) {
+      p.db[k * H + j] = acc + p.beta_b * p.db[k * H + j];
+      p.dc[k * H + j] = acc + p.beta_c * p.dc[k * H + j];
+    } else if (k == 2) {
+      p.db[2 * H + j] = acc + p.beta_b * p.db[2 * H + j];
+    } else {
+      p.dc[2 * H + j] = acc + p.beta_c * p.dc[2 * H + j];
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while a push may still read its shared memory
+  if (warp == 3) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 32);
+  }
+}
+
 // backward arrangement: CG column groups x RG row groups of CL = H / 32 CTAs with NC = H / CG and KR = 96 CG
 // multiples of 64 (NSK_GRU_CG overrides the choice)
 int bwd_groups(int H, int* rg, int* cg) {
@@ -934,6 +1221,11 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
                  : Bc > 16 ? (const void*)gru_bwd_tc_kernel<4>
                  : Bc > 8  ? (const void*)gru_bwd_tc_kernel<2>
                            : (const void*)gru_bwd_tc_kernel<1>;
+  // DSMEM-push variant (no global rings, no per-step cluster barriers) where its buffers fit
+  const PushLayout PL(H, cg, Bc);
+  const size_t push_smem = 1024 + PL.bytes();
+  const bool push = Bc <= 32 && H / cg == 128 && push_smem <= 227 * 1024 &&
+                    !(getenv("NSK_GRU_PUSH") && getenv("NSK_GRU_PUSH")[0] == '0');
   uint8_t* w = (uint8_t*)ws;
   const uint64_t hx_bytes = ((2ull * B * H * 2 + 255) / 256) * 256;
   const uint64_t gex_bytes = ((2ull * rg * B * KR * 2 + 255) / 256) * 256;
@@ -950,8 +1242,17 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   if (tre && tre[0] == '2' && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
   BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
             bpart, T, B, H, rg, cg, Bc, swap, tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
-  void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
-  if ((rc = launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream))) return rc;
+  if (push) {
+    const void* pf = Bc > 16 ? (const void*)gru_bwd_push_kernel<4>
+                   : Bc > 8  ? (const void*)gru_bwd_push_kernel<2>
+                             : (const void*)gru_bwd_push_kernel<1>;
+    void* pargs[] = {(void*)&tmU, (void*)&a};
+    rc = launch_cluster(pf, CL, groups, push_smem, pargs, (cudaStream_t)stream);
+  } else {
+    void* args[] = {(void*)&tmU, (void*)&tmG, (void*)&a};
+    rc = launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream);
+  }
+  if (rc) return rc;
   if (bpart) {
     nsk::launch_pdl(gru_bias_fold_kernel, (4 * H + 255) / 256, 256, 0, (cudaStream_t)stream, (const float*)bpart,
                     groups, H, db, beta_b, dc, beta_c);
