@@ -107,6 +107,31 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* f) {
   for (int i = 0; i < 8; ++i) f[i] = __uint_as_float(r[i]);
 }
 
+// 32 lanes x 32 consecutive 32-bit columns from registers (thread t of the warp: lane base + t)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] . B[smem]: A (M = 128 lanes, K = 16 as 8 columns of packed bf16 pairs) read from tensor
+// memory, so only B comes from shared memory; BOFF is added to B's descriptor
+template <int BOFF>
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 bd;\n\tadd.s64 bd, %2, %5;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], bd, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum), "n"(BOFF)
+      : "memory");
+}
+
 __device__ __forceinline__ void ld16(const float* p, float* v) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) *(float4*)(v + 4 * i) = __ldcg((const float4*)(p + 4 * i));
@@ -207,6 +232,7 @@ struct FwdArgs {
   int Bc;            // batch rows per cluster (cluster k owns rows [k Bc, (k + 1) Bc))
   int NG;            // h-slice barrier groups: the MMA warp waits NG times per step (NS / NG slices each)
   int swap;          // 1: D^T = U h^T (M = the CTA's 96 gate rows, N = the Bc batch rows rounded up to 16)
+  int tmem_a;        // (swap) U copied once into tensor memory: the per-step MMAs read only h from shared memory
   long long* trace;  // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE), 8 per step
 };
 
@@ -281,8 +307,10 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     tma_prefetch_desc(&tmH);
     for (int g = 0; g < NG; ++g) mbar_expect_tx(&hfull[g], group_bytes);  // phase 0
   }
+  const bool tmem_a = p.swap != 0 && p.tmem_a != 0;
+  constexpr uint32_t kUCol = 256;  // tmem_a: U at columns [256, 256 + H/2), the accumulator at [0, NP)
   if (warp == 3) {
-    tmem_alloc(tmem_slot, 128);
+    tmem_alloc(tmem_slot, tmem_a ? 512 : 128);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -322,6 +350,29 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   tc_fence_before();
   cluster_sync_all();  // every CTA's mbarriers are initialised and its h0 slice is in the ring
   if (threadIdx.x == 0) tma_load_2d_mc(&tmH, hbar, hsm + q * 4096, j0, b0, all);
+  if (tmem_a) {  // U rows (gate row m = lane, rows 96..127 zero) from the 128B-swizzled chunks into TMEM, once
+    if (warp < 4) {
+      mbar_wait(ufull, 0);
+      const int m = warp * 32 + lane;
+      for (int c = 0; c < NCH; ++c) {  // 64 k = 32 packed columns per chunk
+        uint32_t w[32];
+#pragma unroll
+        for (int gr = 0; gr < 8; ++gr) {
+          const uint4 v = m < 3 * kUC ? *(const uint4*)(us + c * 12288 + m * 128 + ((gr ^ (m & 7)) << 4))
+                                      : make_uint4(0u, 0u, 0u, 0u);
+          w[gr * 4 + 0] = v.x;
+          w[gr * 4 + 1] = v.y;
+          w[gr * 4 + 2] = v.z;
+          w[gr * 4 + 3] = v.w;
+        }
+        tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + kUCol + c * 32, w);
+      }
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
   const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // swapped: MMA N (batch rows, rows past Bc unused)
@@ -346,7 +397,13 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
           const uint64_t hd = hd0 + (uint64_t)(k * 512), ud = ud0 + (uint64_t)(k * 768);
           const uint32_t acc0 = k > 0 ? 1u : 0u;
           if (elect_one()) {
-            if (swap) {  // U (resident, 128 B swizzle) is the A operand: the MMA reads Bc rows of h, not 128
+            if (tmem_a) {  // U from TMEM: k-steps 4k .. 4k+3 = 8 packed columns each
+              const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);
+              umma_ts<0>(tmem, ua, hd, idesc_s, acc0);
+              umma_ts<2>(tmem, ua + 8, hd, idesc_s, 1u);
+              umma_ts<256>(tmem, ua + 16, hd, idesc_s, 1u);
+              umma_ts<258>(tmem, ua + 24, hd, idesc_s, 1u);
+            } else if (swap) {  // U (resident, 128 B swizzle) is the A operand: the MMA reads Bc rows of h, not 128
               umma_off<0, 0, false>(tmem, ud, hd, idesc_s, acc0);
               umma_off<2, 2, false>(tmem, ud, hd, idesc_s, 1u);
               umma_off<4, 256, false>(tmem, ud, hd, idesc_s, 1u);
@@ -442,7 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   cluster_sync_all();  // no CTA leaves while a peer's multicast may still target it
   if (warp == 3) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, tmem_a ? 512 : 128);
   }
 }
 
@@ -1199,7 +1256,8 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
   if (ng < 1 || ng > CL / 2 || (CL / 2) % ng) ng = 1;
   const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
   const bool trace_fwd = getenv("NSK_GRU_TRACE") && getenv("NSK_GRU_TRACE")[0] != '2';
-  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap,
+  const int tma = getenv("NSK_GRU_TMEMA") ? atoi(getenv("NSK_GRU_TMEMA")) : 1;
+  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap, tma,
             trace_fwd && T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
   return launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream);
