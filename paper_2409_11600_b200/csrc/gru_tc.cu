@@ -521,6 +521,7 @@ struct BwdArgs {
   int T, B, H, RG, CG;
   int Bc;              // batch rows per cluster (see the forward)
   int swap;            // 1: P^T = U^T dgh^T (M = the 128 columns of the column group, N = the batch rows)
+  int tmem_a;          // (push kernel) the U block transposed once into tensor memory as the MMA A operand
   long long* trace;    // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE=2)
 };
 
@@ -887,8 +888,10 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       mbar_expect_tx(&pfull[i], pbytes);
     }
   }
+  const bool tmem_a = p.tmem_a != 0;
+  constexpr uint32_t kUCol = 64;  // tmem_a: U^T at columns [64, 64 + KR/2), the accumulator at [0, NP)
   if (warp == 3) {
-    tmem_alloc(tmem_slot, 32);
+    tmem_alloc(tmem_slot, tmem_a ? 256 : 32);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -904,6 +907,29 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
                       g * H + jj * NC + gi * kUC);
   }
   cluster_sync_all();  // every CTA's receive barriers are initialised and armed before the first push
+  if (tmem_a) {  // A[n][k] = U block[k][n]: lane n gathers its column (2 bytes per 128B-swizzled row), packs k pairs
+    if (warp < 4) {
+      mbar_wait(ufull, 0);
+      const int n = warp * 32 + lane;
+      const uint8_t* col = ub + (n >> 6) * L.KR * 128 + ((n & 7) << 1);
+      const int g0 = (n & 63) >> 3;
+      for (int c = 0; c < L.KR / 64; ++c) {  // 64 k = 32 packed columns
+        uint32_t w[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int k = c * 64 + 2 * i;  // k and k+1 share k / 8 (k even)
+          const uint32_t lo = *(const uint16_t*)(col + k * 128 + ((g0 ^ (k & 7)) << 4));
+          const uint32_t hi = *(const uint16_t*)(col + (k + 1) * 128 + ((g0 ^ ((k + 1) & 7)) << 4));
+          w[i] = lo | (hi << 16);
+        }
+        tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + kUCol + c * 32, w);
+      }
+      tmem_st_wait();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   constexpr int TPR = kUC / UPT;
   const int hf = warp >> 2;
@@ -921,6 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
     cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
   }
   const uint32_t idesc_s = make_idesc(1u, 1u, 0u, 128u, (uint32_t)L.NP);
+  const uint32_t idesc_t = make_idesc(1u, 0u, 0u, 128u, (uint32_t)L.NP);  // A from tensor memory (K-major)
   float pdh[UPT], pr[UPT], pz[UPT], pn[UPT], pa[UPT], php[UPT];
   auto prefetch = [&](int tt) {
     if (!arow || tt < 0) return;
@@ -1012,8 +1039,14 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       for (int c = 0; c < L.NK32; ++c) {  // chunk c: 32 gate rows (dgh + CP, U + 4 KB)
         const uint64_t gd = gd0 + (uint64_t)(c * (L.CP >> 4)), ud = ud0 + (uint64_t)(c * 256);
         if (elect_one()) {
-          umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
-          umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
+          if (tmem_a) {  // chunk c = 16 packed columns of U^T
+            const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);
+            umma_ts<0>(tmem, ua, gd, idesc_t, c > 0 ? 1u : 0u);
+            umma_ts<2>(tmem, ua + 8, gd, idesc_t, 1u);
+          } else {
+            umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
+            umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
+          }
         }
         __syncwarp();
       }
@@ -1087,7 +1120,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
   cluster_sync_all();  // no CTA leaves while a push may still read its shared memory
   if (warp == 3) {
     tc_fence_after();
-    tmem_dealloc(tmem, 32);
+    tmem_dealloc(tmem, tmem_a ? 256 : 32);
   }
 }
 
@@ -1299,7 +1332,8 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   const char* tre = getenv("NSK_GRU_TRACE");
   if (tre && tre[0] == '2' && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
   BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
-            bpart, T, B, H, rg, cg, Bc, swap, tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
+            bpart, T, B, H, rg, cg, Bc, swap, getenv("NSK_GRU_TMEMA") ? atoi(getenv("NSK_GRU_TMEMA")) : 1,
+            tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
   if (push) {
     const void* pf = Bc > 16 ? (const void*)gru_bwd_push_kernel<4>
                    : Bc > 8  ? (const void*)gru_bwd_push_kernel<2>
