@@ -1036,14 +1036,25 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       tc_fence_after();
       const uint64_t gd0 = sdesc_sw64(smem_u32(gsm + par * L.GSZ));
       const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(L.KR * 128), 1024);
-      for (int c = 0; c < L.NK32; ++c) {  // chunk c: 32 gate rows (dgh + CP, U + 4 KB)
+      const int cpd = L.CP >> 4;
+      for (int c = 0; tmem_a && c < L.NK32; c += 2) {  // two chunks (4 MMAs) per elected issue: c, c + 1
+        const uint64_t gd = gd0 + (uint64_t)(c * cpd), ge = gd + (uint64_t)cpd;
+        const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);  // chunk c = 16 packed columns of U^T
+        const bool two = c + 1 < L.NK32;                         // NK32 = 3 CG is odd for CG = 1
+        if (elect_one()) {
+          umma_ts<0>(tmem, ua, gd, idesc_t, c > 0 ? 1u : 0u);
+          umma_ts<2>(tmem, ua + 8, gd, idesc_t, 1u);
+          if (two) {
+            umma_ts<0>(tmem, ua + 16, ge, idesc_t, 1u);
+            umma_ts<2>(tmem, ua + 24, ge, idesc_t, 1u);
+          }
+        }
+        __syncwarp();
+      }
+      for (int c = 0; !tmem_a && c < L.NK32; ++c) {  // chunk c: 32 gate rows (dgh + CP, U + 4 KB)
         const uint64_t gd = gd0 + (uint64_t)(c * (L.CP >> 4)), ud = ud0 + (uint64_t)(c * 256);
         if (elect_one()) {
-          if (tmem_a) {  // chunk c = 16 packed columns of U^T
-            const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);
-            umma_ts<0>(tmem, ua, gd, idesc_t, c > 0 ? 1u : 0u);
-            umma_ts<2>(tmem, ua + 8, gd, idesc_t, 1u);
-          } else {
+          {
             umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
             umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
           }
