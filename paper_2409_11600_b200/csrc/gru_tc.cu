@@ -388,7 +388,30 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
       const uint64_t hd0 = sdesc_sw64(smem_u32(hsm));
       const uint64_t ud0 = sdesc_sw128(smem_u32(us), 16, 1024);
       const int GP = NS / 2 / NG;  // slice pairs per barrier group
-      for (int g = 0; g < NG; ++g) {
+      if (tmem_a && NG == 1) {  // U from TMEM, one barrier: 8 MMAs (two slice pairs) per elected issue
+        mbar_wait(&hfull[0], t & 1);
+        if (tr && lane == 0) tr[1] = tr[2] = gclock();
+        tc_fence_after();
+        for (int k = 0; k < NS / 2; k += 2) {
+          const uint64_t hd = hd0 + (uint64_t)(k * 512);
+          const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);  // k-steps 4k .. 4k+7, 8 packed columns each
+          const bool two = k + 1 < NS / 2;
+          if (elect_one()) {
+            umma_ts<0>(tmem, ua, hd, idesc_s, k > 0 ? 1u : 0u);
+            umma_ts<2>(tmem, ua + 8, hd, idesc_s, 1u);
+            umma_ts<256>(tmem, ua + 16, hd, idesc_s, 1u);
+            umma_ts<258>(tmem, ua + 24, hd, idesc_s, 1u);
+            if (two) {
+              umma_ts<512>(tmem, ua + 32, hd, idesc_s, 1u);
+              umma_ts<514>(tmem, ua + 40, hd, idesc_s, 1u);
+              umma_ts<768>(tmem, ua + 48, hd, idesc_s, 1u);
+              umma_ts<770>(tmem, ua + 56, hd, idesc_s, 1u);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      for (int g = 0; !(tmem_a && NG == 1) && g < NG; ++g) {
         mbar_wait(&hfull[g], t & 1);
         if (tr && lane == 0 && (g == 0 || g == NG - 1)) tr[g == 0 ? 1 : 2] = gclock();
         tc_fence_after();
@@ -1037,16 +1060,16 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       const uint64_t gd0 = sdesc_sw64(smem_u32(gsm + par * L.GSZ));
       const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(L.KR * 128), 1024);
       const int cpd = L.CP >> 4;
-      for (int c = 0; tmem_a && c < L.NK32; c += 2) {  // two chunks (4 MMAs) per elected issue: c, c + 1
-        const uint64_t gd = gd0 + (uint64_t)(c * cpd), ge = gd + (uint64_t)cpd;
+      for (int c = 0; tmem_a && c < L.NK32; c += 4) {  // four chunks (8 MMAs) per elected issue
         const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);  // chunk c = 16 packed columns of U^T
-        const bool two = c + 1 < L.NK32;                         // NK32 = 3 CG is odd for CG = 1
+        const int nc = L.NK32 - c < 4 ? L.NK32 - c : 4;         // NK32 = 3 CG
         if (elect_one()) {
-          umma_ts<0>(tmem, ua, gd, idesc_t, c > 0 ? 1u : 0u);
-          umma_ts<2>(tmem, ua + 8, gd, idesc_t, 1u);
-          if (two) {
-            umma_ts<0>(tmem, ua + 16, ge, idesc_t, 1u);
-            umma_ts<2>(tmem, ua + 24, ge, idesc_t, 1u);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i >= nc) break;
+            const uint64_t gd = gd0 + (uint64_t)((c + i) * cpd);
+            umma_ts<0>(tmem, ua + 16 * i, gd, idesc_t, c + i > 0 ? 1u : 0u);
+            umma_ts<2>(tmem, ua + 16 * i + 8, gd, idesc_t, 1u);
           }
         }
         __syncwarp();
