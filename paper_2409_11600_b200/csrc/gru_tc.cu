@@ -392,20 +392,20 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
         mbar_wait(&hfull[0], t & 1);
         if (tr && lane == 0) tr[1] = tr[2] = gclock();
         tc_fence_after();
-        for (int k = 0; k < NS / 2; k += 2) {
+        for (int k = 0; k < NS / 2; k += 4) {
           const uint64_t hd = hd0 + (uint64_t)(k * 512);
-          const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);  // k-steps 4k .. 4k+7, 8 packed columns each
-          const bool two = k + 1 < NS / 2;
+          const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);  // k-steps 4k .. 4k+15, 8 packed columns each
+          const int np = NS / 2 - k < 4 ? NS / 2 - k : 4;          // slice pairs in this issue
           if (elect_one()) {
-            umma_ts<0>(tmem, ua, hd, idesc_s, k > 0 ? 1u : 0u);
-            umma_ts<2>(tmem, ua + 8, hd, idesc_s, 1u);
-            umma_ts<256>(tmem, ua + 16, hd, idesc_s, 1u);
-            umma_ts<258>(tmem, ua + 24, hd, idesc_s, 1u);
-            if (two) {
-              umma_ts<512>(tmem, ua + 32, hd, idesc_s, 1u);
-              umma_ts<514>(tmem, ua + 40, hd, idesc_s, 1u);
-              umma_ts<768>(tmem, ua + 48, hd, idesc_s, 1u);
-              umma_ts<770>(tmem, ua + 56, hd, idesc_s, 1u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if (i >= np) break;
+              const uint64_t h2 = hd + (uint64_t)(i * 512);
+              const uint32_t u2 = ua + (uint32_t)(i * 32);
+              umma_ts<0>(tmem, u2, h2, idesc_s, k + i > 0 ? 1u : 0u);
+              umma_ts<2>(tmem, u2 + 8, h2, idesc_s, 1u);
+              umma_ts<256>(tmem, u2 + 16, h2, idesc_s, 1u);
+              umma_ts<258>(tmem, u2 + 24, h2, idesc_s, 1u);
             }
           }
           __syncwarp();
@@ -1060,12 +1060,12 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       const uint64_t gd0 = sdesc_sw64(smem_u32(gsm + par * L.GSZ));
       const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(L.KR * 128), 1024);
       const int cpd = L.CP >> 4;
-      for (int c = 0; tmem_a && c < L.NK32; c += 4) {  // four chunks (8 MMAs) per elected issue
+      for (int c = 0; tmem_a && c < L.NK32; c += 8) {  // eight chunks (16 MMAs) per elected issue
         const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);  // chunk c = 16 packed columns of U^T
-        const int nc = L.NK32 - c < 4 ? L.NK32 - c : 4;         // NK32 = 3 CG
+        const int nc = L.NK32 - c < 8 ? L.NK32 - c : 8;         // NK32 = 3 CG
         if (elect_one()) {
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int i = 0; i < 8; ++i) {
             if (i >= nc) break;
             const uint64_t gd = gd0 + (uint64_t)((c + i) * cpd);
             umma_ts<0>(tmem, ua + 16 * i, gd, idesc_t, c + i > 0 ? 1u : 0u);
