@@ -14,3 +14,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-co
     --log-file gpurun_out/${T}_launches_gru.csv python tools/probe_gru.py > /dev/null 2>&1
 python tools/ncu_summary.py gpurun_out/${T}_launches_gru.csv > gpurun_out/${T}_launches_gru_summary.txt 2>&1
 head -6 gpurun_out/${T}_launches_r18_summary.txt
+B=64 T=128 timeout 300 python tools/trace_gru.py > gpurun_out/${T}_gru_trace_fwd.txt 2>&1
+BWD=1 B=64 T=128 timeout 300 python tools/trace_gru.py > gpurun_out/${T}_gru_trace_bwd.txt 2>&1
+timeout 900 python bench.py --impl reference > gpurun_out/${T}_bench_reference.log 2>&1; tail -1 gpurun_out/${T}_bench_reference.log | cut -c1-300
