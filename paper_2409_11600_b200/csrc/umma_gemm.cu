@@ -1794,7 +1794,10 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   p.bx = nullptr;
   p.bmask = nullptr;
   p.bacc = 0;
-  if ((rc = dispatch_bn<2>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st))) return rc;
+  const bool staged = !(getenv("NSK_SPLIT_STAGED") && getenv("NSK_SPLIT_STAGED")[0] == '0');
+  if ((rc = staged ? dispatch_bn<2, 3>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st)
+                   : dispatch_bn<2>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st)))
+    return rc;
   const int CV = N / 8, RPB = kFoldThreads / CV;
   unsigned grid = (unsigned)((M + RPB - 1) / RPB);
   if (stats && grid > (unsigned)(2 * nsk::sm_count())) grid = 2 * nsk::sm_count();
