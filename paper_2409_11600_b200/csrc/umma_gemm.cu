@@ -687,18 +687,18 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
           }
           continue;
         }
-        if (p.bias) {
-#pragma unroll
-          for (int t = 0; t < 32; ++t)
-            if (col0 + t < p.N) f[t] += p.bias[col0 + t];
-        }
-        const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
         if constexpr (S::NSTG == 2 && STATS == 3) {
-          if (p.out_f32 && full_chunk && !p.tma_store) {
+          if (p.out_f32 && !p.tma_store && (col0 + 32 <= p.N) && vec_ok && !((uintptr_t)p.bias & 15)) {
             // fp32 through the warp's two staging buffers (32 x 32 floats, 16-byte granule g of row r at g ^ (r % 8):
             // conflict-free both ways), then 8 lanes per row: each store instruction covers 4 rows x 128 contiguous
-            // bytes instead of 32 rows x 16 bytes. A separate instantiation (STATS 3, fp32-output GEMMs): compiled
-            // into the conv kernels it raised them from 96 to 119 registers (ResNet-18 2.10 -> 2.14 ms/step)
+            // bytes instead of 32 rows x 16 bytes; lane owns columns 4 (lane % 8) .. +3, so the bias is one float4 per
+            // lane. A separate instantiation (STATS 3, fp32-output GEMMs and split-K partials): compiled into the
+            // conv kernels it raised them from 96 to 119 registers (ResNet-18 2.10 -> 2.14 ms/step)
+            const int part = lane & 7;
+            const float4 bv = p.bias ? __ldg((const float4*)(p.bias + col0) + part) : make_float4(0.f, 0.f, 0.f, 0.f);
+            // GEMM and split-K rows are linear in m: row pr of this warp's 32 sits pr * ldc after row 0
+            const long long ro0 = __shfl_sync(0xffffffffu, row_off, 0);
+            const int mrow0 = w.m0 + q * 32;
             float* sf = (float*)(stage_base + (warp - 4) * S::NSTG * kStgBytes);
             __syncwarp();  // the previous chunk's reads of the staging tile are done
 #pragma unroll
@@ -708,11 +708,14 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             __syncwarp();
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
-              const int pr = it * 4 + (lane >> 3), part = lane & 7;
-              const long long ro = __shfl_sync(0xffffffffu, row_off, pr);
-              const int ok = __shfl_sync(0xffffffffu, (int)row_ok, pr);
-              if (ok) {
+              const int pr = it * 4 + (lane >> 3);
+              const long long ro = ro0 + (long long)pr * p.ldc;
+              if (mrow0 + pr < p.M) {
                 float4 v = *(const float4*)(sf + pr * 32 + ((part ^ (pr & 7)) << 2));
+                v.x += bv.x;
+                v.y += bv.y;
+                v.z += bv.z;
+                v.w += bv.w;
                 float4* dst = (float4*)((float*)p.out + ro + col0 + part * 4);
                 if (p.beta != 0.f) {
                   const float4 o = *dst;
@@ -727,6 +730,12 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             continue;
           }
         }
+        if (p.bias) {
+#pragma unroll
+          for (int t = 0; t < 32; ++t)
+            if (col0 + t < p.N) f[t] += p.bias[col0 + t];
+        }
+        const bool full_chunk = (col0 + 32 <= p.N) && vec_ok;
         if (p.out_f32) {
           if (row_ok) {
             float* o = (float*)p.out + row_off + col0;
