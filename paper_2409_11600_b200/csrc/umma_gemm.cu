@@ -688,6 +688,37 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
           continue;
         }
         if constexpr (S::NSTG == 2 && STATS == 3) {
+          if (p.out_f32 && p.tma_store && (col0 + 32 <= p.N) && !((uintptr_t)p.bias & 15)) {
+            // beta = 0: the swizzled staging tile is the TMA store's source (SWIZZLE_128B map over [splits][M][N]
+            // fp32, so a ragged M tile clips inside its split)
+            if (p.bias) {
+#pragma unroll
+              for (int g = 0; g < 8; ++g) {
+                const float4 b4 = __ldg((const float4*)(p.bias + col0) + g);
+                f[4 * g] += b4.x;
+                f[4 * g + 1] += b4.y;
+                f[4 * g + 2] += b4.z;
+                f[4 * g + 3] += b4.w;
+              }
+            }
+            float* sf = (float*)(stage_base + (warp - 4) * S::NSTG * kStgBytes);
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous store read it
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < 8; ++g)
+              *(float4*)(sf + lane * 32 + ((g ^ (lane & 7)) << 2)) = make_float4(f[4 * g], f[4 * g + 1], f[4 * g + 2],
+                                                                                 f[4 * g + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+              asm volatile(
+                  "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(&tmC),
+                  "r"(smem_u32(sf)), "r"(col0), "r"(w.m0 + q * 32), "r"(p.k_per_split > 0 ? w.z : 0)
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            continue;
+          }
           if (p.out_f32 && !p.tma_store && (col0 + 32 <= p.N) && vec_ok && !((uintptr_t)p.bias & 15)) {
             // fp32 through the warp's two staging buffers (32 x 32 floats, 16-byte granule g of row r at g ^ (r % 8):
             // conflict-free both ways), then 8 lanes per row: each store instruction covers 4 rows x 128 contiguous
@@ -1574,7 +1605,10 @@ template <int ESZ, int STATS = 0>
 int dispatch_bn(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaProb p, int mt, int nt, int nz,
                 cudaStream_t st, int* grid_out = nullptr, const CUtensorMap* cmap = nullptr) {
   if constexpr (STATS == 3) {
-    if (p.rr || p.mc || BN != 256 || !p.out_f32) return dispatch_bn_main<ESZ, 0>(BN, a, b, p, mt, nt, nz, st, grid_out, cmap);
+    if (p.rr || p.mc || BN != 256 || !p.out_f32) {
+      if (p.out_f32) p.tma_store = 0;  // an fp32 store map is only read by this instantiation
+      return dispatch_bn_main<ESZ, 0>(BN, a, b, p, mt, nt, nz, st, grid_out, p.out_f32 ? nullptr : cmap);
+    }
     static CUtensorMap dummy{};
     const CUtensorMap& c = cmap ? *cmap : dummy;
     if (!cmap) p.tma_store = 0;
@@ -1711,6 +1745,18 @@ bool out_map(CUtensorMap* m, void* out, long long M, int N, long long ldc) {
                           CU_TENSOR_MAP_SWIZZLE_64B) == NSK_OK;  // matches the staging layout (stg_off)
 }
 
+// fp32 output (or split-K partials [splits][M][N]) for the staged STATS 3 epilogue: 32 x 32 boxes, 128-byte swizzle
+bool out_map_f32(CUtensorMap* m, void* out, long long M, int N, long long ldc, int splits) {
+  if ((ldc * 4) % 16 || ((uintptr_t)out & 15)) return false;
+  const char* env = getenv("NSK_TMA_STORE_F32");
+  if (env && env[0] == '0') return false;
+  uint64_t dims[3] = {(uint64_t)N, (uint64_t)M, (uint64_t)splits};
+  uint64_t str[2] = {(uint64_t)ldc * 4, (uint64_t)M * ldc * 4};
+  uint32_t box[3] = {32, 32, 1};
+  return nsk::encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, out, dims, str, box, nullptr,
+                          CU_TENSOR_MAP_SWIZZLE_128B) == NSK_OK;
+}
+
 bool force_i2c() {
   const char* env = getenv("NSK_CONV_I2C");
   return env && env[0] == '1';
@@ -1804,7 +1850,10 @@ int conv_split_run(UmmaProb p, const CUtensorMap& ma, const CUtensorMap& mb, int
   p.bmask = nullptr;
   p.bacc = 0;
   const bool staged = !(getenv("NSK_SPLIT_STAGED") && getenv("NSK_SPLIT_STAGED")[0] == '0');
-  if ((rc = staged ? dispatch_bn<2, 3>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st)
+  CUtensorMap mw;
+  const bool tw = staged && out_map_f32(&mw, ws, M, N, N, splits);
+  p.tma_store = tw;
+  if ((rc = staged ? dispatch_bn<2, 3>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st, nullptr, tw ? &mw : nullptr)
                    : dispatch_bn<2>(256, ma, mb, p, (M + 127) / 128, N / 256, splits, st)))
     return rc;
   const int CV = N / 8, RPB = kFoldThreads / CV;
@@ -1909,8 +1958,11 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
     p.out_f32 = 1;
     p.bias = nullptr;
     p.beta = 0.f;
-    rc = esz == 2 ? dispatch_bn<2, 3>(BN, ma, mb, p, mt, nt, splits, st)
-                  : dispatch_bn<4, 3>(BN, ma, mb, p, mt, nt, splits, st);
+    CUtensorMap mw;
+    const bool tw = out_map_f32(&mw, ws, M, N, N, splits);
+    p.tma_store = tw;
+    rc = esz == 2 ? dispatch_bn<2, 3>(BN, ma, mb, p, mt, nt, splits, st, nullptr, tw ? &mw : nullptr)
+                  : dispatch_bn<4, 3>(BN, ma, mb, p, mt, nt, splits, st, nullptr, tw ? &mw : nullptr);
     if (rc) return rc;
     const long long total = (long long)M * N;
     const bool vec = N % 4 == 0 && ldc % 4 == 0 && ((uintptr_t)C & 15) == 0 && (!bias || ((uintptr_t)bias & 15) == 0);
@@ -1924,7 +1976,7 @@ int nsk_gemm(int dtype, int a_mn, int b_mn, int M, int N, int K, const void* A, 
     return NSK_OK;
   }
   CUtensorMap mc;
-  const bool ts = !c_f32 && beta == 0.f && out_map(&mc, C, M, N, ldc);
+  const bool ts = beta == 0.f && (c_f32 ? out_map_f32(&mc, C, M, N, ldc, 1) : out_map(&mc, C, M, N, ldc));
   p.tma_store = ts;
   if (esz == 2) return dispatch_bn<2, 3>(BN, ma, mb, p, mt, nt, 1, st, nullptr, ts ? &mc : nullptr);
   return dispatch_bn<4, 3>(BN, ma, mb, p, mt, nt, 1, st, nullptr, ts ? &mc : nullptr);
