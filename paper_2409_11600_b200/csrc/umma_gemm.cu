@@ -281,7 +281,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
   uint64_t* tempty = tfull + NACC;   // [NACC] accumulator drained by the epilogue
   uint64_t* wfull = tempty + NACC;   // resident filter taps landed (WRES)
   uint32_t* tmem_slot = (uint32_t*)(wfull + 1);
-  uint8_t* stage_base = smem + S::STG_OFF;
+  // STATS 3 stages fp32 32 x 32 tiles for 128B-swizzled TMA stores: 1 KB aligned (the host adds 512 bytes)
+  uint8_t* stage_base = smem + (STATS == 3 ? (S::STG_OFF + 1023) / 1024 * 1024 : S::STG_OFF);
 
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform role index
   const int lane = threadIdx.x & 31;
@@ -690,7 +691,8 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
         if constexpr (S::NSTG == 2 && STATS == 3) {
           if (p.out_f32 && p.tma_store && (col0 + 32 <= p.N) && !((uintptr_t)p.bias & 15)) {
             // beta = 0: the swizzled staging tile is the TMA store's source (SWIZZLE_128B map over [splits][M][N]
-            // fp32, so a ragged M tile clips inside its split)
+            // fp32, so a ragged M tile clips inside its split). The hardware swizzle follows address bits 7-9: the
+            // tile starts on a 1 KB boundary (stage_base above)
             if (p.bias) {
 #pragma unroll
               for (int g = 0; g < 8; ++g) {
@@ -719,7 +721,7 @@ __global__ void __launch_bounds__(Launch<Smem<BN, ESZ, STAGES, RR, EPI, WRES>>::
             }
             continue;
           }
-          if (p.out_f32 && !p.tma_store && (col0 + 32 <= p.N) && vec_ok && !((uintptr_t)p.bias & 15)) {
+          if (p.out_f32 && (col0 + 32 <= p.N) && vec_ok && !((uintptr_t)p.bias & 15)) {
             // fp32 through the warp's two staging buffers (32 x 32 floats, 16-byte granule g of row r at g ^ (r % 8):
             // conflict-free both ways), then 8 lanes per row: each store instruction covers 4 rows x 128 contiguous
             // bytes instead of 32 rows x 16 bytes; lane owns columns 4 (lane % 8) .. +3, so the bias is one float4 per
@@ -1516,7 +1518,7 @@ int launch_umma(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c
                 int* grid_out) {
   using S = Smem<BN, ESZ, STAGES, RR, EPI, WRES>;
   auto kern = umma_kernel<BN, ESZ, STAGES, RR, EPI, WRES, STATS>;
-  const int smem = S::TOTAL + epi_extra_smem(p, EPI);
+  const int smem = S::TOTAL + epi_extra_smem(p, EPI) + (STATS == 3 ? 512 : 0);
   if (smem > 227 * 1024) return nsk::set_error(NSK_ERR_UNSUPPORTED, "umma: shared memory budget exceeded");
   static int configured = 0;
   if (smem > configured) {
