@@ -1,4 +1,4 @@
-// Fused GRU recurrence on the tensor cores (K16, tcgen05): one thread-block cluster walks all T steps.
+// Fused GRU recurrence on the tensor cores (K16, tcgen05): thread-block clusters walk all T steps.
 //
 // Reference: the reference has no GRU op; SURVEY.md A26 defines it as the composition of its primitives
 // (linear = matmul_t + bias-add, sigmoid, tanh, hadamard, add, neg, scalar-add: tensor.py:213-296,
@@ -8,30 +8,22 @@
 //   h' = n - z * n + z * h
 // gx = x W^T + b for all T steps is one tcgen05 GEMM on the host side; this file is the recurrence.
 //
-// Forward (one cluster of CL = H / 32 CTAs, CTA q owns hidden units [32q, 32q + 32)):
-//   * the CTA's 96 rows of U (r, z, n rows of its units) stay resident in shared memory (bf16, 128B-swizzled
-//     K-major, loaded once by TMA) -- the B operand of every step;
-//   * per step the full h_t (bf16, [B, H]) is TMA-loaded from a global exchange ring into shared memory (the A
-//     operand, K-major; M = 128 rows of which the first B are the batch -- rows past B are never read back);
-//   * one elected thread issues H/16 tcgen05.mma (M = 128, N = 96, K = 16) into TMEM: D[b][g*32 + u] = h U_g^T;
-//   * four epilogue warps read D with tcgen05.ld (thread = batch row), fuse the gate math in fp32 with the
-//     fp32 state h (kept in registers for the whole sequence), write h_{t+1} (fp32, and bf16 into the ring),
-//     the saved gates (r, z, n, a) for backward;
-//   * one hardware cluster barrier per step publishes h_{t+1} (release/acquire; the ring's other slot is the
-//     one being written, so a step never overwrites what a peer may still be loading).
+// Batch groups: rows of the batch never interact inside the recurrence, so B / Bc independent clusters of
+// CL = H / 32 CTAs each take Bc rows (4 groups of 16 at C3); CTA q of a cluster owns hidden units [32q, 32q + 32).
 //
-// Backward (BPTT, reverse sweep; the same cluster, arranged RG x CG):
+// Forward (gru_fwd_tc_kernel): the CTA's 96 rows of U live in tensor memory as the MMA's A operand; per step
+// 32 tcgen05.mma compute D^T = U_q h_t^T (N = the batch rows), all eight warps share the gate math through a
+// shared-memory tile, and each CTA's bf16 slice of h_{t+1} is TMA-multicast from a global ring into every CTA.
+//
+// Backward (BPTT, reverse sweep; the cluster arranged RG x CG):
 //   dh_{t-1} = dh_t * z_t + dgh_t U       (dgh = [dr', dz', dn' * r], the gradient w.r.t. h U^T + c)
-// CTA (i, j) owns units [j*H/CG + 32 i, +32); it keeps U[rows of row group i, cols of column group j] resident
-// (bf16, MN-major B operand), and per step:
-//   A) forms dh_t for its units from the partial products of step t+1, the gate derivatives (fp32), writes
-//      dgx / dgh (fp32, for the batched weight-gradient GEMMs) and its dgh block (bf16) into a global ring;
-//   -- cluster barrier --
-//   B) TMA-loads the dgh of its row group (K = 3*32*CG gate rows) and issues tcgen05.mma into TMEM:
-//      P[b][k] = sum over the row group's gate rows of dgh * U, k over its column group; the epilogue writes the
-//      slice of P that belongs to each CTA of the column group into a global partial ring;
-//   -- cluster barrier --
-// so each CTA exchanges 1/CG of dgh and 1/RG of the partial sums per step instead of the full dgh.
+// CTA (i, j) owns units [j*H/CG + 32 i, +32) and keeps U[rows of row group i, cols of column group j] (in tensor
+// memory, transposed: the A operand). Per step: A) form dh_t from the partial products of step t+1 and the gate
+// derivatives (fp32), write dgx / dgh for the batched weight-gradient GEMMs, and send this CTA's dgh piece to the
+// CTAs of its row group; B) P^T = U^T dgh^T over the row group's gate rows, each 32-column slice to its owner in the
+// column group. gru_bwd_push_kernel moves both exchanges by DSMEM bulk copies into double-buffered receive buffers
+// (no global rings, no barriers inside the sweep); gru_bwd_tc_kernel (rings in global memory, two split cluster
+// barriers per step) covers the shapes the push kernel's buffers do not fit.
 //
 // Precision: the MMA operands are bf16 (h, dgh, U), accumulation and all gate math / state fp32 (SURVEY.md
 // §7 hard part 5; oracle/restated.gru_*_bf16 emulates exactly these roundings).
@@ -219,8 +211,7 @@ __device__ __forceinline__ void st16_bf16(__nv_bfloat16* p, const float* v) {
 
 // ---------------------------------------------------------------------------------------------------------
 // forward
-// smem: [U rows: H/64 chunks x 96 rows x 128 B] [h: H/64 chunks x 64 rows x 128 B] [8 KB slack: M = 128 rows of
-// the last chunk] [mbarriers]
+// smem: [U rows: H/64 chunks x 96 rows x 128 B] [h: H/32 slices x 4 KB] [4 KB slack] [accumulator tile] [mbarriers]
 struct FwdArgs {
   const float* gx;   // [T][B][3H] (includes b)
   const float* c;    // [3H]
@@ -230,9 +221,6 @@ struct FwdArgs {
   __nv_bfloat16* hx; // [2][B][H] exchange ring
   int T, B, H;
   int Bc;            // batch rows per cluster (cluster k owns rows [k Bc, (k + 1) Bc))
-  int NG;            // h-slice barrier groups: the MMA warp waits NG times per step (NS / NG slices each)
-  int swap;          // 1: D^T = U h^T (M = the CTA's 96 gate rows, N = the Bc batch rows rounded up to 16)
-  int tmem_a;        // (swap) U copied once into tensor memory: the per-step MMAs read only h from shared memory
   long long* trace;  // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE), 8 per step
 };
 
@@ -263,14 +251,17 @@ __device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t*
       : "memory");
 }
 
-// Per step: every CTA writes its 32-unit slice of h_{t+1} (bf16) to the global ring and multicasts that slice --
-// one 64-row x 64-byte TMA box -- into all CTAs' h buffers, signalling their per-slice mbarriers; the MMA on
-// slice c starts as soon as it lands. The only cluster-wide barrier is split: each CTA arrives once its MMA has
-// finished reading h_t and waits right before its multicast overwrites the peers' h buffers, so its latency hides
-// behind the gate math.
-// Batch groups: the rows of the batch are independent through the recurrence, so the grid is B / Bc clusters,
-// each the full H / 32 CTAs (U resident in every cluster) over its own Bc rows. Each SM then receives Bc rows of
-// h per step instead of B: the multicast delivery into a CTA (~17 B/clk) is what bounds the exchange.
+// Batch groups: the rows of the batch are independent through the recurrence, so the grid is B / Bc clusters, each
+// the full H / 32 CTAs (U resident in every cluster) over its own Bc rows.
+// Per CTA (units [32q, 32q + 32)) and step:
+//   * D^T = U_q h^T: the CTA's 96 gate rows of U (copied once into tensor memory, packed bf16 pairs: the MMA's A
+//     operand, M = 128 lanes of which 96 are used) times h_t (bf16, the Bc batch rows as N, K-major in shared memory)
+//     -- 32 tcgen05.mma (K = 16) issued 16 per elected thread (the issue loop, not the tensor pipe, bounded it);
+//   * the accumulator (lane = gate row, column = batch row) goes through a shared-memory tile so all eight warps
+//     share the gate math (fp32, state h kept in registers);
+//   * each CTA writes its bf16 slice of h_{t+1} to a global ring and multicasts it (one TMA box) into every CTA's
+//     h buffer, all slices completing one mbarrier per step. A split cluster barrier protects the buffer: the
+//     arrive follows the MMAs' reads of h_t, the wait precedes the multicast (its latency hides behind the math).
 template <int UPT>  // hidden units per thread in the gate math: Bc <= 8 UPT rows x 32 / UPT threads per row
 __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmU,
                                                                  const __grid_constant__ CUtensorMap tmH,
@@ -282,35 +273,32 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   const int NCH = H / 64;                  // 64-wide K chunks of U
   const int NS = H / kUC;                  // 32-wide h slices = CTAs of the cluster
   const int b0 = (int)(blockIdx.x / NS) * Bc;  // first batch row of this cluster
-  uint8_t* us = smem;                      // NCH x 12 KB (SW128, B operand)
-  uint8_t* hsm = us + NCH * 12288;         // NS x 4 KB (SW64, A operand) + 4 KB slack (rows 64..127 of the last)
+  uint8_t* us = smem;                      // NCH x 12 KB (SW128): staging of U on its way into tensor memory
+  uint8_t* hsm = us + NCH * 12288;         // NS x 4 KB (SW64, B operand) + 4 KB slack
   float* dsm = (float*)(hsm + NS * 4096 + 4096);   // [64][kDP] accumulator tile for the gate math
   uint64_t* bars = (uint64_t*)(dsm + 64 * kDP);
-  uint64_t* ufull = bars;                  // 1
-  uint64_t* hfull = bars + 1;              // NG: one per group of NS / NG slices (producing CTAs)
-  uint64_t* mdone = hfull + NS;            // 1
-  uint32_t* tmem_slot = (uint32_t*)(mdone + 1);
+  uint64_t* ufull = bars;
+  uint64_t* hfull = bars + 1;              // every CTA's slice of h_t
+  uint64_t* mdone = bars + 2;
+  uint32_t* tmem_slot = (uint32_t*)(bars + 3);
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int q = (int)cluster_rank();
   const int j0 = q * kUC;
   const uint16_t all = (uint16_t)((1u << NS) - 1u);
-  const int NG = p.NG, GS = NS / NG;       // barrier groups, slices per group
-  const uint32_t group_bytes = (uint32_t)(GS * Bc * 64);
-  uint64_t* hbar = &hfull[q / GS];         // the barrier this CTA's slice completes (in every CTA)
+  const uint32_t hbytes = (uint32_t)(NS * Bc * 64);
   if (threadIdx.x == 0) {
     mbar_init(ufull, 1);
-    for (int g = 0; g < NG; ++g) mbar_init(&hfull[g], 1);
+    mbar_init(hfull, 1);
     mbar_init(mdone, 1);
     fence_mbar_init();
     tma_prefetch_desc(&tmU);
     tma_prefetch_desc(&tmH);
-    for (int g = 0; g < NG; ++g) mbar_expect_tx(&hfull[g], group_bytes);  // phase 0
+    mbar_expect_tx(hfull, hbytes);  // phase 0
   }
-  const bool tmem_a = p.swap != 0 && p.tmem_a != 0;
-  constexpr uint32_t kUCol = 256;  // tmem_a: U at columns [256, 256 + H/2), the accumulator at [0, NP)
+  constexpr uint32_t kUCol = 256;  // U at columns [256, 256 + H/2), the accumulator at [0, NP)
   if (warp == 3) {
-    tmem_alloc(tmem_slot, tmem_a ? 512 : 128);
+    tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -318,12 +306,9 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  // TMEM readers: warps 0,1,4,5 (sub-partitions 0 and 1 hold accumulator rows = batch rows 0..63); they copy D to a
-  // shared-memory tile so that ALL eight warps (all four schedulers) share the gate math: thread -> batch row
-  // gb = tid / TPR, units [UPT gq, UPT gq + UPT) of this CTA
+  // gate math: thread -> batch row gb = tid / TPR, units [UPT gq, UPT gq + UPT) of this CTA
   constexpr int TPR = kUC / UPT;  // threads per batch row
-  const bool rd = (warp & 2) == 0;
-  const int sp = warp & 1, hf = warp >> 2;
+  const int hf = warp >> 2;
   const int gb = threadIdx.x / TPR, gq = threadIdx.x % TPR;
   const bool row_ok = gb < Bc;
   const size_t grow = (size_t)(b0 + gb);  // global batch row
@@ -349,97 +334,56 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   fence_proxy_async_global();
   tc_fence_before();
   cluster_sync_all();  // every CTA's mbarriers are initialised and its h0 slice is in the ring
-  if (threadIdx.x == 0) tma_load_2d_mc(&tmH, hbar, hsm + q * 4096, j0, b0, all);
-  if (tmem_a) {  // U rows (gate row m = lane, rows 96..127 zero) from the 128B-swizzled chunks into TMEM, once
-    if (warp < 4) {
-      mbar_wait(ufull, 0);
-      const int m = warp * 32 + lane;
-      for (int c = 0; c < NCH; ++c) {  // 64 k = 32 packed columns per chunk
-        uint32_t w[32];
+  if (threadIdx.x == 0) tma_load_2d_mc(&tmH, hfull, hsm + q * 4096, j0, b0, all);
+  if (warp < 4) {  // U rows (gate row m = lane, rows 96..127 zero) from the 128B-swizzled chunks into TMEM, once
+    mbar_wait(ufull, 0);
+    const int m = warp * 32 + lane;
+    for (int c = 0; c < NCH; ++c) {  // 64 k = 32 packed columns per chunk
+      uint32_t w[32];
 #pragma unroll
-        for (int gr = 0; gr < 8; ++gr) {
-          const uint4 v = m < 3 * kUC ? *(const uint4*)(us + c * 12288 + m * 128 + ((gr ^ (m & 7)) << 4))
-                                      : make_uint4(0u, 0u, 0u, 0u);
-          w[gr * 4 + 0] = v.x;
-          w[gr * 4 + 1] = v.y;
-          w[gr * 4 + 2] = v.z;
-          w[gr * 4 + 3] = v.w;
-        }
-        tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + kUCol + c * 32, w);
+      for (int g8 = 0; g8 < 8; ++g8) {
+        const uint4 v = m < 3 * kUC ? *(const uint4*)(us + c * 12288 + m * 128 + ((g8 ^ (m & 7)) << 4))
+                                    : make_uint4(0u, 0u, 0u, 0u);
+        w[g8 * 4 + 0] = v.x;
+        w[g8 * 4 + 1] = v.y;
+        w[g8 * 4 + 2] = v.z;
+        w[g8 * 4 + 3] = v.w;
       }
-      tmem_st_wait();
+      tmem_st32(tmem + ((uint32_t)(warp * 32) << 16) + kUCol + c * 32, w);
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    tmem_st_wait();
   }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
-  const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, 96u);
-  const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // swapped: MMA N (batch rows, rows past Bc unused)
-  const uint32_t idesc_s = make_idesc(1u, 0u, 0u, 128u, (uint32_t)NP);
-  const bool swap = p.swap != 0;
+  const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // MMA N (batch rows, rows past Bc unused)
+  const uint32_t idesc = make_idesc(1u, 0u, 0u, 128u, (uint32_t)NP);
+  const uint64_t hd0 = sdesc_sw64(smem_u32(hsm));
   for (int t = 0; t < T; ++t) {
     long long* tr = p.trace && b0 == 0 ? p.trace + ((size_t)q * T + t) * 16 : nullptr;
     if (warp == 3) {
-      if (t == 0) mbar_wait(ufull, 0);
-      // Lean issue loop (it is the step's critical path): a wait by the MMA warp also waits for the queued MMAs'
-      // operand reads (~130 cycles), so few barrier groups; per pair of slices one U chunk (its two 64-byte
-      // halves), descriptors advanced by immediates. Slice c: h at + c * 4 KB, U chunk c / 2, half c & 1.
-      const uint64_t hd0 = sdesc_sw64(smem_u32(hsm));
-      const uint64_t ud0 = sdesc_sw128(smem_u32(us), 16, 1024);
-      const int GP = NS / 2 / NG;  // slice pairs per barrier group
-      if (tmem_a && NG == 1) {  // U from TMEM, one barrier: 8 MMAs (two slice pairs) per elected issue
-        mbar_wait(&hfull[0], t & 1);
-        if (tr && lane == 0) tr[1] = tr[2] = gclock();
-        tc_fence_after();
-        for (int k = 0; k < NS / 2; k += 4) {
-          const uint64_t hd = hd0 + (uint64_t)(k * 512);
-          const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);  // k-steps 4k .. 4k+15, 8 packed columns each
-          const int np = NS / 2 - k < 4 ? NS / 2 - k : 4;          // slice pairs in this issue
-          if (elect_one()) {
+      // slice pair k: h slices 2k, 2k + 1 (4 KB apart), U k-steps 4k .. 4k+3 (8 packed columns each)
+      mbar_wait(hfull, t & 1);
+      if (tr && lane == 0) tr[1] = tr[2] = gclock();
+      tc_fence_after();
+      for (int k = 0; k < NS / 2; k += 4) {
+        const uint64_t hd = hd0 + (uint64_t)(k * 512);
+        const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);
+        const int np = NS / 2 - k < 4 ? NS / 2 - k : 4;  // slice pairs in this issue
+        if (elect_one()) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (i >= np) break;
-              const uint64_t h2 = hd + (uint64_t)(i * 512);
-              const uint32_t u2 = ua + (uint32_t)(i * 32);
-              umma_ts<0>(tmem, u2, h2, idesc_s, k + i > 0 ? 1u : 0u);
-              umma_ts<2>(tmem, u2 + 8, h2, idesc_s, 1u);
-              umma_ts<256>(tmem, u2 + 16, h2, idesc_s, 1u);
-              umma_ts<258>(tmem, u2 + 24, h2, idesc_s, 1u);
-            }
+          for (int i = 0; i < 4; ++i) {
+            if (i >= np) break;
+            const uint64_t h2 = hd + (uint64_t)(i * 512);
+            const uint32_t u2 = ua + (uint32_t)(i * 32);
+            umma_ts<0>(tmem, u2, h2, idesc, k + i > 0 ? 1u : 0u);
+            umma_ts<2>(tmem, u2 + 8, h2, idesc, 1u);
+            umma_ts<256>(tmem, u2 + 16, h2, idesc, 1u);
+            umma_ts<258>(tmem, u2 + 24, h2, idesc, 1u);
           }
-          __syncwarp();
         }
-      }
-      for (int g = 0; !(tmem_a && NG == 1) && g < NG; ++g) {
-        mbar_wait(&hfull[g], t & 1);
-        if (tr && lane == 0 && (g == 0 || g == NG - 1)) tr[g == 0 ? 1 : 2] = gclock();
-        tc_fence_after();
-        for (int kk = 0; kk < GP; ++kk) {
-          const int k = g * GP + kk;
-          const uint64_t hd = hd0 + (uint64_t)(k * 512), ud = ud0 + (uint64_t)(k * 768);
-          const uint32_t acc0 = k > 0 ? 1u : 0u;
-          if (elect_one()) {
-            if (tmem_a) {  // U from TMEM: k-steps 4k .. 4k+3 = 8 packed columns each
-              const uint32_t ua = tmem + kUCol + (uint32_t)(k * 32);
-              umma_ts<0>(tmem, ua, hd, idesc_s, acc0);
-              umma_ts<2>(tmem, ua + 8, hd, idesc_s, 1u);
-              umma_ts<256>(tmem, ua + 16, hd, idesc_s, 1u);
-              umma_ts<258>(tmem, ua + 24, hd, idesc_s, 1u);
-            } else if (swap) {  // U (resident, 128 B swizzle) is the A operand: the MMA reads Bc rows of h, not 128
-              umma_off<0, 0, false>(tmem, ud, hd, idesc_s, acc0);
-              umma_off<2, 2, false>(tmem, ud, hd, idesc_s, 1u);
-              umma_off<4, 256, false>(tmem, ud, hd, idesc_s, 1u);
-              umma_off<6, 258, false>(tmem, ud, hd, idesc_s, 1u);
-            } else {
-              umma_off<0, 0, false>(tmem, hd, ud, idesc, acc0);
-              umma_off<2, 2, false>(tmem, hd, ud, idesc, 1u);
-              umma_off<256, 4, false>(tmem, hd, ud, idesc, 1u);
-              umma_off<258, 6, false>(tmem, hd, ud, idesc, 1u);
-            }
-          }
-          __syncwarp();
-        }
+        __syncwarp();
       }
       if (elect_one()) umma_commit(mdone);
       __syncwarp();
@@ -448,9 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     mbar_wait_backoff(mdone, t & 1);
     if (tr && threadIdx.x == 0) tr[3] = gclock();
     tc_fence_after();
-    if (threadIdx.x == 0 && t + 1 < T)  // next phase of every slice barrier (this step's phases are complete)
-      for (int g = 0; g < NG; ++g) mbar_expect_tx(&hfull[g], group_bytes);
-    if (swap) {  // D^T lane = gate row m (sub-partitions 0..2), column = batch row b -> dsm[b][m]
+    if (threadIdx.x == 0 && t + 1 < T) mbar_expect_tx(hfull, hbytes);  // next phase (this one is complete)
+    {  // D^T lane = gate row m (sub-partitions 0..2), column = batch row b -> dsm[b][m]
       const int sub = warp & 3;
       if (sub < 3) {
         const int nh = NP / 2;
@@ -462,16 +405,6 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
           for (int i = 0; i < 8; ++i)
             if (cb + i < Bc) dsm[(cb + i) * kDP + sub * 32 + lane] = d[i];
         }
-      }
-    } else if (rd) {  // D row (32 sp + lane), columns [16 hf, +16) of each gate -> dsm[row][g*32 + col]
-      float d[16];
-      const uint32_t ta = tmem + ((uint32_t)(sp * 32) << 16) + hf * 16;
-      float* drow = dsm + (sp * 32 + lane) * kDP + hf * 16;
-#pragma unroll
-      for (int g = 0; g < 3; ++g) {
-        tmem_ld16(ta + g * 32, d);
-        tmem_ld_wait();
-        st16(drow + g * 32, d);
       }
     }
     tc_fence_before();
@@ -500,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA is done with h_t: buffers are free
     if (tr && threadIdx.x == 0) tr[7] = gclock();
     if (threadIdx.x == 0 && t + 1 < T)
-      tma_load_2d_mc(&tmH, hbar, hsm + q * 4096, j0, ((t + 1) & 1) * B + b0, all);
+      tma_load_2d_mc(&tmH, hfull, hsm + q * 4096, j0, ((t + 1) & 1) * B + b0, all);
     if (row_ok) {  // needed only by backward: off the critical path
       stv<UPT>(p.hs + ((size_t)(t + 1) * B + grow) * H + ju, h);
       stvb<UPT>(p.hsb + ((size_t)(t + 1) * B + grow) * H + ju, h);
@@ -522,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_fwd_tc_kernel(const __grid_co
   cluster_sync_all();  // no CTA leaves while a peer's multicast may still target it
   if (warp == 3) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_a ? 512 : 128);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -543,8 +476,6 @@ struct BwdArgs {
   float* bpart;        // [clusters][4][H] per-cluster bias-gradient sums (nullptr: one cluster writes db / dc)
   int T, B, H, RG, CG;
   int Bc;              // batch rows per cluster (see the forward)
-  int swap;            // 1: P^T = U^T dgh^T (M = the 128 columns of the column group, N = the batch rows)
-  int tmem_a;          // (push kernel) the U block transposed once into tensor memory as the MMA A operand
   long long* trace;    // optional per-step timestamps of the first cluster's CTAs (NSK_GRU_TRACE=2)
 };
 
@@ -620,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_tc_kernel(const __grid_co
   }
   const uint32_t idesc = make_idesc(1u, 0u, 1u, 128u, (uint32_t)NC);
   const int NP = Bc <= 16 ? 16 : (Bc + 15) / 16 * 16;  // swapped: MMA N (batch rows, rows past Bc unused)
-  const bool swap = p.swap != 0 && NC == 128;
+  const bool swap = NC == 128;  // P^T = U^T dgh^T: M = the column group's 128 columns, N = the batch rows
   const uint32_t idesc_s = make_idesc(1u, 1u, 0u, 128u, (uint32_t)NP);
   // step t's external gradient, saved gates and h_t do not depend on the recurrence: they are loaded during step
   // t + 1's exchange and MMA phase, so only the partial products stay on the per-step critical path
@@ -911,10 +842,9 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       mbar_expect_tx(&pfull[i], pbytes);
     }
   }
-  const bool tmem_a = p.tmem_a != 0;
-  constexpr uint32_t kUCol = 64;  // tmem_a: U^T at columns [64, 64 + KR/2), the accumulator at [0, NP)
+  constexpr uint32_t kUCol = 64;  // U^T at columns [64, 64 + KR/2), the accumulator at [0, NP)
   if (warp == 3) {
-    tmem_alloc(tmem_slot, tmem_a ? 256 : 32);
+    tmem_alloc(tmem_slot, 256);
     tmem_relinquish();
   }
   tc_fence_before();
@@ -930,7 +860,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
                       g * H + jj * NC + gi * kUC);
   }
   cluster_sync_all();  // every CTA's receive barriers are initialised and armed before the first push
-  if (tmem_a) {  // A[n][k] = U block[k][n]: lane n gathers its column (2 bytes per 128B-swizzled row), packs k pairs
+  {  // A[n][k] = U block[k][n] into tensor memory: lane n gathers its column (2 bytes per 128B-swizzled row), packs
+     // k pairs; the per-step MMAs then read only the dgh block from shared memory
     if (warp < 4) {
       mbar_wait(ufull, 0);
       const int n = warp * 32 + lane;
@@ -969,7 +900,6 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
     dhz[u] = 0.f;
     cs[0][u] = cs[1][u] = cs[2][u] = cs[3][u] = 0.f;
   }
-  const uint32_t idesc_s = make_idesc(1u, 1u, 0u, 128u, (uint32_t)L.NP);
   const uint32_t idesc_t = make_idesc(1u, 0u, 0u, 128u, (uint32_t)L.NP);  // A from tensor memory (K-major)
   float pdh[UPT], pr[UPT], pz[UPT], pn[UPT], pa[UPT], php[UPT];
   auto prefetch = [&](int tt) {
@@ -1058,9 +988,8 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
       if (tr && lane == 0) tr[3] = gclock();
       tc_fence_after();
       const uint64_t gd0 = sdesc_sw64(smem_u32(gsm + par * L.GSZ));
-      const uint64_t ud0 = sdesc_sw128(smem_u32(ub), (uint32_t)(L.KR * 128), 1024);
       const int cpd = L.CP >> 4;
-      for (int c = 0; tmem_a && c < L.NK32; c += 8) {  // eight chunks (16 MMAs) per elected issue
+      for (int c = 0; c < L.NK32; c += 8) {  // eight chunks (16 MMAs) per elected issue
         const uint32_t ua = tmem + kUCol + (uint32_t)(c * 16);  // chunk c = 16 packed columns of U^T
         const int nc = L.NK32 - c < 8 ? L.NK32 - c : 8;         // NK32 = 3 CG
         if (elect_one()) {
@@ -1070,16 +999,6 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
             const uint64_t gd = gd0 + (uint64_t)((c + i) * cpd);
             umma_ts<0>(tmem, ua + 16 * i, gd, idesc_t, c + i > 0 ? 1u : 0u);
             umma_ts<2>(tmem, ua + 16 * i + 8, gd, idesc_t, 1u);
-          }
-        }
-        __syncwarp();
-      }
-      for (int c = 0; !tmem_a && c < L.NK32; ++c) {  // chunk c: 32 gate rows (dgh + CP, U + 4 KB)
-        const uint64_t gd = gd0 + (uint64_t)(c * (L.CP >> 4)), ud = ud0 + (uint64_t)(c * 256);
-        if (elect_one()) {
-          {
-            umma_off<0, 0, false>(tmem, ud, gd, idesc_s, c > 0 ? 1u : 0u);
-            umma_off<128, 2, false>(tmem, ud, gd, idesc_s, 1u);
           }
         }
         __syncwarp();
@@ -1154,7 +1073,7 @@ __global__ void __launch_bounds__(kThreads, 1) gru_bwd_push_kernel(const __grid_
   cluster_sync_all();  // no CTA leaves while a push may still read its shared memory
   if (warp == 3) {
     tc_fence_after();
-    tmem_dealloc(tmem, tmem_a ? 256 : 32);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -1319,13 +1238,8 @@ int nsk_gru_fwd_tc(const float* gx, const void* Ubf, const float* c, int T, int 
       return rc;
   }
   if (getenv("NSK_GRU_TRACE") && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
-  int ng = getenv("NSK_GRU_NG") ? atoi(getenv("NSK_GRU_NG")) : 1;
-  if (ng < 1 || ng > CL / 2 || (CL / 2) % ng) ng = 1;
-  const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
   const bool trace_fwd = getenv("NSK_GRU_TRACE") && getenv("NSK_GRU_TRACE")[0] != '2';
-  const int tma = getenv("NSK_GRU_TMEMA") ? atoi(getenv("NSK_GRU_TMEMA")) : 1;
-  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, ng, swap, tma,
-            trace_fwd && T <= 4096 ? g_trace : nullptr};
+  FwdArgs a{gx, c, hs, gates, (__nv_bfloat16*)hsb, hx, T, B, H, Bc, trace_fwd && T <= 4096 ? g_trace : nullptr};
   void* args[] = {(void*)&tmU, (void*)&tmH, (void*)&a};
   return launch_cluster(fn, CL, groups, smem, args, (cudaStream_t)stream);
 }
@@ -1362,12 +1276,10 @@ int nsk_gru_bwd_tc(const float* dhs, const void* Ubf, const float* hs, const flo
   int rc = tmap_2d_bf16(&tmU, Ubf, (uint64_t)3 * H, (uint64_t)H, kUC);
   if (rc) return rc;
   if ((rc = tmap_2d_bf16(&tmG, gex, (uint64_t)2 * rg * B, (uint64_t)KR, (uint32_t)Bc))) return rc;
-  const int swap = getenv("NSK_GRU_SWAP") ? atoi(getenv("NSK_GRU_SWAP")) : 1;
   const char* tre = getenv("NSK_GRU_TRACE");
   if (tre && tre[0] == '2' && !g_trace) cudaMalloc(&g_trace, (size_t)16 * 16 * 4096 * sizeof(long long));
   BwdArgs a{dhs, hs, gates, (__nv_bfloat16*)dgx, (__nv_bfloat16*)dgh, dh0, db, dc, beta_b, beta_c, gex, pex,
-            bpart, T, B, H, rg, cg, Bc, swap, getenv("NSK_GRU_TMEMA") ? atoi(getenv("NSK_GRU_TMEMA")) : 1,
-            tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
+            bpart, T, B, H, rg, cg, Bc, tre && tre[0] == '2' && T <= 4096 ? g_trace : nullptr};
   if (push) {
     const void* pf = Bc > 16 ? (const void*)gru_bwd_push_kernel<4>
                    : Bc > 8  ? (const void*)gru_bwd_push_kernel<2>
