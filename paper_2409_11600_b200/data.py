@@ -24,6 +24,7 @@ order the workers finish in.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import queue
 import threading
 
@@ -146,6 +147,48 @@ class ImageDataset:
         if self.world == 1:
             return rows
         return rows[self.rank * self.local_batch:(self.rank + 1) * self.local_batch]
+
+
+    @classmethod
+    def from_cifar_bin(cls, paths, batch_size: int, **kw) -> "ImageDataset":
+        """A uint8 dataset from CIFAR-10 binary batches (read_cifar_bin)."""
+        images, labels = read_cifar_bin(paths)
+        return cls(images, labels, batch_size, **kw)
+
+
+# ---- on-disk image format (SURVEY.md §8(f) item 2; the reference reads CSV only, dataset.py:48-90) ----
+CIFAR_RECORD = 1 + 3 * 32 * 32  # label byte, then the 1024 red, 1024 green and 1024 blue bytes (row-major 32x32)
+
+
+def read_cifar_bin(paths) -> tuple[np.ndarray, np.ndarray]:
+    """CIFAR-10 binary batches (``data_batch_*.bin`` / ``test_batch.bin``, memory-mapped) -> uint8 images
+    [N, 32, 32, 3] (NHWC: the layout the GPU crop/flip/normalise reads) and float32 labels, files concatenated in
+    the order given."""
+    if isinstance(paths, (str, os.PathLike)):
+        paths = [paths]
+    images, labels = [], []
+    for path in paths:
+        raw = np.memmap(path, dtype=np.uint8, mode="r")
+        if raw.size == 0 or raw.size % CIFAR_RECORD:
+            raise NskRuntimeError(f"{path}: {raw.size} bytes is not a whole number of {CIFAR_RECORD}-byte records")
+        rec = raw.reshape(-1, CIFAR_RECORD)
+        labels.append(rec[:, 0].astype(np.float32))
+        images.append(rec[:, 1:].reshape(-1, 3, 32, 32).transpose(0, 2, 3, 1))
+    return np.ascontiguousarray(np.concatenate(images)), np.concatenate(labels)
+
+
+def write_cifar_bin(path, images: np.ndarray, labels) -> None:
+    """The inverse of read_cifar_bin for one file: uint8 NHWC [N, 32, 32, 3] images and labels 0..255."""
+    images = np.asarray(images)
+    labels = np.asarray(labels)
+    if images.dtype != np.uint8 or images.shape[1:] != (32, 32, 3) or len(images) != len(labels):
+        raise NskRuntimeError("write_cifar_bin needs uint8 [N, 32, 32, 3] images and N labels")
+    if labels.min() < 0 or labels.max() > 255 or np.any(labels != np.round(labels)):
+        raise NskRuntimeError("CIFAR labels are single bytes")
+    rec = np.empty((len(images), CIFAR_RECORD), np.uint8)
+    rec[:, 0] = labels.astype(np.uint8)
+    rec[:, 1:] = images.transpose(0, 3, 1, 2).reshape(len(images), -1)
+    rec.tofile(path)
 
 
 def _draw_crop_flip(rng: np.random.Generator, n: int, pad: int) -> np.ndarray:

@@ -3,6 +3,7 @@
 reference), and the crop/flip draw is the oracle's (restated.draw_crop_flip)."""
 
 import numpy as np
+import pytest
 
 from oracle import ref_ops as R
 from oracle import restated as X
@@ -143,3 +144,31 @@ def test_reset_epoch_mid_epoch_with_full_ring_does_not_deadlock():
         np.testing.assert_array_equal(r, ld.ds.batch_rows(i))
     ld.shutdown()
     assert ld._free.qsize() == len(ld.slots)  # every slot back in the ring
+
+
+def test_cifar_binary_round_trip(tmp_path):
+    """On-disk format: CIFAR-10 binary records (label byte + R, G, B planes) read as uint8
+    NHWC images bit-exactly, files concatenated in order; malformed sizes raise the reference's runtime error."""
+    from paper_2409_11600_b200 import data
+    from paper_2409_11600_b200.errors import NskRuntimeError
+
+    rng = np.random.default_rng(3)
+    im1 = rng.integers(0, 256, (5, 32, 32, 3), dtype=np.uint8)
+    im2 = rng.integers(0, 256, (3, 32, 32, 3), dtype=np.uint8)
+    lb1, lb2 = rng.integers(0, 10, 5), rng.integers(0, 10, 3)
+    p1, p2 = tmp_path / "data_batch_1.bin", tmp_path / "data_batch_2.bin"
+    data.write_cifar_bin(p1, im1, lb1)
+    data.write_cifar_bin(p2, im2, lb2)
+    assert p1.stat().st_size == 5 * data.CIFAR_RECORD
+    raw = np.fromfile(p1, np.uint8).reshape(5, -1)  # the published layout: label, then the red plane row-major
+    assert raw[2, 0] == lb1[2] and raw[2, 1 + 7 * 32 + 9] == im1[2, 7, 9, 0] and raw[2, 1 + 1024 + 5] == im1[2, 0, 5, 1]
+    x, y = data.read_cifar_bin([p1, p2])
+    assert x.dtype == np.uint8 and x.shape == (8, 32, 32, 3) and x.flags["C_CONTIGUOUS"]
+    np.testing.assert_array_equal(x, np.concatenate([im1, im2]))
+    np.testing.assert_array_equal(y, np.concatenate([lb1, lb2]).astype(np.float32))
+    ds = data.ImageDataset.from_cifar_bin(str(p1), batch_size=2, seed=1)
+    assert ds.uint8 and ds.num_rows == 5 and ds.num_batches() == 3
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"\0" * (data.CIFAR_RECORD + 1))
+    with pytest.raises(NskRuntimeError):
+        data.read_cifar_bin(bad)

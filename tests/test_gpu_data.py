@@ -85,3 +85,30 @@ def test_loader_fed_graph_replay_matches_eager(dev):
         ld.shutdown()
     np.testing.assert_allclose(out[(True, 1)], out[(False, 1)], rtol=1e-5)
     assert len(out[(True, 3)]) == 6 and all(np.isfinite(out[(True, 3)]))
+
+
+def test_cifar_binary_file_feeds_the_loader(dev, tmp_path):
+    """CIFAR-10 binary batches on disk -> ImageDataset.from_cifar_bin -> pinned-ring loader -> GPU crop/flip ->
+    graphed ResNet-18 steps: the staged batch is the file's bytes, and training runs through it."""
+    from paper_2409_11600_b200 import _lib
+    from paper_2409_11600_b200.data import END_OF_DATA, DeviceLoader, ImageDataset, write_cifar_bin
+
+    imgs, labels = _u8_dataset(48)
+    write_cifar_bin(tmp_path / "data_batch_1.bin", imgs[:32], labels[:32])
+    write_cifar_bin(tmp_path / "data_batch_2.bin", imgs[32:], labels[32:])
+    ds = ImageDataset.from_cifar_bin([tmp_path / "data_batch_1.bin", tmp_path / "data_batch_2.bin"], 16, seed=4)
+    tr = _trainer(16, graph=True)
+    ld = DeviceLoader(ds, tr, workers=2)
+    ld.reset_epoch()
+    losses = []
+    for _ in range(ds.num_batches()):
+        idx = ld.next()
+        if idx is END_OF_DATA:
+            break
+        _lib.sync()
+        rows = ds.batch_rows(idx)
+        raw = tr.x_dev.buffer.host().view(np.uint8)[: imgs[rows].size].reshape(imgs[rows].shape)
+        np.testing.assert_array_equal(raw, imgs[rows])
+        losses.append(float(tr.run_staged()))
+    ld.shutdown()
+    assert len(losses) == 3 and all(np.isfinite(losses))
