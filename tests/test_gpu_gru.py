@@ -16,7 +16,11 @@ def rel(a, b):
 
 # (V, E, H, T, B): the first shape runs the fp32 cooperative recurrence (H = 64 is below the cluster kernel's
 # tiling), the others the tcgen05 cluster kernel (gru_tc.cu); the last is configuration C3 itself
-GRU_CASES = [(50, 64, 64, 6, 4), (1000, 128, 128, 32, 16), (4000, 256, 256, 24, 40), (32768, 512, 512, 128, 64)]
+# (V, E, H, T, B): H = 64 takes the fp32 cooperative kernels; the rest the tcgen05 clusters -- Bc = 4 / 10 / 16 /
+# 25 rows per batch group, H = 384 (12-CTA clusters: the forward's issue loop ends on a partial group, the backward
+# runs the global-ring kernel with 192-column groups), T = 1 (single-step barrier arming)
+GRU_CASES = [(50, 64, 64, 6, 4), (1000, 128, 128, 32, 16), (4000, 256, 256, 24, 40), (32768, 512, 512, 128, 64),
+             (2000, 128, 384, 16, 50), (100, 128, 128, 1, 8)]
 
 
 @pytest.mark.parametrize("V,E,H,T,B", GRU_CASES, ids=lambda v: str(v))
