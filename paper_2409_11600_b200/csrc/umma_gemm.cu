@@ -1586,15 +1586,18 @@ int dispatch_bn_main(int BN, const CUtensorMap& a, const CUtensorMap& b, UmmaPro
       // 8 epilogue warps unless the statistics buffers would not fit beside them
       using S8 = Smem<256, ESZ, 4, false, 8>;
       const int need = S8::TOTAL + epi_extra_smem(p, 8);
-      const bool epi8 = !(getenv("NSK_EPI8") && getenv("NSK_EPI8")[0] == '0');
+      // 8 epilogue warps pay on store-bound passes (large M, or short-K expands to >= 1024 channels: ResNet-50's
+      // 1x1 layers); the long-K ResNet-18 layers (M <= 16k) measured 0.9 % faster per step with 4. NSK_EPI8=0/1 forces
+      const char* e8 = getenv("NSK_EPI8");
+      const bool store_bound = p.M >= (1 << 15) || (p.k_steps <= 16 && p.N >= 1024);
+      const bool epi8 = e8 ? e8[0] != '0' : store_bound;
       if (need <= 227 * 1024 && epi8)
         return launch_umma<256, ESZ, 4, false, 8, false, STATS>(a, b, c, p, st, grid_out);
       if constexpr (STATS == 1) {
         // the statistics do not fit beside four stages: the store-bound layers (large M, or ResNet-50's short-K
         // 1x1 expands to >= 1024 channels) keep the 8-warp epilogue with three stages (R50 9.85k -> 10.24k
         // img/s); ResNet-18's small 8x8 layers measure 0.15 % faster on the deeper 4-warp ring
-        if (epi8 && (p.M >= (1 << 15) || (p.k_steps <= 16 && p.N >= 1024)) &&
-            !(getenv("NSK_STATS_S3") && getenv("NSK_STATS_S3")[0] == '0'))
+        if (epi8 && store_bound && !(getenv("NSK_STATS_S3") && getenv("NSK_STATS_S3")[0] == '0'))
           return launch_umma<256, ESZ, 3, false, 8, false, STATS>(a, b, c, p, st, grid_out);
       }
       return launch_umma<256, ESZ, 4, false, 4, false, STATS>(a, b, c, p, st, grid_out);
