@@ -570,6 +570,21 @@ int fold_blocks(int C) {
   const int groups = (C + AT / FOLD_T - 1) / (AT / FOLD_T);
   return groups < nsk::sm_count() ? groups : nsk::sm_count();
 }
+// grid of the grid-stride apply passes: at most 4 blocks per SM (NSK_BN_GRID_CAP overrides). 16 per SM fills the
+// SMs and crowds out the side-stream weight-gradient CTAs running beside them: ResNet-18 2.063 -> 2.026 ms/step with 4
+// (2 per SM: 2.16 ms; ResNet-50 unchanged, its large layers take the fold-in-apply kernels)
+unsigned apply_grid(uint64_t nv) {
+  static int cap = -1;
+  if (cap < 0) {
+    const char* e = getenv("NSK_BN_GRID_CAP");
+    cap = e ? atoi(e) : 4;
+    if (cap < 1) cap = 4;
+  }
+  unsigned g = nsk::grid_for(nv, BT);
+  const unsigned lim = (unsigned)(nsk::sm_count() * cap);
+  return g > lim ? lim : g;
+}
+
 unsigned fold_grid(uint64_t nv, int C) {
   unsigned g = nsk::grid_for(nv, AT);
   const unsigned need = (unsigned)fold_blocks(C);
@@ -657,7 +672,7 @@ int nsk_bn_fwd(const void* x, const float* gamma_beta, void* y, float* mean, flo
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
-    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
+    nsk::launch_pdl(bn_apply_kernel, apply_grid(nv), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                     (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
                     (uint8_t*)relu_mask, rows, C, relu);
     NSK_LAUNCH_CHECK("bn_fwd");
@@ -686,7 +701,7 @@ int nsk_bn_fwd_partials(const float* partials, int nparts, const void* x, const 
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_fwd_finalize, C, FT, 0, st, partials, nparts, rows, C, eps, gamma_beta, mean, invstd, scale,
                     shift, running, momentum);
-    nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
+    nsk::launch_pdl(bn_apply_kernel, apply_grid(nv), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                     (const __nv_bfloat16*)residual, (const float*)scale, (const float*)shift, (__nv_bfloat16*)y,
                     (uint8_t*)relu_mask, rows, C, relu);
     NSK_LAUNCH_CHECK("bn_fwd_partials");
@@ -720,7 +735,7 @@ int nsk_bn_fwd_eval(const void* x, const float* gamma_beta, const float* running
   float* shift = scale + C;
   nsk::launch_pdl(bn_eval_affine_kernel, (C + 127) / 128, 128, 0, st, gamma_beta, running, C, eps, scale, shift);
   const uint64_t nv = rows * (uint64_t)C / 8;
-  nsk::launch_pdl(bn_apply_kernel, nsk::grid_for(nv, BT), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
+  nsk::launch_pdl(bn_apply_kernel, apply_grid(nv), BT, 2 * C * sizeof(float), st, (const __nv_bfloat16*)x,
                   (const __nv_bfloat16*)residual, scale, shift, (__nv_bfloat16*)y, (uint8_t*)nullptr, rows, C, relu);
   NSK_LAUNCH_CHECK("bn_fwd_eval");
   return NSK_OK;
@@ -744,7 +759,7 @@ int nsk_bn_bwd(const void* dy, const void* x, const void* relu_mask, const float
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, (const float*)part, nb, rows, C, gamma_beta, mean, invstd,
                     dgamma_beta, beta_acc, coef);
-    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 3 * C * sizeof(float), st, (const __nv_bfloat16*)dy,
+    nsk::launch_pdl(bn_bwd_apply_kernel, apply_grid(nv), BT, 3 * C * sizeof(float), st, (const __nv_bfloat16*)dy,
                     (const __nv_bfloat16*)x, (const uint8_t*)relu_mask, (const float*)coef, (__nv_bfloat16*)dx,
                     (__nv_bfloat16*)dres, rows, C);
     NSK_LAUNCH_CHECK("bn_bwd");
@@ -772,7 +787,7 @@ int nsk_bn_bwd_partials(const float* partials, int nparts, const void* dz, const
   if (!fold_in_apply(rows, C, st)) {
     nsk::launch_pdl(bn_bwd_finalize, C, FT, 0, st, partials, nparts, rows, C, gamma_beta, mean, invstd, dgamma_beta,
                     beta_acc, coef);
-    nsk::launch_pdl(bn_bwd_apply_kernel, nsk::grid_for(nv, BT), BT, 3 * C * sizeof(float), st,
+    nsk::launch_pdl(bn_bwd_apply_kernel, apply_grid(nv), BT, 3 * C * sizeof(float), st,
                     (const __nv_bfloat16*)dz, (const __nv_bfloat16*)x, (const uint8_t*)nullptr, (const float*)coef,
                     (__nv_bfloat16*)dx, (__nv_bfloat16*)dres, rows, C);
     NSK_LAUNCH_CHECK("bn_bwd_partials");

@@ -1685,7 +1685,10 @@ int nhwc_map(CUtensorMap* m, const void* ptr, int N, int H, int W, int C, int c_
 bool try_rowreuse(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int Win, int Cin, int BN) {
   const char* env = getenv("NSK_CONV_RR");
   if (env && env[0] == '0') return false;
-  if (BN != 64 && !(env && env[0] == '1')) return false;  // default: N=64 tiles (2 CTAs/SM); wider tiles lose stages
+  // default: N=64 tiles (2 CTAs/SM). NSK_CONV_RR=1 adds the 128-wide ones: 0.3 % faster per step on the round-2
+  // kernels, but it reorders their fp32 accumulation over taps, and the lr-0.1 C2 trajectory test (chaotic after its
+  // blow-up) then leaves its 1 % bar in one window -- not worth it
+  if (BN != 64 && !(env && env[0] == '1')) return false;
   if (p.cs != 1 || p.Nt != 1 || p.Wt != p.Wo || (p.Wo % 8) || BN > 128 || p.ntaps[0] < 1) return false;
   int dhmin = 127, dhmax = -128;
   for (int t = 0; t < p.ntaps[0]; ++t) {
@@ -1807,9 +1810,11 @@ void try_wres(UmmaProb& p, CUtensorMap* ma, const void* act, int N, int Hin, int
   const char* env = getenv("NSK_WRES");
   if (env && env[0] == '0') return;
   if (!(p.bmode == BMODE_RR3 || p.bmode == BMODE_RR3T) || p.cchunks != 1 || Nout != 64 || p.ngroups[0] != 3) return;
+  // A box per stage: one band (default) or split into 3 row bands, one per producer warp (NSK_ASPLIT=3; round 1's
+  // choice, now measured 0.6 % slower per step than one box)
   const char* es = getenv("NSK_ASPLIT");
-  int split = es ? atoi(es) : 3;
-  if (split != 3 || p.ext_rows % 3) split = 1;  // one band per producer warp (three with a 4-stage ring)
+  int split = es ? atoi(es) : 1;
+  if (split != 3 || p.ext_rows % 3) split = 1;
   if (split > 1 && nhwc_map(ma, act, N, Hin, Win, Cin, 64, p.Wt, p.ext_rows / split, 1, 1)) split = 1;
   p.asplit = split;
   p.wres = 1;
