@@ -625,7 +625,13 @@ bool fold_in_apply(uint64_t rows, int C, cudaStream_t st) {
 int nblocks(uint64_t rows, int C) {
   const int RPB = BT / (C / 8);
   uint64_t want = (rows + RPB * 8 - 1) / (RPB * 8);  // >= 8 rows per thread
-  if (want > MAXBLK) want = MAXBLK;
+  static int cap = -1;  // NSK_BN_RED_BLK: blocks of the statistics passes (the workspace holds MAXBLK partials)
+  if (cap < 0) {
+    const char* e = getenv("NSK_BN_RED_BLK");
+    cap = e ? atoi(e) : MAXBLK;
+    if (cap < 1 || cap > MAXBLK) cap = MAXBLK;
+  }
+  if (want > (uint64_t)cap) want = cap;
   if (want < 1) want = 1;
   return (int)want;
 }
