@@ -240,10 +240,12 @@ uint64_t nsk_gru_bwd_workspace(int T, int B, int H);
 int nsk_gru_bwd(const float* dhs, const float* U, const float* hs, const float* gates, int T, int B, int H, float* dgx,
                 float* dgh, float* dh0, void* ws, uint64_t ws_bytes, void* stream);
 
-/* tensor-core GRU recurrence (gru_tc.cu): one thread-block cluster of H/32 CTAs for all T steps, U resident
- * in shared memory as bf16 (Ubf [3H, H] = the bf16 shadow of U), h / dgh exchanged per step through rings in
- * `ws` (nsk_gru_tc_workspace bytes), one tcgen05.mma chain per step, fp32 state and gate math. Same outputs as
- * nsk_gru_fwd / nsk_gru_bwd. Shapes: 1 <= B <= 64, H in 128..512 with H % 64 == 0 (nsk_gru_tc_supported). */
+/* tensor-core GRU recurrence (gru_tc.cu): per group of batch rows one thread-block cluster of H/32 CTAs walks all
+ * T steps (NSK_GRU_GROUPS, default 4 groups when they divide B and fit), U (Ubf [3H, H] = the bf16 shadow of U)
+ * copied once into each CTA's tensor memory, tcgen05.mma per step, fp32 state and gate math; h exchanged by TMA
+ * multicast from a ring in `ws`, the backward's pieces by DSMEM bulk copies (or rings in `ws` where those buffers
+ * do not fit). Same outputs as nsk_gru_fwd / nsk_gru_bwd (bias-gradient sums in a different fixed order).
+ * Shapes: 1 <= B <= 64, H in 128..512 with H % 64 == 0 (nsk_gru_tc_supported). */
 int nsk_gru_tc_supported(int B, int H);
 /* diagnostics: 16 globaltimer stamps per (CTA, step) of the last forward launched with NSK_GRU_TRACE=1 */
 int nsk_gru_trace(long long* out, int steps);
