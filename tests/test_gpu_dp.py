@@ -58,6 +58,39 @@ def test_dp_one_rank_nccl_captured_step_is_bit_identical(dev):
     assert sorted(dp.launch_log[:nb]) == list(range(nb))
 
 
+def test_dp_one_rank_nccl_adamw_clip_gru_step_is_bit_identical(dev):
+    """The AdamW + clip_grad_norm path under data parallelism (gradients scaled by 1/N before the norm is taken,
+    the update without the group scale) on the C3 model family through the tcgen05 GRU: one NCCL rank inside a
+    captured step equals the step without data parallelism bit for bit."""
+    from paper_2409_11600_b200 import _lib, nn
+    from paper_2409_11600_b200.dp import DataParallel
+    from paper_2409_11600_b200.models import GRUClassifier
+    from paper_2409_11600_b200.runtime import Session
+    from paper_2409_11600_b200.train import Trainer
+
+    rng = np.random.default_rng(6)
+    V, T, B = 1000, 16, 16
+    xs = [rng.integers(0, V, (B, T)).astype(np.float32) for _ in range(5)]
+    ys = [rng.integers(0, 2, B).astype(np.float32) for _ in range(5)]
+    runs = {}
+    for use_dp in (False, True):
+        s = Session(seed=0)
+        model = GRUClassifier(s, vocab=V, embed=128, hidden=128)
+        dp = None
+        if use_dp:
+            raw = (C.c_uint8 * 128)()
+            _lib.check(_lib.lib().nsk_comm_unique_id(raw))
+            dp = DataParallel(s, 0, 1, bucket_mb=1.0, uid=bytes(raw))
+        opt = ("adamw", nn.Hyperparams(learning_rate=1e-3, weight_decay=1e-4), 0.5)  # the clip engages
+        tr = Trainer(s, model, (B, T), 2, optimizer=opt, graph=True, warmup=2, dp=dp)
+        losses = [float(tr.step(x, y)) for x, y in zip(xs, ys)]
+        assert tr.graph is not None
+        runs[use_dp] = (losses, {n: t.data.copy() for n, t in s.param_group.params})
+    assert runs[True][0] == runs[False][0]
+    for n in runs[False][1]:
+        np.testing.assert_array_equal(runs[True][1][n], runs[False][1][n])
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
